@@ -1,0 +1,633 @@
+// obtree_capi.cu -- host side of the C ABI declared in include/obtree_b200.h.
+//
+// Owns model validation and packing (the ModelTables / build_leaf_bank step of the
+// reference, evaluate.py:138-166 and model.py:231-277), device residency, the
+// per-call launch plan (tile size, workspace) and kernel dispatch.  No CPU compute
+// path exists: if a kernel cannot run the call fails with an error code.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/obtree_b200.h"
+#include "obtree_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_error;
+thread_local int g_launches = 0;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_error = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                 \
+  do {                                                                                 \
+    cudaError_t err__ = (expr);                                                        \
+    if (err__ != cudaSuccess)                                                          \
+      return fail(OBT_E_CUDA, "%s failed: %s", #expr, cudaGetErrorString(err__));      \
+  } while (0)
+
+constexpr int kMaxBorders = 254;  // model.py:21
+constexpr int kMaxDepth = 12;     // smem-staged leaf tables (2^12 fp32 = 16 KiB per tree)
+constexpr int kSentinel = 255;    // evaluate.py:32
+
+// Instantiated depths of the apply kernel; a model of depth D runs on the
+// smallest instantiation >= D with sentinel (never-true) padding splits.
+int instantiated_depth(int d) {
+  if (d <= 8) return d < 1 ? 1 : d;
+  if (d <= 10) return 10;
+  if (d <= 12) return 12;
+  return -1;
+}
+
+struct ChunkSet {
+  uint8_t* d_chunks = nullptr;
+  int chunk_trees = 0;
+  int n_chunks = 0;
+  uint32_t chunk_bytes = 0;
+  uint32_t desc_bytes = 0;
+};
+
+}  // namespace
+
+struct obt_model {
+  int device = 0;
+  int n_features = 0, n_trees = 0, max_depth = 0, n_outputs = 1;
+  int depth_inst = 1;        // DI
+  int precision = OBT_PRECISION_BINARY64;
+  int leaf_storage = 1;      // 0 fp64, 1 fp32, 2 fp16
+  int compare_mode = 7;      // 7: all buckets < 128; 8: full byte compare
+  int levels = 0;            // Eytzinger levels
+  int eytz_pitch = 0;
+  double scale = 1.0, bias = 0.0;
+  float* d_eytz = nullptr;   // [F][eytz_pitch]
+  // host copies used to (re)build descriptor records for a tile size
+  std::vector<int32_t> split_feature;   // [T][DI]
+  std::vector<uint8_t> split_ordinal;   // [T][DI]
+  std::vector<uint8_t> leaf_bytes;      // [T][2^DI] in leaf_storage
+  // chunk geometry (independent of the tile size)
+  int chunk_trees = 1, n_chunks = 0;
+  uint32_t chunk_bytes = 128, desc_bytes = 0;
+  int sm_count = 148;
+  int smem_optin = 232448;
+  std::mutex mu;
+  std::map<int, ChunkSet> chunks_by_tile;
+  ~obt_model() {
+    for (auto& kv : chunks_by_tile) cudaFree(kv.second.d_chunks);
+    if (d_eytz) cudaFree(d_eytz);
+  }
+};
+
+namespace {
+
+size_t leaf_size(int storage) { return storage == 0 ? 8 : storage == 1 ? 4 : 2; }
+
+// binary64 -> binary16, round to nearest even (the numpy astype of model.py:263).
+uint16_t half_rne(double x) {
+  uint64_t bits;
+  std::memcpy(&bits, &x, 8);
+  const uint16_t sign = (uint16_t)((bits >> 48) & 0x8000u);
+  const int exp = (int)((bits >> 52) & 0x7FF);
+  const uint64_t man = bits & 0xFFFFFFFFFFFFFull;
+  if (exp == 0x7FF) return (uint16_t)(sign | (man ? 0x7E00u : 0x7C00u));
+  if (exp == 0) return sign;
+  const int e = exp - 1023;
+  if (e > 15) return (uint16_t)(sign | 0x7C00u);
+  const uint64_t sig = man | (1ull << 52);
+  const int shift = ((e < -14 ? -14 : e) - 10) - (e - 52);
+  uint64_t q = 0;
+  if (shift < 64) {
+    q = sig >> shift;
+    const uint64_t rem = sig & ((1ull << shift) - 1), half = 1ull << (shift - 1);
+    if (rem > half || (rem == half && (q & 1))) ++q;
+  }
+  if (e < -14) return (uint16_t)(sign | q);
+  int he = e;
+  if (q >= 2048) { q >>= 1; ++he; }
+  if (he > 15) return (uint16_t)(sign | 0x7C00u);
+  return (uint16_t)(sign | ((uint32_t)(he + 15) << 10) | (uint32_t)(q - 1024));
+}
+
+// saturation of finite overflow to +/-65504 (model.py:264-267)
+uint16_t half_bank_entry(double x) {
+  uint16_t h = half_rne(x);
+  if (std::isfinite(x) && (h & 0x7FFFu) == 0x7C00u) h = (uint16_t)((h & 0x8000u) | 0x7BFFu);
+  return h;
+}
+
+void eytzinger_fill(const float* sorted, int n, float* out, int pitch, int& pos, int node) {
+  // in-order walk of the implicit complete tree (children 2i+1, 2i+2)
+  if (node >= pitch) return;
+  eytzinger_fill(sorted, n, out, pitch, pos, 2 * node + 1);
+  out[node] = pos < n ? sorted[pos] : INFINITY;
+  ++pos;
+  eytzinger_fill(sorted, n, out, pitch, pos, 2 * node + 2);
+}
+
+int validate(const obt_model_desc* d) {
+  if (!d) return fail(OBT_E_INVALID, "invalid model: null description");
+  if (d->n_features < 1) return fail(OBT_E_INVALID, "invalid model: model: at least one float feature is required");
+  if (d->n_trees < 0) return fail(OBT_E_INVALID, "invalid model: negative tree count");
+  if (d->n_outputs != 1)
+    return fail(OBT_E_UNSUPPORTED, "n_outputs=%d: multi-output leaves are not implemented by this build", d->n_outputs);
+  if (d->n_trees > 0 && (d->max_depth < 1 || d->max_depth > 16))
+    return fail(OBT_E_INVALID, "invalid model: max_depth %d outside 1..16", d->max_depth);
+  if (d->n_trees > 0 && instantiated_depth(d->max_depth) < 0)
+    return fail(OBT_E_UNSUPPORTED, "depth %d exceeds the %d supported by the apply kernel", d->max_depth, kMaxDepth);
+  if (!d->border_counts || !d->borders) return fail(OBT_E_INVALID, "invalid model: missing borders");
+  if (d->precision != OBT_PRECISION_BINARY64 && d->precision != OBT_PRECISION_BINARY16)
+    return fail(OBT_E_INVALID, "unknown precision %d", d->precision);
+  for (int f = 0; f < d->n_features; ++f) {
+    const int nb = d->border_counts[f];
+    if (nb < 0 || nb > kMaxBorders || nb > d->border_stride)
+      return fail(OBT_E_INVALID, "invalid model: float_features[%d]: %d borders exceed the limit of %d", f, nb, kMaxBorders);
+    const float* b = d->borders + (size_t)f * d->border_stride;
+    for (int k = 0; k < nb; ++k) {
+      if (std::isnan(b[k])) return fail(OBT_E_INVALID, "invalid model: float_features[%d]: NaN border", f);
+      if (k > 0 && !(b[k] > b[k - 1])) return fail(OBT_E_INVALID, "invalid model: float_features[%d]: non-ascending borders", f);
+    }
+  }
+  if (d->n_trees > 0) {
+    if (!d->split_feature || !d->split_ordinal || !d->leaves)
+      return fail(OBT_E_INVALID, "invalid model: missing tree arrays");
+    const int D = d->max_depth;
+    for (int t = 0; t < d->n_trees; ++t) {
+      for (int s = 0; s < D; ++s) {
+        const int f = d->split_feature[(size_t)t * D + s];
+        const int ord = d->split_ordinal[(size_t)t * D + s];
+        if (ord == kSentinel) continue;
+        if (f < 0 || f >= d->n_features)
+          return fail(OBT_E_INVALID, "invalid model: trees[%d].splits[%d]: feature index %d out of range", t, s, f);
+        if (ord >= d->border_counts[f])
+          return fail(OBT_E_INVALID,
+                      "invalid model: trees[%d].splits[%d]: border ordinal out of range (%d vs %d borders on feature %d)",
+                      t, s, ord, d->border_counts[f], f);
+      }
+      const double* lv = d->leaves + ((size_t)t << D);
+      for (size_t j = 0; j < ((size_t)1 << D); ++j)
+        if (std::isnan(lv[j])) return fail(OBT_E_INVALID, "invalid model: trees[%d]: NaN leaf value", t);
+    }
+  }
+  return OBT_OK;
+}
+
+// Chunk geometry: trees per record sized so one record is ~12 KiB (the ring holds
+// kStages of them next to the bucket tile).
+void plan_chunks(obt_model* m) {
+  const int DI = m->depth_inst;
+  const size_t per_tree_desc = (size_t)obt::desc_bytes_per_tree(DI, m->compare_mode);
+  const size_t per_tree = per_tree_desc + (leaf_size(m->leaf_storage) << DI);
+  int ct = (int)std::max<size_t>(1, (12 * 1024) / per_tree);
+  ct = std::min(ct, 64);
+  if (m->n_trees > 0) ct = std::min(ct, m->n_trees);
+  m->chunk_trees = ct;
+  m->n_chunks = m->n_trees > 0 ? (m->n_trees + ct - 1) / ct : 0;
+  m->desc_bytes = (uint32_t)((per_tree_desc * ct + 127) & ~(size_t)127);
+  m->chunk_bytes = (uint32_t)((m->desc_bytes + (leaf_size(m->leaf_storage) << DI) * ct + 127) & ~(size_t)127);
+}
+
+// Descriptor + leaf records for a given tile size (descriptor offsets are f * tile).
+int build_chunks(obt_model* m, int tile, ChunkSet& out) {
+  const int DI = m->depth_inst;
+  const size_t per_tree_leaf = leaf_size(m->leaf_storage) << DI;
+  const int ct = m->chunk_trees;
+  const size_t tree_desc = (size_t)obt::desc_bytes_per_tree(DI, m->compare_mode);
+  const size_t desc_bytes = m->desc_bytes, chunk_bytes = m->chunk_bytes;
+  const int n_chunks = m->n_chunks;
+  std::vector<uint8_t> host((size_t)std::max(n_chunks, 1) * chunk_bytes, 0);
+  for (int t = 0; t < m->n_trees; ++t) {
+    const int c = t / ct, tl = t % ct;
+    uint8_t* rec = host.data() + (size_t)c * chunk_bytes;
+    for (int d = 0; d < DI; ++d) {
+      const int ord = m->split_ordinal[(size_t)t * DI + d];
+      const uint32_t f = ord == kSentinel ? 0u : (uint32_t)m->split_feature[(size_t)t * DI + d];
+      const uint32_t off = f * (uint32_t)tile;
+      if (m->compare_mode == 7) {
+        // q + (127 - ord) >= 128  <=>  q > ord, for q <= 127; sentinel: k = 0 never carries
+        const uint32_t k = ord == kSentinel ? 0u : (uint32_t)(127 - ord) * 0x01010101u;
+        obt::Desc7 ds{off, k};
+        std::memcpy(rec + (size_t)tl * tree_desc + (size_t)d * sizeof(ds), &ds, sizeof(ds));
+      } else {
+        // ord < 128: bit7(((q & 127) + 127 - ord) | q); ord >= 128: bit7(((q & 127) + 255 - ord) & q)
+        uint32_t k, s;
+        if (ord == kSentinel) { k = 0; s = 0; }
+        else if (ord < 128) { k = (uint32_t)(127 - ord) * 0x01010101u; s = 0xFFFFFFFFu; }
+        else { k = (uint32_t)(255 - ord) * 0x01010101u; s = 0; }
+        obt::Desc8 ds{off, k, s, 0};
+        std::memcpy(rec + (size_t)tl * tree_desc + (size_t)d * sizeof(ds), &ds, sizeof(ds));
+      }
+    }
+    std::memcpy(rec + desc_bytes + (size_t)tl * per_tree_leaf,
+                m->leaf_bytes.data() + (size_t)t * per_tree_leaf, per_tree_leaf);
+  }
+  out.chunk_trees = ct;
+  out.n_chunks = n_chunks;
+  out.chunk_bytes = (uint32_t)chunk_bytes;
+  out.desc_bytes = (uint32_t)desc_bytes;
+  CUDA_TRY(cudaMalloc(&out.d_chunks, host.size()));
+  CUDA_TRY(cudaMemcpy(out.d_chunks, host.data(), host.size(), cudaMemcpyHostToDevice));
+  return OBT_OK;
+}
+
+int get_chunks(obt_model* m, int tile, const ChunkSet** out) {
+  std::lock_guard<std::mutex> lock(m->mu);
+  auto it = m->chunks_by_tile.find(tile);
+  if (it == m->chunks_by_tile.end()) {
+    ChunkSet cs;
+    const int rc = build_chunks(m, tile, cs);
+    if (rc != OBT_OK) return rc;
+    it = m->chunks_by_tile.emplace(tile, cs).first;
+  }
+  *out = &it->second;
+  return OBT_OK;
+}
+
+constexpr int kStages = 3;
+
+// Largest tile (multiple of 128 objects, <= 4096) whose bucket tile fits next to the
+// stage ring; then shrink for small batches so the grid still covers the SMs.
+int plan_tile(const obt_model* m, int64_t n) {
+  const int64_t fixed = 128 + (int64_t)kStages * m->chunk_bytes;
+  int64_t tmax = (m->smem_optin - fixed) / m->n_features;
+  tmax = std::min<int64_t>(tmax / 128 * 128, 4096);
+  if (tmax < 128) return -1;
+  int64_t want = (n + m->sm_count - 1) / m->sm_count;
+  want = std::max<int64_t>(128, (want + 127) / 128 * 128);
+  return (int)std::min(tmax, want);
+}
+
+// ---------------------------------------------------------------------------
+// kernel dispatch
+using QuantFn = void (*)(obt::QuantizeParams);
+using ApplyFn = void (*)(obt::ApplyParams);
+
+template <int L>
+QuantFn quant_fn(int layout, bool tiled) {
+  if (layout == 0) return tiled ? obt::quantize_kernel<L, 0, true> : obt::quantize_kernel<L, 0, false>;
+  return tiled ? obt::quantize_kernel<L, 1, true> : obt::quantize_kernel<L, 1, false>;
+}
+
+QuantFn pick_quant(int levels, int layout, bool tiled) {
+  switch (levels) {
+    case 0: return quant_fn<0>(layout, tiled);
+    case 1: return quant_fn<1>(layout, tiled);
+    case 2: return quant_fn<2>(layout, tiled);
+    case 3: return quant_fn<3>(layout, tiled);
+    case 4: return quant_fn<4>(layout, tiled);
+    case 5: return quant_fn<5>(layout, tiled);
+    case 6: return quant_fn<6>(layout, tiled);
+    case 7: return quant_fn<7>(layout, tiled);
+    case 8: return quant_fn<8>(layout, tiled);
+    default: return nullptr;
+  }
+}
+
+template <int DI, int CMP>
+ApplyFn apply_fn_leaf(int leaf, bool write_idx) {
+  if (write_idx) return obt::apply_kernel<DI, CMP, 1, true>;
+  switch (leaf) {
+    case 0: return obt::apply_kernel<DI, CMP, 0, false>;
+    case 1: return obt::apply_kernel<DI, CMP, 1, false>;
+    default: return obt::apply_kernel<DI, CMP, 2, false>;
+  }
+}
+
+template <int DI>
+ApplyFn apply_fn_cmp(int cmp, int leaf, bool write_idx) {
+  return cmp == 7 ? apply_fn_leaf<DI, 7>(leaf, write_idx) : apply_fn_leaf<DI, 8>(leaf, write_idx);
+}
+
+ApplyFn pick_apply(int di, int cmp, int leaf, bool write_idx) {
+  switch (di) {
+    case 1: return apply_fn_cmp<1>(cmp, leaf, write_idx);
+    case 2: return apply_fn_cmp<2>(cmp, leaf, write_idx);
+    case 3: return apply_fn_cmp<3>(cmp, leaf, write_idx);
+    case 4: return apply_fn_cmp<4>(cmp, leaf, write_idx);
+    case 5: return apply_fn_cmp<5>(cmp, leaf, write_idx);
+    case 6: return apply_fn_cmp<6>(cmp, leaf, write_idx);
+    case 7: return apply_fn_cmp<7>(cmp, leaf, write_idx);
+    case 8: return apply_fn_cmp<8>(cmp, leaf, write_idx);
+    case 10: return apply_fn_cmp<10>(cmp, leaf, write_idx);
+    case 12: return apply_fn_cmp<12>(cmp, leaf, write_idx);
+    default: return nullptr;
+  }
+}
+
+int launch_quantize(const obt_model* m, const float* x, int64_t n, int layout, uint8_t* out, bool tiled,
+                    int tile, int64_t n_slots, cudaStream_t stream) {
+  QuantFn fn = pick_quant(m->levels, layout, tiled);
+  if (!fn) return fail(OBT_E_UNSUPPORTED, "no quantize kernel for %d levels", m->levels);
+  obt::QuantizeParams p{};
+  p.x = x;
+  p.n = n;
+  p.n_slots = n_slots;
+  p.n_features = m->n_features;
+  p.eytz = m->d_eytz;
+  p.eytz_pitch = m->eytz_pitch;
+  p.out = out;
+  p.tile = tile;
+  dim3 grid((unsigned)((n_slots + obt::kQuantObjects - 1) / obt::kQuantObjects),
+            (unsigned)((m->n_features + obt::kQuantFeatures - 1) / obt::kQuantFeatures));
+  fn<<<grid, obt::kQuantThreads, 0, stream>>>(p);
+  ++g_launches;
+  CUDA_TRY(cudaGetLastError());
+  return OBT_OK;
+}
+
+int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, double* out, uint16_t* idx_out,
+                 int tree_begin, int tree_end, cudaStream_t stream) {
+  const bool write_idx = idx_out != nullptr;
+  const ChunkSet* cs = nullptr;
+  int rc = get_chunks(m, tile, &cs);
+  if (rc != OBT_OK) return rc;
+  ApplyFn fn = pick_apply(m->depth_inst, m->compare_mode, m->leaf_storage, write_idx);
+  if (!fn) return fail(OBT_E_UNSUPPORTED, "no apply kernel for depth %d", m->depth_inst);
+  const int64_t n_tiles = (n + tile - 1) / tile;
+  const size_t smem = 128 + (size_t)kStages * cs->chunk_bytes + (size_t)m->n_features * tile;
+  if (smem > (size_t)m->smem_optin)
+    return fail(OBT_E_UNSUPPORTED, "tile of %d objects needs %zu bytes of shared memory", tile, smem);
+  CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  obt::ApplyParams p{};
+  p.q = q;
+  p.chunks = cs->d_chunks;
+  p.out = out;
+  p.idx_out = idx_out;
+  p.n = n;
+  p.tile = tile;
+  p.n_trees = m->n_trees;
+  p.chunk_trees = cs->chunk_trees;
+  p.n_chunks = cs->n_chunks;
+  p.chunk_bytes = cs->chunk_bytes;
+  p.desc_bytes = cs->desc_bytes;
+  p.q_tile_bytes = (uint32_t)((size_t)m->n_features * tile);
+  p.n_stages = kStages;
+  p.tree_begin = tree_begin;
+  p.tree_end = tree_end;
+  p.scale = m->scale;
+  p.bias = m->bias;
+  fn<<<(unsigned)n_tiles, tile / 4, smem, stream>>>(p);
+  ++g_launches;
+  CUDA_TRY(cudaGetLastError());
+  return OBT_OK;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+size_t workspace_bytes(const obt_model* m, int64_t n, int tile) {
+  const int64_t n_tiles = (n + tile - 1) / tile;
+  return (size_t)n_tiles * tile * m->n_features;
+}
+
+int check_layout(int layout) {
+  if (layout != OBT_LAYOUT_OBJECT_MAJOR && layout != OBT_LAYOUT_FEATURE_MAJOR)
+    return fail(OBT_E_INVALID, "unknown layout %d", layout);
+  return OBT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int obt_abi_version(void) { return OBT_ABI_VERSION; }
+
+const char* obt_last_error(void) { return g_error.c_str(); }
+
+int obt_last_launch_count(void) { return g_launches; }
+
+int obt_model_create(const obt_model_desc* d, int device, obt_model** out) {
+  if (!out) return fail(OBT_E_INVALID, "null output handle");
+  *out = nullptr;
+  int rc = validate(d);
+  if (rc != OBT_OK) return rc;
+  int n_dev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&n_dev));
+  if (device < 0 || device >= n_dev) return fail(OBT_E_INVALID, "device %d not present (%d visible)", device, n_dev);
+  DeviceGuard guard(device);
+
+  std::unique_ptr<obt_model> m(new obt_model());
+  m->device = device;
+  m->n_features = d->n_features;
+  m->n_trees = d->n_trees;
+  m->max_depth = d->n_trees > 0 ? d->max_depth : 0;
+  m->n_outputs = d->n_outputs;
+  m->precision = d->precision;
+  m->scale = d->scale;
+  m->bias = d->bias;
+  m->depth_inst = d->n_trees > 0 ? instantiated_depth(d->max_depth) : 1;
+  CUDA_TRY(cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount, device));
+  CUDA_TRY(cudaDeviceGetAttribute(&m->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+
+  // borders -> Eytzinger arrays
+  int bmax = 0;
+  for (int f = 0; f < d->n_features; ++f) bmax = std::max(bmax, d->border_counts[f]);
+  m->compare_mode = bmax <= 127 ? 7 : 8;
+  int levels = 0;
+  while (((1 << levels) - 1) < bmax) ++levels;
+  m->levels = levels;
+  m->eytz_pitch = std::max(1, (1 << levels) - 1);
+  std::vector<float> eytz((size_t)d->n_features * m->eytz_pitch, INFINITY);
+  for (int f = 0; f < d->n_features; ++f) {
+    int pos = 0;
+    if (levels > 0)
+      eytzinger_fill(d->borders + (size_t)f * d->border_stride, d->border_counts[f],
+                     eytz.data() + (size_t)f * m->eytz_pitch, (1 << levels) - 1, pos, 0);
+  }
+  CUDA_TRY(cudaMalloc(&m->d_eytz, eytz.size() * sizeof(float)));
+  CUDA_TRY(cudaMemcpy(m->d_eytz, eytz.data(), eytz.size() * sizeof(float), cudaMemcpyHostToDevice));
+
+  // splits, padded from Dmax to the instantiated depth with sentinels
+  const int D = m->max_depth, DI = m->depth_inst;
+  m->split_feature.assign((size_t)m->n_trees * DI, 0);
+  m->split_ordinal.assign((size_t)m->n_trees * DI, (uint8_t)kSentinel);
+  for (int t = 0; t < m->n_trees; ++t)
+    for (int s = 0; s < D; ++s) {
+      m->split_feature[(size_t)t * DI + s] = d->split_feature[(size_t)t * D + s];
+      m->split_ordinal[(size_t)t * DI + s] = d->split_ordinal[(size_t)t * D + s];
+    }
+
+  // leaf bank: binary16 bits, or binary64 stored as fp32 when that is exact
+  const size_t per_tree_in = (size_t)1 << D, per_tree = (size_t)1 << DI;
+  if (d->precision == OBT_PRECISION_BINARY16) {
+    m->leaf_storage = 2;
+  } else {
+    bool exact32 = true;
+    for (size_t i = 0; i < (size_t)m->n_trees * per_tree_in && exact32; ++i) {
+      const double v = d->leaves[i];
+      const float f = (float)v;
+      exact32 = std::isfinite(f) && (double)f == v && !(v == 0.0 && std::signbit(v) != std::signbit(f));
+    }
+    m->leaf_storage = exact32 ? 1 : 0;
+  }
+  const size_t ls = leaf_size(m->leaf_storage);
+  m->leaf_bytes.assign((size_t)m->n_trees * per_tree * ls, 0);
+  for (int t = 0; t < m->n_trees; ++t) {
+    for (size_t j = 0; j < per_tree_in; ++j) {
+      const double v = d->leaves[(size_t)t * per_tree_in + j];
+      uint8_t* dst = m->leaf_bytes.data() + ((size_t)t * per_tree + j) * ls;
+      if (m->leaf_storage == 0) {
+        std::memcpy(dst, &v, 8);
+      } else if (m->leaf_storage == 1) {
+        const float f = (float)v;
+        std::memcpy(dst, &f, 4);
+      } else {
+        const uint16_t h = d->leaves_f16 ? d->leaves_f16[(size_t)t * per_tree_in + j] : half_bank_entry(v);
+        std::memcpy(dst, &h, 2);
+      }
+    }
+  }
+  plan_chunks(m.get());
+  *out = m.release();
+  return OBT_OK;
+}
+
+int obt_model_destroy(obt_model* m) {
+  if (!m) return OBT_OK;
+  DeviceGuard guard(m->device);
+  delete m;
+  return OBT_OK;
+}
+
+int obt_model_info(const obt_model* m, int32_t* n_features, int32_t* n_trees, int32_t* max_depth,
+                   int32_t* n_outputs, int32_t* precision, int32_t* leaf_storage, int32_t* compare_mode) {
+  if (!m) return fail(OBT_E_INVALID, "null model");
+  if (n_features) *n_features = m->n_features;
+  if (n_trees) *n_trees = m->n_trees;
+  if (max_depth) *max_depth = m->max_depth;
+  if (n_outputs) *n_outputs = m->n_outputs;
+  if (precision) *precision = m->precision;
+  if (leaf_storage) *leaf_storage = m->leaf_storage;
+  if (compare_mode) *compare_mode = m->compare_mode;
+  return OBT_OK;
+}
+
+int obt_workspace_size(const obt_model* m, int64_t n, size_t* bytes) {
+  if (!m || !bytes) return fail(OBT_E_INVALID, "null argument");
+  if (n < 0) return fail(OBT_E_INVALID, "negative object count");
+  const int tile = plan_tile(m, std::max<int64_t>(n, 1));
+  if (tile < 0) return fail(OBT_E_UNSUPPORTED, "%d features do not fit a 128-object tile", m->n_features);
+  *bytes = n == 0 ? 0 : workspace_bytes(m, n, tile);
+  return OBT_OK;
+}
+
+static int predict_impl(obt_model* m, const float* x, int64_t n, int32_t layout, double* out, uint16_t* idx_out,
+                        int tree_begin, int tree_end, void* ws, size_t ws_bytes, cudaStream_t stream) {
+  const int tile = plan_tile(m, n);
+  if (tile < 0) return fail(OBT_E_UNSUPPORTED, "%d features do not fit a 128-object tile", m->n_features);
+  const size_t need = workspace_bytes(m, n, tile);
+  uint8_t* q = static_cast<uint8_t*>(ws);
+  bool owned = false;
+  if (!q || ws_bytes < need) {
+    if (ws && ws_bytes < need) return fail(OBT_E_INVALID, "workspace of %zu bytes, need %zu", ws_bytes, need);
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&q), need, stream));
+    owned = true;
+  }
+  const int64_t n_slots = ((n + tile - 1) / tile) * (int64_t)tile;
+  int rc = launch_quantize(m, x, n, layout, q, true, tile, n_slots, stream);
+  if (rc == OBT_OK) rc = launch_apply(m, q, n, tile, out, idx_out, tree_begin, tree_end, stream);
+  if (owned) cudaFreeAsync(q, stream);
+  return rc;
+}
+
+int obt_predict_dev(const obt_model* mc, const float* x, int64_t n, int32_t layout, double* out, void* ws,
+                    size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  obt_model* m = const_cast<obt_model*>(mc);  // only the per-tile chunk cache mutates (locked)
+  if (!m) return fail(OBT_E_INVALID, "null model");
+  int rc = check_layout(layout);
+  if (rc != OBT_OK) return rc;
+  if (n < 0) return fail(OBT_E_INVALID, "negative object count");
+  if (n == 0) return OBT_OK;
+  if (!x || !out) return fail(OBT_E_INVALID, "null feature or output pointer");
+  DeviceGuard guard(m->device);
+  return predict_impl(m, x, n, layout, out, nullptr, 0, 0, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int obt_leaf_indices_dev(const obt_model* mc, const float* x, int64_t n, int32_t layout, int32_t tree_begin,
+                         int32_t tree_end, uint16_t* idx, void* stream) {
+  g_launches = 0;
+  obt_model* m = const_cast<obt_model*>(mc);
+  if (!m) return fail(OBT_E_INVALID, "null model");
+  int rc = check_layout(layout);
+  if (rc != OBT_OK) return rc;
+  if (tree_begin < 0 || tree_end < tree_begin || tree_end > m->n_trees)
+    return fail(OBT_E_INVALID, "tree range [%d, %d) outside 0..%d", tree_begin, tree_end, m->n_trees);
+  if (n < 0) return fail(OBT_E_INVALID, "negative object count");
+  if (n == 0 || tree_end == tree_begin) return OBT_OK;
+  if (!x || !idx) return fail(OBT_E_INVALID, "null feature or index pointer");
+  DeviceGuard guard(m->device);
+  return predict_impl(m, x, n, layout, nullptr, idx, tree_begin, tree_end, nullptr, 0,
+                      static_cast<cudaStream_t>(stream));
+}
+
+int obt_quantize_dev(const obt_model* m, const float* x, int64_t n, int32_t layout, uint8_t* buckets,
+                     void* stream) {
+  g_launches = 0;
+  if (!m) return fail(OBT_E_INVALID, "null model");
+  int rc = check_layout(layout);
+  if (rc != OBT_OK) return rc;
+  if (n < 0) return fail(OBT_E_INVALID, "negative object count");
+  if (n == 0) return OBT_OK;
+  if (!x || !buckets) return fail(OBT_E_INVALID, "null feature or bucket pointer");
+  DeviceGuard guard(m->device);
+  return launch_quantize(m, x, n, layout, buckets, false, 0, n, static_cast<cudaStream_t>(stream));
+}
+
+int obt_predict_host(const obt_model* mc, const float* x_host, int64_t n, int32_t layout, double* out_host,
+                     void* stream_v) {
+  g_launches = 0;
+  obt_model* m = const_cast<obt_model*>(mc);
+  if (!m) return fail(OBT_E_INVALID, "null model");
+  int rc = check_layout(layout);
+  if (rc != OBT_OK) return rc;
+  if (n < 0) return fail(OBT_E_INVALID, "negative object count");
+  if (n == 0) return OBT_OK;
+  if (!x_host || !out_host) return fail(OBT_E_INVALID, "null feature or output pointer");
+  DeviceGuard guard(m->device);
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  const size_t xbytes = (size_t)n * m->n_features * sizeof(float);
+  float* x_dev = nullptr;
+  double* out_dev = nullptr;
+  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&x_dev), xbytes, stream));
+  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&out_dev), (size_t)n * sizeof(double), stream));
+  rc = OBT_OK;
+  cudaError_t e = cudaMemcpyAsync(x_dev, x_host, xbytes, cudaMemcpyHostToDevice, stream);
+  if (e != cudaSuccess) rc = fail(OBT_E_CUDA, "host->device copy failed: %s", cudaGetErrorString(e));
+  if (rc == OBT_OK) rc = predict_impl(m, x_dev, n, layout, out_dev, nullptr, 0, 0, nullptr, 0, stream);
+  if (rc == OBT_OK) {
+    e = cudaMemcpyAsync(out_host, out_dev, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, stream);
+    if (e != cudaSuccess) rc = fail(OBT_E_CUDA, "device->host copy failed: %s", cudaGetErrorString(e));
+  }
+  cudaFreeAsync(x_dev, stream);
+  cudaFreeAsync(out_dev, stream);
+  e = cudaStreamSynchronize(stream);
+  if (rc == OBT_OK && e != cudaSuccess) rc = fail(OBT_E_CUDA, "stream synchronize failed: %s", cudaGetErrorString(e));
+  return rc;
+}
+
+}  // extern "C"

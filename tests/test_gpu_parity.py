@@ -1,0 +1,223 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle.
+
+Bucket ids and leaf indices must be bit-exact; predictions are bit-exact too for
+both precision families (binary64 tree-order fold of binary64/fp32-exact leaves;
+binary16 leaves with a binary32 fold), which is stricter than the reference's own
+1e-12 / 1e-6 tolerances (SPEC.md acceptance 3).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2211_00391_b200 as obt
+from paper_2211_00391_b200 import stages, synthetic
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _model(F, B, T, D, seed, affine=True, sigma=0.1):
+    spec = synthetic.WorkloadSpec("t", 1, F, B, T, D, sigma, cfg=1)
+    return synthetic.build_model(spec, seed=seed, affine=affine)
+
+
+def _features(model, n, seed, specials=True):
+    spec = synthetic.WorkloadSpec("t", n, model.n_features, 1, 1, 1, 0.1, cfg=1)
+    x = synthetic.host_features(spec, seed=seed)
+    if specials:
+        x = synthetic.sprinkle_specials(x, [ff.borders for ff in model.float_features], seed=seed + 1)
+    return x
+
+
+def _mixed_depth_model(F, B, T, seed):
+    rng = np.random.default_rng(seed)
+    base = _model(F, B, 1, 1, seed)
+    trees = []
+    for _ in range(T):
+        d = int(rng.integers(1, 9))
+        splits = tuple(obt.SplitCondition(int(rng.integers(0, F)), int(rng.integers(0, B))) for _ in range(d))
+        trees.append(obt.ObliviousTree(depth=d, splits=splits, leaf_values=rng.uniform(-1, 1, 1 << d)))
+    return obt.ObliviousModel(base.float_features, tuple(trees), scale=1.25, bias=-0.5)
+
+
+def test_smoke():
+    import __graft_entry__ as ge
+
+    ge.smoke()
+
+
+@pytest.mark.parametrize("layout", [obt.Layout.OBJECT_MAJOR, obt.Layout.FEATURE_MAJOR])
+@pytest.mark.parametrize("B", [1, 7, 16, 64, 127, 128, 200, 254])
+def test_quantize_bit_exact(layout, B):
+    model = _model(23, B, 3, 2, seed=B)
+    x = _features(model, 1537, seed=100 + B)
+    fm = oracle.flatten(model)
+    xin = x if layout is obt.Layout.OBJECT_MAJOR else np.ascontiguousarray(x.T)
+    got = stages.quantize(model, torch.from_numpy(xin).cuda(), layout).cpu().numpy()
+    want = oracle.quantize(fm, xin, oracle.OBJECT_MAJOR if layout is obt.Layout.OBJECT_MAJOR else oracle.FEATURE_MAJOR)
+    assert got.shape == want.shape
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("D", [1, 2, 3, 5, 6, 7, 8])
+@pytest.mark.parametrize("B", [16, 128, 254])
+def test_leaf_indices_bit_exact(D, B):
+    model = _model(17, B, 37, D, seed=D * 7 + B)
+    x = _features(model, 777, seed=D)
+    fm = oracle.flatten(model)
+    got = stages.as_uint16(stages.leaf_indices(model, torch.from_numpy(x).cuda()))
+    want = oracle.leaf_indices(fm, oracle.quantize(fm, x))
+    assert np.array_equal(got, want)
+
+
+def test_leaf_indices_tree_range_and_mixed_depth():
+    model = _mixed_depth_model(9, 30, 50, seed=3)
+    x = _features(model, 300, seed=4)
+    fm = oracle.flatten(model)
+    want = oracle.leaf_indices(fm, oracle.quantize(fm, x))
+    got = stages.as_uint16(stages.leaf_indices(model, torch.from_numpy(x).cuda(), tree_begin=11, tree_end=29))
+    assert np.array_equal(got, want[11:29])
+
+
+@pytest.mark.parametrize("strategy", [obt.LeafStrategy.NAIVE, obt.LeafStrategy.NAIVE16])
+@pytest.mark.parametrize("n", [1, 7, 31, 32, 33, 100, 128, 257, 4099])
+def test_predict_bit_exact_batch_sizes(strategy, n):
+    model = _model(31, 40, 90, 6, seed=n)
+    x = _features(model, n, seed=n + 5)
+    prec = oracle.BINARY64 if strategy is obt.LeafStrategy.NAIVE else oracle.BINARY16
+    want = oracle.evaluate_scalar(oracle.flatten(model), x, oracle.OBJECT_MAJOR, prec)
+    got = obt.Evaluator(model, obt.EvalConfig(strategy=strategy)).predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("D", [1, 2, 3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("B", [5, 64, 128, 254])
+def test_predict_bit_exact_depth_borders(D, B):
+    model = _model(13, B, 61, D, seed=1000 + D * 10 + B)
+    x = _features(model, 513, seed=D + B)
+    fm = oracle.flatten(model)
+    for strategy, prec in ((obt.LeafStrategy.NAIVE, oracle.BINARY64), (obt.LeafStrategy.PERMUTE16, oracle.BINARY16)):
+        ev = obt.Evaluator(model, obt.EvalConfig(strategy=strategy, width=obt.VectorWidth.W512))
+        got = ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
+        want = oracle.evaluate_scalar(fm, x, oracle.OBJECT_MAJOR, prec)
+        assert np.array_equal(got, want), (strategy, int(np.count_nonzero(got != want)))
+
+
+def test_predict_binary64_leaves_not_fp32_exact():
+    """Arbitrary binary64 leaves (not fp32-representable) use the fp64 table."""
+    rng = np.random.default_rng(11)
+    base = _model(8, 20, 1, 1, seed=11)
+    trees = tuple(
+        obt.ObliviousTree(
+            depth=5,
+            splits=tuple(obt.SplitCondition(int(rng.integers(0, 8)), int(rng.integers(0, 20))) for _ in range(5)),
+            leaf_values=rng.standard_normal(32) * 10.0 ** rng.integers(-8, 3),
+        )
+        for _ in range(70)
+    )
+    model = obt.ObliviousModel(base.float_features, trees, scale=0.75, bias=0.125)
+    x = _features(model, 999, seed=12)
+    ev = obt.Evaluator(model)
+    assert ev.leaf_storage == "fp64"
+    got = ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
+    assert np.array_equal(got, oracle.evaluate_scalar(oracle.flatten(model), x))
+
+
+def test_predict_mixed_depth_and_layouts():
+    model = _mixed_depth_model(11, 25, 120, seed=21)
+    x = _features(model, 1000, seed=22)
+    want = oracle.evaluate_scalar(oracle.flatten(model), x)
+    ev = obt.Evaluator(model)
+    om = obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR)
+    assert np.array_equal(ev.predict(om), want)
+    assert np.array_equal(ev.predict(om.transposed()), want)
+
+
+def test_predict_zero_trees_and_empty_batch():
+    model = obt.ObliviousModel(
+        float_features=(obt.FloatFeatureBorders(0, np.array([0.5], dtype=np.float32)),), trees=(), scale=2.0, bias=0.75
+    )
+    ev = obt.Evaluator(model)
+    x = np.zeros((5, 1), dtype=np.float32)
+    assert np.all(ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR)) == 0.75)
+    assert ev.predict(obt.FeatureMatrix(np.zeros((0, 1), np.float32), obt.Layout.OBJECT_MAJOR)).shape == (0,)
+
+
+def test_depth3_known_answer():
+    # (root, d1, d2) conditions (1, 0, 1) address leaf 0b101 = 5 (test_acceptance.py:194-214)
+    features = tuple(obt.FloatFeatureBorders(i, np.array([0.5], dtype=np.float32)) for i in range(3))
+    tree = obt.ObliviousTree(
+        depth=3,
+        splits=(obt.SplitCondition(0, 0), obt.SplitCondition(1, 0), obt.SplitCondition(2, 0)),
+        leaf_values=np.arange(10.0, 18.0),
+    )
+    model = obt.ObliviousModel(features, (tree,), scale=2.0, bias=1.0)
+    x = np.array([[1.0, 0.0, 1.0]], dtype=np.float32)
+    assert obt.evaluate(model, obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))[0] == 15.0 * 2.0 + 1.0
+    idx = stages.as_uint16(stages.leaf_indices(model, torch.from_numpy(x).cuda()))
+    assert idx[0, 0] == 5
+
+
+def test_predict_device_matches_host_path():
+    model = _model(40, 64, 200, 6, seed=5, affine=False)
+    x = _features(model, 20000, seed=6, specials=False)
+    ev = obt.Evaluator(model)
+    host = ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
+    dev = ev.predict_device(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.array_equal(host, dev)
+    ws = torch.empty(ev.workspace_bytes(x.shape[0]), dtype=torch.uint8, device="cuda")
+    dev2 = ev.predict_device(torch.from_numpy(x).cuda(), workspace=ws).cpu().numpy()
+    assert np.array_equal(host, dev2)
+
+
+@pytest.mark.parametrize("D", [9, 10, 12])
+def test_predict_deeper_than_reference(D):
+    """Depths 9..12 (the multiclass config needs 10) through the padded instantiations."""
+    rng = np.random.default_rng(D)
+    F, B, T = 10, 30, 25
+    borders = tuple(obt.FloatFeatureBorders(f, np.sort(rng.standard_normal(B)).astype(np.float32)) for f in range(F))
+    fm = oracle.FlatModel(
+        borders=np.stack([b.borders for b in borders]),
+        border_counts=np.full(F, B, np.int32),
+        depths=np.full(T, D, np.int32),
+        split_feature=rng.integers(0, F, (T, D)).astype(np.int32),
+        split_ordinal=rng.integers(0, B, (T, D)).astype(np.int32),
+        leaves=rng.standard_normal((T, 1, 1 << D)).astype(np.float32).astype(np.float64),
+        scale=1.0,
+        bias=0.0,
+    )
+    x = rng.standard_normal((700, F)).astype(np.float32)
+    want = oracle.evaluate_scalar(fm, x)
+    from paper_2211_00391_b200.evaluate import DeviceModel  # noqa: F401 (low-level path below)
+    import ctypes
+
+    from paper_2211_00391_b200 import _native
+
+    lib = _native.require_gpu()
+    desc = _native.ModelDesc()
+    so = fm.split_ordinal.astype(np.uint8)
+    leaves = np.ascontiguousarray(fm.leaves[:, 0, :])
+    desc.n_features, desc.n_trees, desc.max_depth, desc.n_outputs = F, T, D, 1
+    desc.border_counts = fm.border_counts.ctypes.data
+    desc.borders = fm.borders.ctypes.data
+    desc.border_stride = B
+    desc.split_feature = fm.split_feature.ctypes.data
+    desc.split_ordinal = so.ctypes.data
+    desc.leaves = leaves.ctypes.data
+    desc.leaves_f16 = None
+    desc.scale, desc.bias, desc.precision = 1.0, 0.0, 0
+    h = ctypes.c_void_p()
+    _native.check(lib.obt_model_create(ctypes.byref(desc), 0, ctypes.byref(h)))
+    try:
+        xd = torch.from_numpy(x).cuda()
+        out = torch.empty(x.shape[0], dtype=torch.float64, device="cuda")
+        _native.check(lib.obt_predict_dev(h, xd.data_ptr(), x.shape[0], 0, out.data_ptr(), None, 0,
+                                          _native.current_stream_handle()))
+        got = out.cpu().numpy()
+    finally:
+        lib.obt_model_destroy(h)
+    assert np.array_equal(got, want)
