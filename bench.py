@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""Benchmark: object-trees/s of oblivious-ensemble predict on B200, with roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+One "step" is one predict over one batch of the workload (BASELINE.json configs[1]
+by default: 1,000,000 objects x 200 features, 64 borders, 2,000 depth-6 trees, fp32
+leaves).  Under torchrun each rank owns one GPU and its own batch of that size
+(object sharding, no data-path collective: weak scaling); NCCL carries only the
+barrier and the max-over-ranks of the device-timed region.
+
+Printed on rank 0 as ONE JSON line:
+  value      whole-job object-trees/s, features resident in HBM, CUDA-event timed
+  e2e        the same metric through Evaluator.predict with pinned host buffers
+             (host->device features and device->host scores inside the timed region)
+  roofline   the dominant kernel (tree apply) against the integer-issue peak, plus the
+             whole-step roofline of BASELINE.md section 6
+  cpu_baseline  the C oracle port of the reference algorithm on this host's cores
+`--impl reference` times that CPU port alone on the same config and metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "object-trees/sec for oblivious-ensemble predict at 1/2/4/8 B200; % roofline"
+UNIT = "object-trees/s"
+FALLBACK_HBM_GBS = 6650.0
+FALLBACK_SM_MHZ = 1965.0
+
+
+def peaks() -> dict:
+    path = ROOT / "MEASURED_PEAKS.json"
+    if path.exists():
+        data = json.loads(path.read_text())
+        return {"hbm_gbs": float(data["hbm_gbs"]), "sm_max_mhz": float(data.get("sm_max_mhz", FALLBACK_SM_MHZ)),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": FALLBACK_HBM_GBS, "sm_max_mhz": FALLBACK_SM_MHZ, "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.sw_power_cap,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._reader = threading.Thread(target=self._read, daemon=True)
+            self._reader.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.perf_counter(), line.strip()))
+
+    def stop(self, t0: float, t1: float) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        for ts, line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            rows.append((ts, parts))
+        inside = [r for r in rows if t0 <= r[0] <= t1 + 0.06] or rows[-3:]
+        sm = sorted(float(p[0]) for _, p in inside if p[0].replace(".", "").isdigit())
+        smax = [float(p[1]) for _, p in inside if p[1].replace(".", "").isdigit()]
+        names = ("sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown")
+        reasons = sorted({names[i] for _, p in inside for i in range(4) if p[3 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(inside)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def max_over_ranks(value: float, world: int) -> float:
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def roofline_terms(spec) -> dict:
+    """bytes = 4NF + 8NC, ops = NTD + NF*ceil(log2(B+1)) + NTC."""
+    N, F, B, T, D, C = spec.n_objects, spec.n_features, spec.borders, spec.n_trees, spec.depth, spec.n_outputs
+    return {
+        "bytes": 4 * N * F + 8 * N * C,
+        "ops": N * T * D + N * F * math.ceil(math.log2(B + 1)) + N * T * C,
+        "apply_ops": N * T * D + N * T * C,
+        "quantize_bytes": 4 * N * F + N * F,
+    }
+
+
+def cpu_baseline(spec, model, seconds: float, verify_fn=None) -> dict:
+    """The C oracle port of the reference algorithm on this host's cores, on a bounded
+    prefix sample of the same workload (doubling until the run takes >= `seconds`/4)."""
+    import numpy as np
+
+    import oracle
+    from paper_2211_00391_b200 import synthetic
+
+    fm = oracle.flatten(model)
+    threads = oracle.max_threads()
+    n = 4096
+    best = None
+    while True:
+        x = synthetic.host_features(spec, n_objects=n, seed=spec.data_seed + 7)
+        t0 = time.perf_counter()
+        ref = oracle.evaluate_scalar(fm, x, oracle.OBJECT_MAJOR,
+                                     oracle.BINARY16 if spec.half_leaves else oracle.BINARY64)
+        dt = time.perf_counter() - t0
+        best = (n, dt, x, ref)
+        if dt >= seconds / 4 or n >= spec.n_objects or n >= 1 << 22:
+            break
+        n *= 2
+    n, dt, x, ref = best
+    reps = max(1, int(round(seconds * 0.75 / max(dt, 1e-6))))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        oracle.evaluate_scalar(fm, x, oracle.OBJECT_MAJOR, oracle.BINARY16 if spec.half_leaves else oracle.BINARY64)
+    dt = (time.perf_counter() - t0) / reps
+    out = {
+        "value": n * spec.n_trees / dt,
+        "unit": UNIT,
+        "cores": threads,
+        "host_cpus": os.cpu_count(),
+        "kind": "port",
+        "sample": f"first {n} objects of the workload (full {spec.n_trees}-tree model), {reps} reps, "
+                  f"C restatement of evaluate_scalar (oracle/obtree_oracle.c), OpenMP over objects",
+    }
+    if verify_fn is not None:
+        got = verify_fn(x)
+        out["gpu_verified_bit_exact"] = bool(np.array_equal(got, ref))
+        rel = np.abs(got - ref) / np.maximum(np.maximum(np.abs(got), np.abs(ref)), 1e-300)
+        out["gpu_max_rel_dev"] = float(rel.max()) if rel.size else 0.0
+    return out
+
+
+def load_ncu_traffic(cfg: int):
+    path = ROOT / "profiles" / "ncu_apply_summary.json"
+    if not path.exists():
+        return None
+    try:
+        data = json.loads(path.read_text())
+        return data.get(f"cfg{cfg}", {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the CPU port of the reference algorithm, all host threads."""
+    if rank != 0:
+        return
+    import numpy as np  # noqa: F401
+
+    import oracle
+    from paper_2211_00391_b200 import synthetic
+
+    spec = synthetic.CONFIGS[args.config]
+    model = synthetic.build_model(spec)
+    fm = oracle.flatten(model)
+    prec = oracle.BINARY16 if spec.half_leaves else oracle.BINARY64
+    n = args.ref_sample
+    x = synthetic.host_features(spec, n_objects=n, seed=spec.data_seed + 7)
+    for _ in range(args.warmup):
+        oracle.evaluate_scalar(fm, x, oracle.OBJECT_MAJOR, prec)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.evaluate_scalar(fm, x, oracle.OBJECT_MAJOR, prec)
+        times.append(time.perf_counter() - t0)
+    step = sum(times) / len(times)
+    value = n * spec.n_trees / step
+    line = {
+        "impl": "reference",
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f16/f32" if spec.half_leaves else "f64", "data": "synthetic",
+        "config": {"workload": spec.name, "n_objects_per_step": n, "features": spec.n_features,
+                   "borders": spec.borders, "trees": spec.n_trees, "depth": spec.depth},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.max_threads(), "host_cpus": os.cpu_count(),
+                         "kind": "port",
+                         "sample": f"{n} objects per step of {spec.name}; the reference is pure Python/numpy and "
+                                   f"cannot travel, so its algorithm runs as the C oracle port"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, world, rank, local):
+    import numpy as np
+    import torch
+
+    import paper_2211_00391_b200 as obt
+    from paper_2211_00391_b200 import _native, synthetic
+
+    spec = synthetic.CONFIGS[args.config]
+    if args.objects:
+        spec = synthetic.WorkloadSpec(**{**spec.__dict__, "n_objects": args.objects})
+    device = local
+    torch.cuda.set_device(device)
+    model = synthetic.build_model(spec)
+    strategy = obt.LeafStrategy.NAIVE16 if spec.half_leaves else obt.LeafStrategy.NAIVE
+    ev = obt.Evaluator(model, obt.EvalConfig(strategy=strategy), device=device)
+    x = synthetic.device_features(spec, seed=spec.data_seed + 1000 * rank, device=f"cuda:{device}")
+    N = spec.n_objects
+    out = torch.empty(N, dtype=torch.float64, device=x.device)
+    ws = torch.empty(ev.workspace_bytes(N), dtype=torch.uint8, device=x.device)
+
+    for _ in range(args.warmup):
+        ev.predict_device(x, out=out, workspace=ws)
+    torch.cuda.synchronize()
+
+    stream = _native.current_stream_handle(device)
+    K = args.steps
+    marks = [[_native.Event(), _native.Event(), _native.Event()] for _ in range(K)]
+    t_start, t_end = _native.Event(), _native.Event()
+    clocks = ClockSampler(device)
+    clocks.start()
+    time.sleep(0.15)
+    barrier(world)
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    t_start.record(stream)
+    launches = 0
+    for k in range(K):
+        ev.predict_device_marked(x, marks[k], out=out, workspace=ws)
+        launches += ev.last_launch_count()
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    w1 = time.perf_counter()
+    barrier(world)
+    clk = clocks.stop(w0, w1)
+    elapsed_ms = max_over_ranks(t_start.elapsed_ms(t_end), world)
+    q_ms = sum(m[0].elapsed_ms(m[1]) for m in marks) / K
+    a_ms = sum(m[1].elapsed_ms(m[2]) for m in marks) / K
+    step_s = elapsed_ms / K / 1e3
+    value = world * N * spec.n_trees / step_s
+
+    # end to end through the public API: pinned host features -> scores in pinned host memory
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.empty((N, spec.n_features), dtype=torch.float32, pin_memory=True)
+        xh.copy_(x)
+        oh = torch.empty(N, dtype=torch.float64, pin_memory=True)
+        fmx = obt.FeatureMatrix(xh.numpy(), obt.Layout.OBJECT_MAJOR)
+        ohn = oh.numpy()
+        ev.predict(fmx, out=ohn)
+        ke = max(1, min(K, args.e2e_steps))
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(ke):
+            ev.predict(fmx, out=ohn)
+        dt = max_over_ranks(time.perf_counter() - t0, world) / ke
+        e2e = {"value": world * N * spec.n_trees / dt, "unit": UNIT, "ms_per_step": dt * 1e3,
+               "h2d_bytes_per_step": N * spec.n_features * 4, "d2h_bytes_per_step": N * 8,
+               "api": "Evaluator.predict(FeatureMatrix, out=pinned) -> obt_predict_host", "steps": ke}
+        del xh, oh
+
+    if rank != 0:
+        return
+    pk = peaks()
+    import ctypes
+
+    sms = ctypes.c_int()
+    props = torch.cuda.get_device_properties(device)
+    n_sm = props.multi_processor_count
+    p_int = n_sm * 128 * pk["sm_max_mhz"] * 1e6  # lane-ops/s
+    terms = roofline_terms(spec)
+    apply_achieved = terms["apply_ops"] / (a_ms / 1e3)
+    t_roof = max(terms["bytes"] / (pk["hbm_gbs"] * 1e9), terms["ops"] / p_int)
+    quant_gbs = terms["quantize_bytes"] / (q_ms / 1e3) / 1e9
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f16/f32" if spec.half_leaves else "f64",
+        "data": "synthetic (seeded; BASELINE names no dataset)",
+        "config": {"workload": spec.name, "n_objects_per_gpu": N, "features": spec.n_features,
+                   "borders": spec.borders, "trees": spec.n_trees, "depth": spec.depth,
+                   "leaves": "fp16 (binary32 fold)" if spec.half_leaves else "fp32 values (binary64 fold)",
+                   "leaf_storage_on_device": ev.leaf_storage,
+                   "l2": "inputs larger than L2 (features 4NF bytes, buckets NF bytes > 126 MB)",
+                   "parallelism": f"objects sharded over {world} GPU(s), no data-path collective"},
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "roofline": {
+            "bound": "issue", "kernel": "apply_kernel (leaf index + gather + fold)",
+            "achieved": apply_achieved / 1e12, "peak": p_int / 1e12, "unit": "Tlane-op/s",
+            "frac": apply_achieved / p_int, "traffic": load_ncu_traffic(args.config),
+            "algorithmic_ops_per_launch": terms["apply_ops"], "ms_per_launch": a_ms,
+            "ops_definition": "N*T*D split compares + N*T*C leaf gathers (SURVEY.md 8d)",
+            "peak_source": f"{n_sm} SMs x 128 lanes x {pk['sm_max_mhz']:.0f} MHz",
+        },
+        "roofline_step": {"t_roof_ms": t_roof * 1e3, "t_step_ms": step_s * 1e3, "frac": t_roof / step_s,
+                          "bytes": terms["bytes"], "ops": terms["ops"], "hbm_gbs_peak": pk["hbm_gbs"],
+                          "peak_source": pk["source"]},
+        "kernels": {"quantize_ms": q_ms, "quantize_GBps": quant_gbs, "quantize_frac_hbm": quant_gbs / pk["hbm_gbs"],
+                    "apply_ms": a_ms},
+        "clocks": clk,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        def verify(xs):
+            got = ev.predict(obt.FeatureMatrix(xs, obt.Layout.OBJECT_MAJOR))
+            return got
+
+        line["cpu_baseline"] = cpu_baseline(spec, model, args.cpu_seconds, verify)
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4])
+    ap.add_argument("--objects", type=int, default=0, help="override objects per GPU")
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--ref-sample", type=int, default=65536)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world, rank, local = dist_setup()
+    try:
+        if args.impl == "reference":
+            run_reference(args, world, rank)
+        else:
+            run_ours(args, world, rank, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

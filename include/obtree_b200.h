@@ -116,6 +116,19 @@ int obt_leaf_indices_dev(const obt_model* model, const float* x_dev, int64_t n_o
                          int32_t layout, int32_t tree_begin, int32_t tree_end,
                          uint16_t* idx_dev, void* stream);
 
+/* obt_predict_dev with CUDA events recorded on `stream` before the quantize kernel,
+ * between quantize and apply, and after apply (events from obt_event_create; any may
+ * be NULL).  Used by bench.py to time each kernel on the stream it runs on. */
+int obt_predict_dev_marked(const obt_model* model, const float* x_dev, int64_t n_objects,
+                           int32_t layout, double* out_dev, void* workspace, size_t workspace_bytes,
+                           void* stream, void* ev_begin, void* ev_mid, void* ev_end);
+
+/* Minimal CUDA event helpers (timing-enabled events) for callers without a CUDA binding. */
+int obt_event_create(void** event);
+int obt_event_record(void* event, void* stream);
+int obt_event_elapsed_ms(void* start, void* end, float* ms);
+int obt_event_destroy(void* event);
+
 /* Number of kernel launches the last predict on this thread issued (bench evidence). */
 int obt_last_launch_count(void);
 

@@ -9,9 +9,10 @@
  *
  * Every function restates one piece of the reference package
  * (/root/reference/pkg/src/obtree, pure Python + numpy) in plain C with IEEE
- * semantics: compiled with -O2 -ffp-contract=off and no fast-math, so float
+ * semantics: compiled with -O3 -ffp-contract=off and no fast-math, so float
  * compares, the binary64 left fold and the two-rounding finalize match numpy
- * bit for bit.  Parity of this restatement is pinned by tests/golden (fixtures
+ * bit for bit (vectorisation runs across independent objects, never across
+ * one object's tree-order sum).  Parity of this restatement is pinned by tests/golden (fixtures
  * produced by the reference itself, see tests/golden/make_golden.py).
  *
  * Model layout shared by every entry point (flat, C order):
@@ -217,21 +218,24 @@ int orc_evaluate_scalar(const float* x, int64_t n, int32_t n_features, int layou
   {
     double* acc64 = (double*)malloc(sizeof(double) * ORC_BLOCK * (size_t)n_outputs);
     float* acc32 = (float*)malloc(sizeof(float) * ORC_BLOCK * (size_t)n_outputs);
+    float* xb = (float*)malloc(sizeof(float) * ORC_BLOCK * (size_t)n_features);
     uint32_t idx[ORC_BLOCK];
 #pragma omp for schedule(dynamic, 4)
     for (int64_t b = 0; b < n_blocks; ++b) {
       const int64_t o0 = b * ORC_BLOCK;
       const int64_t live = (n - o0) < ORC_BLOCK ? (n - o0) : ORC_BLOCK;
+      /* the block's raw values, feature-major, so each split reads one contiguous row */
+      for (int64_t i = 0; i < live; ++i)
+        for (int32_t f = 0; f < n_features; ++f)
+          xb[(int64_t)f * ORC_BLOCK + i] = feature_at(x, n, n_features, layout, o0 + i, f);
       for (int64_t i = 0; i < live * n_outputs; ++i) { acc64[i] = 0.0; acc32[i] = 0.0f; }
       for (int32_t t = 0; t < n_trees; ++t) {
         for (int64_t i = 0; i < live; ++i) idx[i] = 0;
         for (int32_t d = 0; d < depths[t]; ++d) {
           const int32_t f = split_feature[(int64_t)t * max_depth + d];
           const float border = borders[(int64_t)f * border_stride + split_ordinal[(int64_t)t * max_depth + d]];
-          for (int64_t i = 0; i < live; ++i) {
-            const float v = feature_at(x, n, n_features, layout, o0 + i, f);
-            idx[i] |= (v > border ? 1u : 0u) << d;
-          }
+          const float* row = xb + (int64_t)f * ORC_BLOCK;
+          for (int64_t i = 0; i < live; ++i) idx[i] |= (row[i] > border ? 1u : 0u) << d;
         }
         for (int32_t c = 0; c < n_outputs; ++c) {
           const int64_t base = ((int64_t)t * n_outputs + c) * table;
@@ -252,6 +256,7 @@ int orc_evaluate_scalar(const float* x, int64_t n, int32_t n_features, int layou
     }
     free(acc64);
     free(acc32);
+    free(xb);
   }
   free(bank16);
   return 0;

@@ -38,6 +38,11 @@ EXPORTED_SYMBOLS = (
     "obt_predict_host",
     "obt_quantize_dev",
     "obt_leaf_indices_dev",
+    "obt_predict_dev_marked",
+    "obt_event_create",
+    "obt_event_record",
+    "obt_event_elapsed_ms",
+    "obt_event_destroy",
     "obt_last_launch_count",
     "obt_last_error",
     "obt_abi_version",
@@ -105,6 +110,11 @@ def load_library() -> ctypes.CDLL:
         "obt_predict_host": (ctypes.c_int, [vp, vp, i64, i32, vp, vp]),
         "obt_quantize_dev": (ctypes.c_int, [vp, vp, i64, i32, vp, vp]),
         "obt_leaf_indices_dev": (ctypes.c_int, [vp, vp, i64, i32, i32, i32, vp, vp]),
+        "obt_predict_dev_marked": (ctypes.c_int, [vp, vp, i64, i32, vp, vp, sz, vp, vp, vp, vp]),
+        "obt_event_create": (ctypes.c_int, [ctypes.POINTER(vp)]),
+        "obt_event_record": (ctypes.c_int, [vp, vp]),
+        "obt_event_elapsed_ms": (ctypes.c_int, [vp, vp, ctypes.POINTER(ctypes.c_float)]),
+        "obt_event_destroy": (ctypes.c_int, [vp]),
         "obt_last_launch_count": (ctypes.c_int, []),
         "obt_last_error": (ctypes.c_char_p, []),
         "obt_abi_version": (ctypes.c_int, []),
@@ -132,6 +142,30 @@ def require_gpu() -> ctypes.CDLL:
     if not torch.cuda.is_available():
         raise NativeUnavailable("no CUDA device is visible; the B200 kernels have no CPU fallback")
     return lib
+
+
+class Event:
+    """A timing CUDA event owned by the library's runtime (works on torch streams)."""
+
+    def __init__(self):
+        self._lib = load_library()
+        self.handle = ctypes.c_void_p()
+        check(self._lib.obt_event_create(ctypes.byref(self.handle)))
+
+    def record(self, stream: int) -> None:
+        check(self._lib.obt_event_record(self.handle, stream))
+
+    def elapsed_ms(self, end: "Event") -> float:
+        ms = ctypes.c_float()
+        check(self._lib.obt_event_elapsed_ms(self.handle, end.handle, ctypes.byref(ms)))
+        return float(ms.value)
+
+    def __del__(self):
+        try:
+            if self.handle.value:
+                self._lib.obt_event_destroy(self.handle)
+        except Exception:
+            pass
 
 
 def current_stream_handle(device=None) -> int:

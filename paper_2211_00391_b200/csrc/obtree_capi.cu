@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -24,6 +25,7 @@ namespace {
 
 thread_local std::string g_error;
 thread_local int g_launches = 0;
+
 
 int fail(int code, const char* fmt, ...) {
   char buf[1024];
@@ -55,12 +57,9 @@ int instantiated_depth(int d) {
   return -1;
 }
 
-struct ChunkSet {
-  uint8_t* d_chunks = nullptr;
-  int chunk_trees = 0;
-  int n_chunks = 0;
-  uint32_t chunk_bytes = 0;
-  uint32_t desc_bytes = 0;
+struct TilePlan {
+  uint8_t* d_chunks = nullptr;          // [n_chunks][chunk_bytes] descriptor + leaf records
+  std::vector<uint32_t> param_desc;     // [padded_trees][words per tree] for the parameter bank
 };
 
 }  // namespace
@@ -81,14 +80,16 @@ struct obt_model {
   std::vector<uint8_t> split_ordinal;   // [T][DI]
   std::vector<uint8_t> leaf_bytes;      // [T][2^DI] in leaf_storage
   // chunk geometry (independent of the tile size)
+  int padded_trees = 0;
   int chunk_trees = 1, n_chunks = 0;
   uint32_t chunk_bytes = 128, desc_bytes = 0;
   int sm_count = 148;
   int smem_optin = 232448;
   std::mutex mu;
-  std::map<int, ChunkSet> chunks_by_tile;
+  std::map<int, TilePlan> plans;
+  obt::ApplyArgs<1> param_args;  // launch-parameter staging (32 KB), guarded by mu
   ~obt_model() {
-    for (auto& kv : chunks_by_tile) cudaFree(kv.second.d_chunks);
+    for (auto& kv : plans) cudaFree(kv.second.d_chunks);
     if (d_eytz) cudaFree(d_eytz);
   }
 };
@@ -186,95 +187,138 @@ int validate(const obt_model_desc* d) {
   return OBT_OK;
 }
 
-// Chunk geometry: trees per record sized so one record is ~12 KiB (the ring holds
-// kStages of them next to the bucket tile).
-void plan_chunks(obt_model* m) {
-  const int DI = m->depth_inst;
-  const size_t per_tree_desc = (size_t)obt::desc_bytes_per_tree(DI, m->compare_mode);
-  const size_t per_tree = per_tree_desc + (leaf_size(m->leaf_storage) << DI);
-  int ct = (int)std::max<size_t>(1, (12 * 1024) / per_tree);
-  ct = std::min(ct, 64);
-  if (m->n_trees > 0) ct = std::min(ct, m->n_trees);
-  m->chunk_trees = ct;
-  m->n_chunks = m->n_trees > 0 ? (m->n_trees + ct - 1) / ct : 0;
-  m->desc_bytes = (uint32_t)((per_tree_desc * ct + 127) & ~(size_t)127);
-  m->chunk_bytes = (uint32_t)((m->desc_bytes + (leaf_size(m->leaf_storage) << DI) * ct + 127) & ~(size_t)127);
+size_t table_stride(const obt_model* m) {
+  return (size_t)obt::leaf_table_stride(m->depth_inst, (int)leaf_size(m->leaf_storage));
 }
 
-// Descriptor + leaf records for a given tile size (descriptor offsets are f * tile).
-int build_chunks(obt_model* m, int tile, ChunkSet& out) {
+// Chunk geometry: trees per record sized so one record is ~8 KiB (the ring holds
+// kStages of them next to the bucket tile); whole groups of obt::kTreeGroup trees,
+// the model padded with null trees to a multiple of the chunk.
+void plan_chunks(obt_model* m) {
   const int DI = m->depth_inst;
-  const size_t per_tree_leaf = leaf_size(m->leaf_storage) << DI;
-  const int ct = m->chunk_trees;
-  const size_t tree_desc = (size_t)obt::desc_bytes_per_tree(DI, m->compare_mode);
-  const size_t desc_bytes = m->desc_bytes, chunk_bytes = m->chunk_bytes;
-  const int n_chunks = m->n_chunks;
-  std::vector<uint8_t> host((size_t)std::max(n_chunks, 1) * chunk_bytes, 0);
-  for (int t = 0; t < m->n_trees; ++t) {
-    const int c = t / ct, tl = t % ct;
-    uint8_t* rec = host.data() + (size_t)c * chunk_bytes;
-    for (int d = 0; d < DI; ++d) {
-      const int ord = m->split_ordinal[(size_t)t * DI + d];
-      const uint32_t f = ord == kSentinel ? 0u : (uint32_t)m->split_feature[(size_t)t * DI + d];
-      const uint32_t off = f * (uint32_t)tile;
+  const size_t per_tree_desc = (size_t)obt::desc_words_per_tree(DI, m->compare_mode) * 4;
+  const size_t per_tree = per_tree_desc + table_stride(m);
+  const int group = obt::kTreeGroup;
+  int ct = (int)std::max<size_t>(group, (8 * 1024) / per_tree / group * group);
+  ct = std::min(ct, 64);
+  const int groups = (m->n_trees + group - 1) / group;
+  if (groups > 0) ct = std::min(ct, groups * group);
+  m->chunk_trees = ct;
+  m->n_chunks = (m->n_trees + ct - 1) / ct;
+  m->padded_trees = m->n_chunks * ct;
+  m->desc_bytes = (uint32_t)((per_tree_desc * ct + 255) & ~(size_t)255);
+  m->chunk_bytes = (uint32_t)((m->desc_bytes + table_stride(m) * ct + 255) & ~(size_t)255);
+}
+
+// Descriptor words of tree t (padded trees are all-sentinel) for a given tile size.
+void tree_descriptors(const obt_model* m, int t, int tile, uint32_t* out) {
+  const int DI = m->depth_inst, dw = obt::desc_words(m->compare_mode);
+  for (int d = 0; d < DI; ++d) {
+    const int ord = t < m->n_trees ? m->split_ordinal[(size_t)t * DI + d] : kSentinel;
+    uint32_t w0 = 0, w1 = 0;  // sentinel: offset 0, k 0 never carries into bit 7
+    if (ord != kSentinel) {
+      const uint32_t off = (uint32_t)m->split_feature[(size_t)t * DI + d] * (uint32_t)tile;
       if (m->compare_mode == 7) {
-        // q + (127 - ord) >= 128  <=>  q > ord, for q <= 127; sentinel: k = 0 never carries
-        const uint32_t k = ord == kSentinel ? 0u : (uint32_t)(127 - ord) * 0x01010101u;
-        obt::Desc7 ds{off, k};
-        std::memcpy(rec + (size_t)tl * tree_desc + (size_t)d * sizeof(ds), &ds, sizeof(ds));
+        w0 = (off << 8) | (uint32_t)(127 - ord);             // q + 127 - ord >= 128 <=> q > ord
       } else {
-        // ord < 128: bit7(((q & 127) + 127 - ord) | q); ord >= 128: bit7(((q & 127) + 255 - ord) & q)
-        uint32_t k, s;
-        if (ord == kSentinel) { k = 0; s = 0; }
-        else if (ord < 128) { k = (uint32_t)(127 - ord) * 0x01010101u; s = 0xFFFFFFFFu; }
-        else { k = (uint32_t)(255 - ord) * 0x01010101u; s = 0; }
-        obt::Desc8 ds{off, k, s, 0};
-        std::memcpy(rec + (size_t)tl * tree_desc + (size_t)d * sizeof(ds), &ds, sizeof(ds));
+        w0 = (off << 8) | (uint32_t)(127 - (ord & 127));
+        w1 = ord < 128 ? 0xFFFFFFFFu : 0u;                    // or-with-q vs and-with-q
       }
     }
-    std::memcpy(rec + desc_bytes + (size_t)tl * per_tree_leaf,
-                m->leaf_bytes.data() + (size_t)t * per_tree_leaf, per_tree_leaf);
+    out[d * dw] = w0;
+    if (dw == 2) out[d * dw + 1] = w1;
   }
-  out.chunk_trees = ct;
-  out.n_chunks = n_chunks;
-  out.chunk_bytes = (uint32_t)chunk_bytes;
-  out.desc_bytes = (uint32_t)desc_bytes;
+}
+
+// Per-tile-size state: device records (descriptors + leaves) for the shared-memory
+// descriptor path, and the flat descriptor stream for the parameter-bank path.
+int build_tile_plan(obt_model* m, int tile, TilePlan& out) {
+  const int DI = m->depth_inst;
+  const int dwt = obt::desc_words_per_tree(DI, m->compare_mode);
+  const size_t per_tree_leaf = leaf_size(m->leaf_storage) << DI;  // bytes of real leaves
+  const size_t stride = table_stride(m);                           // their slot in the record
+  const int ct = m->chunk_trees;
+  const size_t desc_bytes = m->desc_bytes, chunk_bytes = m->chunk_bytes;
+  std::vector<uint8_t> host((size_t)std::max(m->n_chunks, 1) * chunk_bytes, 0);
+  out.param_desc.assign((size_t)m->padded_trees * dwt, 0u);
+  std::vector<uint32_t> words(dwt);
+  for (int t = 0; t < m->padded_trees; ++t) {
+    const int c = t / ct, tl = t % ct;
+    uint8_t* rec = host.data() + (size_t)c * chunk_bytes;
+    tree_descriptors(m, t, tile, words.data());
+    std::memcpy(out.param_desc.data() + (size_t)t * dwt, words.data(), (size_t)dwt * 4);
+    // shared-memory copy: trees in groups of 4, each group's words contiguous
+    std::memcpy(rec + (size_t)tl * dwt * 4, words.data(), (size_t)dwt * 4);
+    uint8_t* leaf_dst = rec + desc_bytes + (size_t)tl * stride;
+    if (t < m->n_trees) {
+      std::memcpy(leaf_dst, m->leaf_bytes.data() + (size_t)t * per_tree_leaf, per_tree_leaf);
+    } else {
+      // null tree: every leaf is -0.0, the exact identity of IEEE addition
+      for (size_t j = 0; j < ((size_t)1 << DI); ++j) {
+        if (m->leaf_storage == 0) { const double z = -0.0; std::memcpy(leaf_dst + j * 8, &z, 8); }
+        else if (m->leaf_storage == 1) { const float z = -0.0f; std::memcpy(leaf_dst + j * 4, &z, 4); }
+        else { const uint16_t z = 0x8000u; std::memcpy(leaf_dst + j * 2, &z, 2); }
+      }
+    }
+  }
   CUDA_TRY(cudaMalloc(&out.d_chunks, host.size()));
   CUDA_TRY(cudaMemcpy(out.d_chunks, host.data(), host.size(), cudaMemcpyHostToDevice));
   return OBT_OK;
 }
 
-int get_chunks(obt_model* m, int tile, const ChunkSet** out) {
+int get_tile_plan(obt_model* m, int tile, const TilePlan** out) {
   std::lock_guard<std::mutex> lock(m->mu);
-  auto it = m->chunks_by_tile.find(tile);
-  if (it == m->chunks_by_tile.end()) {
-    ChunkSet cs;
-    const int rc = build_chunks(m, tile, cs);
+  auto it = m->plans.find(tile);
+  if (it == m->plans.end()) {
+    TilePlan tp;
+    const int rc = build_tile_plan(m, tile, tp);
     if (rc != OBT_OK) return rc;
-    it = m->chunks_by_tile.emplace(tile, cs).first;
+    it = m->plans.emplace(tile, std::move(tp)).first;
   }
   *out = &it->second;
   return OBT_OK;
 }
 
 constexpr int kStages = 3;
+// Tiles are whole multiples of the quantize kernel's 256-object CTA, so a CTA never
+// straddles two tiles; the apply kernel runs tile / 4 consumer threads + 1 producer warp.
+constexpr int kTileQuantum = obt::kQuantObjects;
+// The parameter-bank descriptor path (no shared-memory traffic for descriptors, one
+// bucket-tile re-read per extra launch) measured ~30% slower per tree than the
+// shared-memory path on B200 (register-indexed LDC chains + unpack ALU ops; see
+// profiles/r01), so it is opt-in (OBT_DESC_SOURCE=param) until that changes.
+constexpr int kMaxParamLaunches = 0;
 
-// Largest tile (multiple of 128 objects, <= 4096) whose bucket tile fits next to the
-// stage ring; then shrink for small batches so the grid still covers the SMs.
+// Largest tile (multiple of 256 objects) whose bucket tile fits next to the stage ring;
+// then shrink for small batches so the grid still covers the SMs.
 int plan_tile(const obt_model* m, int64_t n) {
-  const int64_t fixed = 128 + (int64_t)kStages * m->chunk_bytes;
+  const int64_t fixed = 512 + (int64_t)kStages * m->chunk_bytes;
   int64_t tmax = (m->smem_optin - fixed) / m->n_features;
-  tmax = std::min<int64_t>(tmax / 128 * 128, 4096);
-  if (tmax < 128) return -1;
+  tmax = std::min<int64_t>(tmax / kTileQuantum * kTileQuantum, 3968);
+  if (tmax < kTileQuantum) return -1;
   int64_t want = (n + m->sm_count - 1) / m->sm_count;
-  want = std::max<int64_t>(128, (want + 127) / 128 * 128);
+  want = std::max<int64_t>(kTileQuantum, (want + kTileQuantum - 1) / kTileQuantum * kTileQuantum);
   return (int)std::min(tmax, want);
+}
+
+// Chunks one parameter-bank launch can cover.
+int param_chunks_per_launch(const obt_model* m) {
+  const int words_per_chunk = obt::desc_words_per_tree(m->depth_inst, m->compare_mode) * m->chunk_trees;
+  return obt::kParamDescWords / words_per_chunk;
+}
+
+int use_param_descriptors(const obt_model* m) {
+  const char* e = getenv("OBT_DESC_SOURCE");  // tuning override: "smem" or "param"
+  if (e && !strcmp(e, "smem")) return 0;
+  const int per = param_chunks_per_launch(m);
+  if (per < 1) return 0;
+  if (e && !strcmp(e, "param")) return 1;
+  return (m->n_chunks + per - 1) / per <= kMaxParamLaunches ? 1 : 0;
 }
 
 // ---------------------------------------------------------------------------
 // kernel dispatch
 using QuantFn = void (*)(obt::QuantizeParams);
-using ApplyFn = void (*)(obt::ApplyParams);
 
 template <int L>
 QuantFn quant_fn(int layout, bool tiled) {
@@ -297,34 +341,61 @@ QuantFn pick_quant(int levels, int layout, bool tiled) {
   }
 }
 
-template <int DI, int CMP>
-ApplyFn apply_fn_leaf(int leaf, bool write_idx) {
-  if (write_idx) return obt::apply_kernel<DI, CMP, 1, true>;
-  switch (leaf) {
-    case 0: return obt::apply_kernel<DI, CMP, 0, false>;
-    case 1: return obt::apply_kernel<DI, CMP, 1, false>;
-    default: return obt::apply_kernel<DI, CMP, 2, false>;
-  }
+// Both descriptor sources behind one pointer type: the kernel takes ApplyArgs<DSRC>
+// by value; launches go through cudaLaunchKernel with a pointer to the right struct.
+struct ApplyKernel {
+  const void* fn = nullptr;
+  int dsrc = 0;
+  int words = 1;
+};
+
+// bucket words (4 objects each) per apply thread: 1, or 2 (8 objects per thread: half
+// the threads, each with twice the independent work); OBT_WORDS_PER_THREAD overrides
+int words_per_thread() {
+  static const int w = [] {
+    const char* e = getenv("OBT_WORDS_PER_THREAD");
+    return (e && atoi(e) == 2) ? 2 : 1;
+  }();
+  return w;
+}
+
+template <int DI, int CMP, int DSRC, int W>
+ApplyKernel apply_leaf_w(int leaf, bool write_idx) {
+  ApplyKernel k;
+  k.dsrc = DSRC;
+  k.words = W;
+  if (write_idx) k.fn = (const void*)obt::apply_kernel<DI, CMP, 1, true, W, DSRC>;
+  else if (leaf == 0) k.fn = (const void*)obt::apply_kernel<DI, CMP, 0, false, W, DSRC>;
+  else if (leaf == 1) k.fn = (const void*)obt::apply_kernel<DI, CMP, 1, false, W, DSRC>;
+  else k.fn = (const void*)obt::apply_kernel<DI, CMP, 2, false, W, DSRC>;
+  return k;
+}
+
+template <int DI, int CMP, int DSRC>
+ApplyKernel apply_leaf(int leaf, bool write_idx) {
+  return words_per_thread() == 2 && !write_idx ? apply_leaf_w<DI, CMP, DSRC, 2>(leaf, write_idx)
+                                               : apply_leaf_w<DI, CMP, DSRC, 1>(leaf, write_idx);
 }
 
 template <int DI>
-ApplyFn apply_fn_cmp(int cmp, int leaf, bool write_idx) {
-  return cmp == 7 ? apply_fn_leaf<DI, 7>(leaf, write_idx) : apply_fn_leaf<DI, 8>(leaf, write_idx);
+ApplyKernel apply_di(int cmp, int leaf, bool write_idx, int dsrc) {
+  if (cmp == 7) return dsrc ? apply_leaf<DI, 7, 1>(leaf, write_idx) : apply_leaf<DI, 7, 0>(leaf, write_idx);
+  return dsrc ? apply_leaf<DI, 8, 1>(leaf, write_idx) : apply_leaf<DI, 8, 0>(leaf, write_idx);
 }
 
-ApplyFn pick_apply(int di, int cmp, int leaf, bool write_idx) {
+ApplyKernel pick_apply(int di, int cmp, int leaf, bool write_idx, int dsrc) {
   switch (di) {
-    case 1: return apply_fn_cmp<1>(cmp, leaf, write_idx);
-    case 2: return apply_fn_cmp<2>(cmp, leaf, write_idx);
-    case 3: return apply_fn_cmp<3>(cmp, leaf, write_idx);
-    case 4: return apply_fn_cmp<4>(cmp, leaf, write_idx);
-    case 5: return apply_fn_cmp<5>(cmp, leaf, write_idx);
-    case 6: return apply_fn_cmp<6>(cmp, leaf, write_idx);
-    case 7: return apply_fn_cmp<7>(cmp, leaf, write_idx);
-    case 8: return apply_fn_cmp<8>(cmp, leaf, write_idx);
-    case 10: return apply_fn_cmp<10>(cmp, leaf, write_idx);
-    case 12: return apply_fn_cmp<12>(cmp, leaf, write_idx);
-    default: return nullptr;
+    case 1: return apply_di<1>(cmp, leaf, write_idx, dsrc);
+    case 2: return apply_di<2>(cmp, leaf, write_idx, dsrc);
+    case 3: return apply_di<3>(cmp, leaf, write_idx, dsrc);
+    case 4: return apply_di<4>(cmp, leaf, write_idx, dsrc);
+    case 5: return apply_di<5>(cmp, leaf, write_idx, dsrc);
+    case 6: return apply_di<6>(cmp, leaf, write_idx, dsrc);
+    case 7: return apply_di<7>(cmp, leaf, write_idx, dsrc);
+    case 8: return apply_di<8>(cmp, leaf, write_idx, dsrc);
+    case 10: return apply_di<10>(cmp, leaf, write_idx, dsrc);
+    case 12: return apply_di<12>(cmp, leaf, write_idx, dsrc);
+    default: return ApplyKernel{};
   }
 }
 
@@ -341,48 +412,75 @@ int launch_quantize(const obt_model* m, const float* x, int64_t n, int layout, u
   p.eytz_pitch = m->eytz_pitch;
   p.out = out;
   p.tile = tile;
-  dim3 grid((unsigned)((n_slots + obt::kQuantObjects - 1) / obt::kQuantObjects),
-            (unsigned)((m->n_features + obt::kQuantFeatures - 1) / obt::kQuantFeatures));
-  fn<<<grid, obt::kQuantThreads, 0, stream>>>(p);
+  const size_t smem = obt::quantize_smem_bytes(m->eytz_pitch);
+  CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid((unsigned)((n_slots + obt::kQuantObjects - 1) / obt::kQuantObjects));
+  fn<<<grid, obt::kQuantThreads, smem, stream>>>(p);
   ++g_launches;
   CUDA_TRY(cudaGetLastError());
   return OBT_OK;
 }
 
+// One or more launches of the apply kernel folding all trees in order; with the
+// parameter-bank path each launch carries its trees' descriptors, and launches after
+// the first continue the fold from the accumulators the previous one left in `out`.
 int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, double* out, uint16_t* idx_out,
                  int tree_begin, int tree_end, cudaStream_t stream) {
   const bool write_idx = idx_out != nullptr;
-  const ChunkSet* cs = nullptr;
-  int rc = get_chunks(m, tile, &cs);
+  const TilePlan* tp = nullptr;
+  int rc = get_tile_plan(m, tile, &tp);
   if (rc != OBT_OK) return rc;
-  ApplyFn fn = pick_apply(m->depth_inst, m->compare_mode, m->leaf_storage, write_idx);
-  if (!fn) return fail(OBT_E_UNSUPPORTED, "no apply kernel for depth %d", m->depth_inst);
+  const int dsrc = use_param_descriptors(m);
+  ApplyKernel k = pick_apply(m->depth_inst, m->compare_mode, m->leaf_storage, write_idx, dsrc);
+  if (!k.fn) return fail(OBT_E_UNSUPPORTED, "no apply kernel for depth %d", m->depth_inst);
   const int64_t n_tiles = (n + tile - 1) / tile;
-  const size_t smem = 128 + (size_t)kStages * cs->chunk_bytes + (size_t)m->n_features * tile;
+  const size_t smem = 512 + (size_t)kStages * m->chunk_bytes + (size_t)m->n_features * tile;
   if (smem > (size_t)m->smem_optin)
     return fail(OBT_E_UNSUPPORTED, "tile of %d objects needs %zu bytes of shared memory", tile, smem);
-  CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CUDA_TRY(cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+
   obt::ApplyParams p{};
   p.q = q;
-  p.chunks = cs->d_chunks;
+  p.chunks = tp->d_chunks;
   p.out = out;
   p.idx_out = idx_out;
   p.n = n;
   p.tile = tile;
-  p.n_trees = m->n_trees;
-  p.chunk_trees = cs->chunk_trees;
-  p.n_chunks = cs->n_chunks;
-  p.chunk_bytes = cs->chunk_bytes;
-  p.desc_bytes = cs->desc_bytes;
+  p.chunk_trees = m->chunk_trees;
+  p.chunk_bytes = m->chunk_bytes;
+  p.desc_bytes = m->desc_bytes;
   p.q_tile_bytes = (uint32_t)((size_t)m->n_features * tile);
   p.n_stages = kStages;
   p.tree_begin = tree_begin;
   p.tree_end = tree_end;
   p.scale = m->scale;
   p.bias = m->bias;
-  fn<<<(unsigned)n_tiles, tile / 4, smem, stream>>>(p);
-  ++g_launches;
-  CUDA_TRY(cudaGetLastError());
+  const dim3 grid((unsigned)n_tiles), block((unsigned)(obt::kApplyProducerThreads + tile / (4 * k.words)));
+  const int per = dsrc ? param_chunks_per_launch(m) : std::max(m->n_chunks, 1);
+  const int n_launch = m->n_chunks == 0 ? 1 : (m->n_chunks + per - 1) / per;
+  for (int l = 0; l < n_launch; ++l) {
+    p.chunk_begin = l * per;
+    p.chunk_end = std::min(m->n_chunks, (l + 1) * per);
+    p.first = l == 0;
+    p.last = l == n_launch - 1;
+    if (dsrc) {
+      auto* args = &m->param_args;  // scratch; the driver copies parameters at launch
+      std::lock_guard<std::mutex> lock(m->mu);
+      args->p = p;
+      const size_t words = (size_t)(p.chunk_end - p.chunk_begin) * m->chunk_trees *
+                           obt::desc_words_per_tree(m->depth_inst, m->compare_mode);
+      std::memcpy(args->desc, tp->param_desc.data() +
+                  (size_t)p.chunk_begin * m->chunk_trees * obt::desc_words_per_tree(m->depth_inst, m->compare_mode),
+                  words * 4);
+      void* kargs[] = {args};
+      CUDA_TRY(cudaLaunchKernel(k.fn, grid, block, kargs, smem, stream));
+    } else {
+      obt::ApplyArgs<0> small{p};
+      void* kargs[] = {&small};
+      CUDA_TRY(cudaLaunchKernel(k.fn, grid, block, kargs, smem, stream));
+    }
+    ++g_launches;
+  }
   return OBT_OK;
 }
 
@@ -536,7 +634,8 @@ int obt_workspace_size(const obt_model* m, int64_t n, size_t* bytes) {
 }
 
 static int predict_impl(obt_model* m, const float* x, int64_t n, int32_t layout, double* out, uint16_t* idx_out,
-                        int tree_begin, int tree_end, void* ws, size_t ws_bytes, cudaStream_t stream) {
+                        int tree_begin, int tree_end, void* ws, size_t ws_bytes, cudaStream_t stream,
+                        cudaEvent_t ev_begin = nullptr, cudaEvent_t ev_mid = nullptr, cudaEvent_t ev_end = nullptr) {
   const int tile = plan_tile(m, n);
   if (tile < 0) return fail(OBT_E_UNSUPPORTED, "%d features do not fit a 128-object tile", m->n_features);
   const size_t need = workspace_bytes(m, n, tile);
@@ -548,8 +647,11 @@ static int predict_impl(obt_model* m, const float* x, int64_t n, int32_t layout,
     owned = true;
   }
   const int64_t n_slots = ((n + tile - 1) / tile) * (int64_t)tile;
+  if (ev_begin) CUDA_TRY(cudaEventRecord(ev_begin, stream));
   int rc = launch_quantize(m, x, n, layout, q, true, tile, n_slots, stream);
+  if (rc == OBT_OK && ev_mid) CUDA_TRY(cudaEventRecord(ev_mid, stream));
   if (rc == OBT_OK) rc = launch_apply(m, q, n, tile, out, idx_out, tree_begin, tree_end, stream);
+  if (rc == OBT_OK && ev_end) CUDA_TRY(cudaEventRecord(ev_end, stream));
   if (owned) cudaFreeAsync(q, stream);
   return rc;
 }
@@ -566,6 +668,46 @@ int obt_predict_dev(const obt_model* mc, const float* x, int64_t n, int32_t layo
   if (!x || !out) return fail(OBT_E_INVALID, "null feature or output pointer");
   DeviceGuard guard(m->device);
   return predict_impl(m, x, n, layout, out, nullptr, 0, 0, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int obt_predict_dev_marked(const obt_model* mc, const float* x, int64_t n, int32_t layout, double* out, void* ws,
+                           size_t ws_bytes, void* stream, void* ev_begin, void* ev_mid, void* ev_end) {
+  g_launches = 0;
+  obt_model* m = const_cast<obt_model*>(mc);
+  if (!m) return fail(OBT_E_INVALID, "null model");
+  int rc = check_layout(layout);
+  if (rc != OBT_OK) return rc;
+  if (n <= 0) return n < 0 ? fail(OBT_E_INVALID, "negative object count") : OBT_OK;
+  if (!x || !out) return fail(OBT_E_INVALID, "null feature or output pointer");
+  DeviceGuard guard(m->device);
+  return predict_impl(m, x, n, layout, out, nullptr, 0, 0, ws, ws_bytes, static_cast<cudaStream_t>(stream),
+                      static_cast<cudaEvent_t>(ev_begin), static_cast<cudaEvent_t>(ev_mid),
+                      static_cast<cudaEvent_t>(ev_end));
+}
+
+int obt_event_create(void** event) {
+  if (!event) return fail(OBT_E_INVALID, "null event pointer");
+  cudaEvent_t e;
+  CUDA_TRY(cudaEventCreate(&e));
+  *event = e;
+  return OBT_OK;
+}
+
+int obt_event_record(void* event, void* stream) {
+  CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(event), static_cast<cudaStream_t>(stream)));
+  return OBT_OK;
+}
+
+int obt_event_elapsed_ms(void* start, void* end, float* ms) {
+  if (!ms) return fail(OBT_E_INVALID, "null output");
+  CUDA_TRY(cudaEventSynchronize(static_cast<cudaEvent_t>(end)));
+  CUDA_TRY(cudaEventElapsedTime(ms, static_cast<cudaEvent_t>(start), static_cast<cudaEvent_t>(end)));
+  return OBT_OK;
+}
+
+int obt_event_destroy(void* event) {
+  if (event) CUDA_TRY(cudaEventDestroy(static_cast<cudaEvent_t>(event)));
+  return OBT_OK;
 }
 
 int obt_leaf_indices_dev(const obt_model* mc, const float* x, int64_t n, int32_t layout, int32_t tree_begin,

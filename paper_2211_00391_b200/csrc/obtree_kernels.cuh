@@ -50,7 +50,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "{\n"
       ".reg .pred p;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
@@ -90,90 +90,163 @@ struct QuantizeParams {
   int32_t tile;          // TILE (tiled output only)
 };
 
-constexpr int kQuantObjects = 32;     // objects per CTA (one per lane)
-constexpr int kQuantFeatures = 256;   // feature chunk per CTA (grid.y covers F)
+constexpr int kQuantObjects = 256;    // objects per CTA: 8 per lane, 8 independent searches
+constexpr int kQuantChunk = 16;       // features staged per pass
 constexpr int kQuantThreads = 256;
 
-// bucket of x against one feature's Eytzinger array: i <- 2i + 1 + [x > e_i], L times.
-template <int L>
-__device__ __forceinline__ uint32_t eytz_bucket(float x, const float* __restrict__ e) {
-  uint32_t i = 0;
-#pragma unroll
-  for (int l = 0; l < L; ++l) {
-    const float b = __ldg(e + i);
-    i = 2 * i + 1 + (x > b ? 1u : 0u);
-  }
-  return i - ((1u << L) - 1u);
+__host__ __device__ constexpr size_t quantize_smem_bytes(int eytz_pitch) {
+  return (size_t)kQuantObjects * (kQuantChunk + 1) * 4      // raw values, odd pitch
+         + (size_t)kQuantChunk * eytz_pitch * 4             // the chunk's Eytzinger arrays
+         + (size_t)kQuantChunk * kQuantObjects;             // bucket rows
 }
 
+// One CTA: 256 objects x all features, 16 features per pass.  Raw values and the
+// pass's Eytzinger arrays are staged in shared memory with coalesced loads; each lane
+// then runs 8 branchless searches (i <- 2i + 1 + [x > e_i], L levels) in lockstep, so
+// the dependent smem loads of one search overlap the other seven.  Bucket rows are
+// staged and leave as 16-byte stores into the tile-blocked matrix.
 template <int L, int LAYOUT, bool TILED>
 __global__ void __launch_bounds__(kQuantThreads) quantize_kernel(QuantizeParams p) {
-  __shared__ float xs[kQuantObjects * (kQuantFeatures + 1)];
+  extern __shared__ __align__(16) unsigned char qsm[];
+  constexpr int kPitch = kQuantChunk + 1;
+  constexpr int kPer = kQuantObjects / 32;
+  constexpr int kE = (1 << L) - 1;
+  float* xs = reinterpret_cast<float*>(qsm);
+  float* ey = xs + kQuantObjects * kPitch;
+  uint8_t* qs = reinterpret_cast<uint8_t*>(ey + (size_t)kQuantChunk * (kE > 0 ? kE : 1));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t o0 = (int64_t)blockIdx.x * kQuantObjects;
-  const int f0 = blockIdx.y * kQuantFeatures;
-  const int nf = min(kQuantFeatures, p.n_features - f0);
-  constexpr int kPitch = kQuantFeatures + 1;  // odd pitch: column reads are conflict-free
-  if (LAYOUT == 0) {
-    // object-major: each warp copies whole row segments (coalesced) into smem.
-    for (int r = warp; r < kQuantObjects; r += kQuantThreads / 32) {
-      const int64_t o = o0 + r;
-      const float* row = p.x + o * p.n_features + f0;
-      for (int f = lane; f < nf; f += 32) xs[r * kPitch + f] = (o < p.n) ? __ldg(row + f) : 0.0f;
+  const int F = p.n_features;
+
+  for (int f0 = 0; f0 < F; f0 += kQuantChunk) {
+    const int nf = min(kQuantChunk, F - f0);
+    if (LAYOUT == 0) {
+      // rows of the object-major matrix: lanes 0..15 read one object's chunk, 16..31 the next
+      for (int r = threadIdx.x >> 4; r < kQuantObjects; r += kQuantThreads / 16) {
+        const int c = threadIdx.x & 15;
+        const int64_t o = o0 + r;
+        float v = 0.0f;
+        if (c < nf && o < p.n) v = __ldg(p.x + o * F + f0 + c);
+        xs[r * kPitch + c] = v;
+      }
+    } else {
+      for (int fl = warp; fl < nf; fl += kQuantThreads / 32) {
+        const float* row = p.x + (int64_t)(f0 + fl) * p.n;
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+          const int64_t o = o0 + lane + 32 * j;
+          xs[(lane + 32 * j) * kPitch + fl] = (o < p.n) ? __ldg(row + o) : 0.0f;
+        }
+      }
+    }
+    if (kE > 0) {
+      const float* src = p.eytz + (int64_t)f0 * p.eytz_pitch;
+      for (int i = threadIdx.x; i < nf * kE; i += kQuantThreads) ey[i] = __ldg(src + i);
     }
     __syncthreads();
-  }
-  const int64_t o = o0 + lane;
-  for (int fl = warp; fl < nf; fl += kQuantThreads / 32) {
-    const int f = f0 + fl;
-    float x;
-    if (LAYOUT == 0) x = xs[lane * kPitch + fl];
-    else x = (o < p.n) ? __ldg(p.x + (int64_t)f * p.n + o) : 0.0f;
-    uint32_t q = eytz_bucket<L>(x, p.eytz + (int64_t)f * p.eytz_pitch);
-    if (TILED) {
-      if (o >= p.n) q = 0;  // padding slots are zero (quantize.py:172)
-      const int64_t t = o / p.tile, w = o - t * p.tile;
-      p.out[(t * p.n_features + f) * p.tile + w] = (uint8_t)q;
-    } else if (o < p.n) {
-      p.out[(int64_t)f * p.n + o] = (uint8_t)q;
+    for (int fl = warp; fl < nf; fl += kQuantThreads / 32) {
+      // branchless Eytzinger walk on absolute shared addresses: with a = base + 4i,
+      // i' = 2i + 1 + [x > e_i]  <=>  a' = 2a + (4 - base) + 4[x > e_i]
+      const uint32_t base = smem_u32(ey) + 4u * (uint32_t)(fl * kE);
+      const uint32_t c0 = 4u - base, c1 = 8u - base;
+      float x[kPer];
+      uint32_t a[kPer];
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) { x[j] = xs[(lane + 32 * j) * kPitch + fl]; a[j] = base; }
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+          // LDS, FSETP, SEL, IADD3: one search level
+          asm volatile(
+              "{\n"
+              ".reg .pred gt;\n"
+              ".reg .f32 b;\n"
+              ".reg .u32 t;\n"
+              "ld.shared.f32 b, [%0];\n"
+              "setp.gt.f32 gt, %1, b;\n"
+              "selp.u32 t, %2, %3, gt;\n"
+              "add.u32 %0, %0, %0;\n"
+              "add.u32 %0, %0, t;\n"
+              "}\n"
+              : "+r"(a[j])
+              : "f"(x[j]), "r"(c1), "r"(c0));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        const int64_t o = o0 + lane + 32 * j;
+        const uint32_t i = (a[j] - base) >> 2;  // leaf position E..2E of the implicit tree
+        const uint32_t q = (o < p.n) ? i - (uint32_t)kE : 0u;  // padding slots are zero (quantize.py:172)
+        qs[fl * kQuantObjects + lane + 32 * j] = (uint8_t)q;
+      }
     }
+    __syncthreads();
+    if (TILED) {
+      // 16-byte stores: each feature row of the CTA is 256 contiguous bytes of the tile
+      const int64_t t = o0 / p.tile, w = o0 - t * p.tile;
+      for (int v = threadIdx.x; v < nf * (kQuantObjects / 16); v += kQuantThreads) {
+        const int fl = v / (kQuantObjects / 16), c = v % (kQuantObjects / 16);
+        const uint4 val = reinterpret_cast<const uint4*>(qs + fl * kQuantObjects)[c];
+        uint8_t* dst = p.out + (t * F + f0 + fl) * (int64_t)p.tile + w + 16 * c;
+        *reinterpret_cast<uint4*>(dst) = val;
+      }
+    } else {
+      for (int v = threadIdx.x; v < nf * kQuantObjects; v += kQuantThreads) {
+        const int fl = v / kQuantObjects, c = v % kQuantObjects;
+        const int64_t o = o0 + c;
+        if (o < p.n) p.out[(int64_t)(f0 + fl) * p.n + o] = qs[v];
+      }
+    }
+    __syncthreads();
   }
 }
 
 // ---------------------------------------------------------------------------
 // K2: tree apply.
+//
+// A split descriptor is one 32-bit word (off << 8) | k (plus, in 8-bit mode, a second
+// word s): off = byte offset of the feature's row in the bucket tile, and adding k
+// replicated to the 4 bytes of a bucket word carries [q > ordinal] into bit 7 of each:
+//   7-bit mode (all buckets <= 127): k = 127 - ordinal;                  sentinel k = 0
+//   8-bit mode: k = 127 - (ordinal & 127), s = all-ones iff ordinal < 128;
+//               condition = bit7(((q & 127) + k) | q) if ordinal < 128
+//                         = bit7(((q & 127) + k) & q) otherwise;          sentinel k = s = 0
+// Descriptors come either from the kernel-parameter bank (DSRC 1: uniform loads, no
+// shared-memory traffic; a launch covers as many trees as the 32 KB parameter space
+// holds and the next launch continues the same fold from the carried accumulators),
+// or from the shared-memory ring next to the leaves (DSRC 0, any model size).
+// Trees are processed in groups of 4 whose descriptors are contiguous (LDS.128 in
+// DSRC 0); the tree count is padded to a multiple of 4 with null trees whose splits
+// are sentinels and whose leaves are -0.0, and x + (-0.0) == x exactly for every x,
+// so padding never changes a bit of the fold.
+constexpr int kTreeGroup = 4;
+__host__ __device__ constexpr int desc_words(int cmp) { return cmp == 7 ? 1 : 2; }
+__host__ __device__ constexpr int desc_words_per_tree(int di, int cmp) { return di * desc_words(cmp); }
+
 struct ApplyParams {
   const uint8_t* q;          // tiled buckets [n_tiles][F][tile]
   const uint8_t* chunks;     // [n_chunks][chunk_bytes] descriptor+leaf records
-  double* out;               // [n] predictions (accumulate mode)
+  double* out;               // [n] predictions; also the fold carry between launches
   uint16_t* idx_out;         // [tree_end - tree_begin][n] (index mode)
   int64_t n;
   int32_t tile;
-  int32_t n_trees;
   int32_t chunk_trees;
-  int32_t n_chunks;
-  uint32_t chunk_bytes;      // multiple of 128
-  uint32_t desc_bytes;       // descriptor part of a record (multiple of 16)
+  int32_t chunk_begin, chunk_end;  // chunks (of chunk_trees trees) this launch folds
+  uint32_t chunk_bytes;      // multiple of 256
+  uint32_t desc_bytes;       // descriptor part of a record (multiple of 256)
   uint32_t q_tile_bytes;     // F * tile
   int32_t n_stages;
-  int32_t tree_begin, tree_end;
+  int32_t tree_begin, tree_end;  // index mode: trees written
+  int32_t first, last;       // start the fold at 0 / finalize into predictions
   double scale, bias;
 };
 
-// Descriptor of one (tree, depth) split.  off = byte offset of the feature's row in
-// the bucket tile; k = per-byte addend that carries [q > ordinal] into bit 7;
-// s = all-ones when ordinal < 128 (8-bit compare mode only).  A tree's descriptors
-// are padded to a multiple of 16 bytes so they load as LDS.128 broadcasts.
-struct alignas(8) Desc7 { uint32_t off, k; };
-struct alignas(16) Desc8 { uint32_t off, k, s, pad; };
+constexpr int kParamDescWords = 7936;  // 31744 bytes of descriptors + ApplyParams < 32764
 
-template <int CMP> struct DescT;
-template <> struct DescT<7> { using D = Desc7; };
-template <> struct DescT<8> { using D = Desc8; };
-
-__host__ __device__ constexpr int desc_bytes_per_tree(int di, int cmp) {
-  return cmp == 7 ? ((di * 8 + 15) / 16) * 16 : di * 16;
-}
+template <int DSRC> struct ApplyArgs;
+template <> struct ApplyArgs<0> { ApplyParams p; };
+template <> struct ApplyArgs<1> { ApplyParams p; uint32_t desc[kParamDescWords]; };
 
 template <int LEAF> struct LeafT;
 template <> struct LeafT<0> { using T = double; using Acc = double; static constexpr int kShift = 3;
@@ -193,116 +266,213 @@ __device__ __forceinline__ uint32_t byte_of(uint32_t w) {
   return __byte_perm(w, 0u, 0x4440u | K);
 }
 
-template <int DI, int CMP, int LEAF, bool WRITE_IDX>
-__global__ void __launch_bounds__(1024, 1) apply_kernel(ApplyParams p) {
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+// W consecutive bucket words (4W objects) of one feature row.
+template <int W>
+__device__ __forceinline__ void lds_words(uint32_t addr, uint32_t (&w)[W]) {
+  if constexpr (W == 1) {
+    w[0] = lds_u32(addr);
+  } else if constexpr (W == 2) {
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w[0]), "=r"(w[1]) : "r"(addr));
+  } else {
+    static_assert(W == 4, "1, 2 or 4 bucket words per thread");
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "r"(addr));
+  }
+}
+
+// Leaf loads by 32-bit shared address.
+template <int LEAF> __device__ __forceinline__ typename LeafT<LEAF>::T lds_leaf(uint32_t addr);
+template <> __device__ __forceinline__ double lds_leaf<0>(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+template <> __device__ __forceinline__ float lds_leaf<1>(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+template <> __device__ __forceinline__ __half lds_leaf<2>(uint32_t addr) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+  return __ushort_as_half(v);
+}
+
+// Leaf-table stride in a stage: prescaled tables sit on 256-byte boundaries so the
+// gather address is one PRMT: (index byte) into byte 0 of the table's base address.
+__host__ __device__ constexpr int leaf_table_stride(int di, int leaf_bytes) {
+  return (1 << di) * leaf_bytes <= 256 ? 256 : (1 << di) * leaf_bytes;
+}
+
+constexpr int kApplyProducerThreads = 32;
+
+template <int DI, int CMP, int LEAF, bool WRITE_IDX, int W, int DSRC>
+__global__ void __launch_bounds__(1024, 1) apply_kernel(const __grid_constant__ ApplyArgs<DSRC> args) {
+  const ApplyParams& p = args.p;
   using LT = LeafT<LEAF>;
-  using leaf_t = typename LT::T;
   using acc_t = typename LT::Acc;
-  using Desc = typename DescT<CMP>::D;
-  constexpr int kLeaves = 1 << DI;
-  constexpr int kTreeDescBytes = desc_bytes_per_tree(DI, CMP);
+  constexpr int kDW = desc_words(CMP);
+  constexpr int kTabStride = leaf_table_stride(DI, (int)sizeof(typename LT::T));
   // When the scaled index still fits a byte, the SWAR words carry byte offsets
   // (index << kShift) directly and a gather is PRMT + LDS.
   constexpr bool kPrescaled = !WRITE_IDX && (DI + LT::kShift) <= 8;
   constexpr int kBitBase = kPrescaled ? LT::kShift : 0;
 
-  extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);  // [0] tile, [1 + s] stage s
-  unsigned char* stages = smem + 128;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  // 256-byte aligned working base (the host reserves 256 bytes of slack)
+  unsigned char* smem = smem_raw + ((256u - (smem_u32(smem_raw) & 255u)) & 255u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);    // [S]   stage landed
+  uint64_t* empty = full + 8;                            // [S]   stage consumed
+  uint64_t* tile_bar = full + 16;
+  unsigned char* stages = smem + 256;
   unsigned char* qtile = stages + (size_t)p.n_stages * p.chunk_bytes;
 
   const int tid = threadIdx.x;
+  const int n_consumer_warps = (blockDim.x - kApplyProducerThreads) / 32;
   const int64_t tile_idx = blockIdx.x;
+  const int n_chunks = p.chunk_end - p.chunk_begin;
   if (tid == 0) {
-    for (int i = 0; i <= p.n_stages; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < p.n_stages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], n_consumer_warps);
+    }
+    mbar_init(tile_bar, 1);
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid == 0) {
-    mbar_expect_tx(&bars[0], p.q_tile_bytes);
-    bulk_g2s_split(qtile, p.q + tile_idx * (int64_t)p.q_tile_bytes, p.q_tile_bytes, &bars[0]);
-    const int pre = p.n_chunks < p.n_stages ? p.n_chunks : p.n_stages;
-    for (int s = 0; s < pre; ++s) {
-      mbar_expect_tx(&bars[1 + s], p.chunk_bytes);
-      bulk_g2s_split(stages + (size_t)s * p.chunk_bytes, p.chunks + (size_t)s * p.chunk_bytes,
-                     p.chunk_bytes, &bars[1 + s]);
+
+  if (tid < kApplyProducerThreads) {
+    // producer warp: the bucket tile once, then the leaf (+descriptor) ring
+    if (tid == 0) {
+      mbar_expect_tx(tile_bar, p.q_tile_bytes);
+      bulk_g2s_split(qtile, p.q + tile_idx * (int64_t)p.q_tile_bytes, p.q_tile_bytes, tile_bar);
+      for (int c = 0; c < n_chunks; ++c) {
+        const int s = c % p.n_stages;
+        if (c >= p.n_stages) mbar_wait(&empty[s], (uint32_t)(c / p.n_stages - 1) & 1u);
+        mbar_expect_tx(&full[s], p.chunk_bytes);
+        bulk_g2s_split(stages + (size_t)s * p.chunk_bytes,
+                       p.chunks + (size_t)(p.chunk_begin + c) * p.chunk_bytes, p.chunk_bytes, &full[s]);
+      }
     }
+    return;
   }
-  mbar_wait(&bars[0], 0);
 
-  const unsigned char* my_q = qtile + 4 * tid;  // this thread's 4 objects in every row
-  const int64_t obj0 = tile_idx * p.tile + 4 * tid;
-  acc_t acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
-
-  for (int c = 0; c < p.n_chunks; ++c) {
-    const int s = c % p.n_stages;
-    mbar_wait(&bars[1 + s], (uint32_t)(c / p.n_stages) & 1u);
-    const unsigned char* st = stages + (size_t)s * p.chunk_bytes;
-    const unsigned char* leaf_base = st + p.desc_bytes;
-    const int t_base = c * p.chunk_trees;
-    const int nt = min(p.chunk_trees, p.n_trees - t_base);
-#pragma unroll 2
-    for (int t = 0; t < nt; ++t) {
-      const Desc* desc = reinterpret_cast<const Desc*>(st + t * kTreeDescBytes);
-      uint32_t lo = 0, hi = 0;
+  const int ctid = tid - kApplyProducerThreads;
+  const int lane = tid & 31;
+  constexpr int kObj = 4 * W;                            // objects per thread
+  const uint32_t my_q = smem_u32(qtile) + kObj * ctid;   // this thread's words in every row
+  const int64_t obj0 = tile_idx * p.tile + kObj * ctid;
+  acc_t acc[kObj];
 #pragma unroll
-      for (int d = 0; d < DI; ++d) {
-        const Desc ds = desc[d];
-        const uint32_t w = *reinterpret_cast<const uint32_t*>(my_q + ds.off);
-        uint32_t b7;  // [q > ordinal] in bit 7 of each byte, garbage below
-        if constexpr (CMP == 7) {
-          b7 = w + ds.k;
-        } else {
-          b7 = maj3((w & 0x7f7f7f7fu) + ds.k, w, ds.s);
-        }
-        const int pos = d + kBitBase;  // target bit of condition d inside each byte
-        if (pos < 8) lo |= (pos == 7 ? b7 : (b7 >> (7 - pos))) & (0x01010101u << pos);
-        else hi |= (pos == 15 ? b7 : (b7 >> (15 - pos))) & (0x01010101u << (pos - 8));
-      }
-      uint32_t i0, i1, i2, i3;
-      if constexpr (DI > 8) {
-        i0 = byte_of<0>(lo) | (byte_of<0>(hi) << 8);
-        i1 = byte_of<1>(lo) | (byte_of<1>(hi) << 8);
-        i2 = byte_of<2>(lo) | (byte_of<2>(hi) << 8);
-        i3 = byte_of<3>(lo) | (byte_of<3>(hi) << 8);
-      } else {
-        i0 = byte_of<0>(lo);
-        i1 = byte_of<1>(lo);
-        i2 = byte_of<2>(lo);
-        i3 = byte_of<3>(lo);
-      }
-      if constexpr (WRITE_IDX) {
-        const int tg = t_base + t;
-        if (tg >= p.tree_begin && tg < p.tree_end) {
-          uint16_t* row = p.idx_out + (int64_t)(tg - p.tree_begin) * p.n;
-          if (obj0 + 0 < p.n) row[obj0 + 0] = (uint16_t)i0;
-          if (obj0 + 1 < p.n) row[obj0 + 1] = (uint16_t)i1;
-          if (obj0 + 2 < p.n) row[obj0 + 2] = (uint16_t)i2;
-          if (obj0 + 3 < p.n) row[obj0 + 3] = (uint16_t)i3;
+  for (int k = 0; k < kObj; ++k) {
+    // continue the fold of the previous launch (exact: the carry holds acc_t values)
+    acc[k] = (p.first || WRITE_IDX || obj0 + k >= p.n) ? (acc_t)0 : (acc_t)p.out[obj0 + k];
+  }
+  mbar_wait(tile_bar, 0);
+
+  const int launch_tree0 = p.chunk_begin * p.chunk_trees;
+  for (int c = 0; c < n_chunks; ++c) {
+    const int s = c % p.n_stages;
+    mbar_wait(&full[s], (uint32_t)(c / p.n_stages) & 1u);
+    const unsigned char* st = stages + (size_t)s * p.chunk_bytes;
+    const uint32_t leaf_base = smem_u32(st + p.desc_bytes);
+    const int t_base = (p.chunk_begin + c) * p.chunk_trees;
+    for (int g = 0; g < p.chunk_trees / kTreeGroup; ++g) {
+      uint32_t dw[kTreeGroup * DI * kDW];
+      if constexpr (DSRC == 0) {
+        const uint4* dsrc = reinterpret_cast<const uint4*>(st + (size_t)g * kTreeGroup * DI * kDW * 4);
+#pragma unroll
+        for (int v = 0; v < DI * kDW; ++v) {
+          const uint4 q4 = dsrc[v];
+          dw[4 * v + 0] = q4.x; dw[4 * v + 1] = q4.y; dw[4 * v + 2] = q4.z; dw[4 * v + 3] = q4.w;
         }
       } else {
-        const unsigned char* tab = leaf_base + (size_t)t * (kLeaves * sizeof(leaf_t));
-        constexpr int kSh = kPrescaled ? 0 : LT::kShift;
-        acc0 += LT::widen(*reinterpret_cast<const leaf_t*>(tab + (i0 << kSh)));
-        acc1 += LT::widen(*reinterpret_cast<const leaf_t*>(tab + (i1 << kSh)));
-        acc2 += LT::widen(*reinterpret_cast<const leaf_t*>(tab + (i2 << kSh)));
-        acc3 += LT::widen(*reinterpret_cast<const leaf_t*>(tab + (i3 << kSh)));
+        const int base = (t_base - launch_tree0 + g * kTreeGroup) * DI * kDW;
+#pragma unroll
+        for (int v = 0; v < kTreeGroup * DI * kDW; ++v) dw[v] = args.desc[base + v];
+      }
+#pragma unroll
+      for (int tt = 0; tt < kTreeGroup; ++tt) {
+        const int t = g * kTreeGroup + tt;
+        uint32_t lo_even[W], lo_odd[W], hi[W];
+#pragma unroll
+        for (int x = 0; x < W; ++x) { lo_even[x] = 0; lo_odd[x] = 0; hi[x] = 0; }
+#pragma unroll
+        for (int d = 0; d < DI; ++d) {
+          const uint32_t ds = dw[(tt * DI + d) * kDW];
+          uint32_t w[W];
+          lds_words<W>(my_q + (ds >> 8), w);
+          const uint32_t krep = __byte_perm(ds, 0u, 0x0000u);
+#pragma unroll
+          for (int x = 0; x < W; ++x) {
+            uint32_t b7;  // [q > ordinal] in bit 7 of each byte, garbage below
+            if constexpr (CMP == 7) {
+              b7 = w[x] + krep;
+            } else {
+              b7 = maj3((w[x] & 0x7f7f7f7fu) + (krep & 0x7f7f7f7fu), w[x], dw[(tt * DI + d) * kDW + 1]);
+            }
+            const int pos = d + kBitBase;  // target bit of condition d inside each byte
+            if (pos < 8) {
+              const uint32_t term = (pos == 7 ? b7 : (b7 >> (7 - pos))) & (0x01010101u << pos);
+              if (d & 1) lo_odd[x] |= term; else lo_even[x] |= term;
+            } else {
+              hi[x] |= (pos == 15 ? b7 : (b7 >> (15 - pos))) & (0x01010101u << (pos - 8));
+            }
+          }
+        }
+#pragma unroll
+        for (int x = 0; x < W; ++x) {
+          const uint32_t lo = lo_even[x] | lo_odd[x];
+          if constexpr (WRITE_IDX) {
+            const int tg = t_base + t;
+            if (tg >= p.tree_begin && tg < p.tree_end) {
+              uint16_t* row = p.idx_out + (int64_t)(tg - p.tree_begin) * p.n;
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const uint32_t idx = ((lo >> (8 * k)) & 0xffu) | (DI > 8 ? ((hi[x] >> (8 * k)) & 0xffu) << 8 : 0u);
+                if (obj0 + 4 * x + k < p.n) row[obj0 + 4 * x + k] = (uint16_t)idx;
+              }
+            }
+          } else if constexpr (kPrescaled) {
+            const uint32_t tab = leaf_base + (uint32_t)t * 256u;
+            acc[4 * x + 0] += LT::widen(lds_leaf<LEAF>(__byte_perm(lo, tab, 0x7650u)));
+            acc[4 * x + 1] += LT::widen(lds_leaf<LEAF>(__byte_perm(lo, tab, 0x7651u)));
+            acc[4 * x + 2] += LT::widen(lds_leaf<LEAF>(__byte_perm(lo, tab, 0x7652u)));
+            acc[4 * x + 3] += LT::widen(lds_leaf<LEAF>(__byte_perm(lo, tab, 0x7653u)));
+          } else {
+            const uint32_t tab = leaf_base + (uint32_t)t * kTabStride;
+            uint32_t ix[4];
+            ix[0] = byte_of<0>(lo); ix[1] = byte_of<1>(lo); ix[2] = byte_of<2>(lo); ix[3] = byte_of<3>(lo);
+            if constexpr (DI > 8) {
+              ix[0] |= byte_of<0>(hi[x]) << 8; ix[1] |= byte_of<1>(hi[x]) << 8;
+              ix[2] |= byte_of<2>(hi[x]) << 8; ix[3] |= byte_of<3>(hi[x]) << 8;
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) acc[4 * x + k] += LT::widen(lds_leaf<LEAF>(tab + (ix[k] << LT::kShift)));
+          }
+        }
       }
     }
-    __syncthreads();  // every thread is done reading stage s
-    if (tid == 0 && c + p.n_stages < p.n_chunks) {
-      mbar_expect_tx(&bars[1 + s], p.chunk_bytes);
-      bulk_g2s_split(stages + (size_t)s * p.chunk_bytes,
-                     p.chunks + (size_t)(c + p.n_stages) * p.chunk_bytes, p.chunk_bytes, &bars[1 + s]);
-    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done reading stage s
   }
 
   if constexpr (!WRITE_IDX) {
-    // finalize: f64(acc) * scale + bias, two roundings (evaluate.py:298-299, oracle.py:53-54)
-    const double a[4] = {(double)acc0, (double)acc1, (double)acc2, (double)acc3};
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (obj0 + k < p.n) p.out[obj0 + k] = __dadd_rn(__dmul_rn(a[k], p.scale), p.bias);
+    for (int k = 0; k < kObj; ++k) {
+      if (obj0 + k < p.n) {
+        // finalize: f64(acc) * scale + bias, two roundings (evaluate.py:298-299, oracle.py:53-54)
+        p.out[obj0 + k] = p.last ? __dadd_rn(__dmul_rn((double)acc[k], p.scale), p.bias) : (double)acc[k];
+      }
     }
   }
 }

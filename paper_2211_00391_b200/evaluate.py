@@ -169,16 +169,20 @@ class Evaluator:
     def leaf_storage(self) -> str:
         return self._dev.leaf_storage
 
-    def predict(self, matrix) -> np.ndarray:
+    def predict(self, matrix, out: Optional[np.ndarray] = None) -> np.ndarray:
         """Raw scores for every object, in input order (reference evaluate.py:268-300).
 
-        A ``FeatureMatrix`` (host memory) returns a float64 ndarray; a CUDA tensor is
-        routed to ``predict_device`` and returns a CUDA float64 tensor."""
+        A ``FeatureMatrix`` (host memory) returns a float64 ndarray (written into
+        ``out`` when given, e.g. a pinned buffer); a CUDA tensor is routed to
+        ``predict_device`` and returns a CUDA float64 tensor."""
         if not isinstance(matrix, FeatureMatrix):
             return self.predict_device(matrix)
         _check_features(matrix.n_features, self.model)
         n = matrix.n_objects
-        out = np.empty(n, dtype=np.float64)
+        if out is None:
+            out = np.empty(n, dtype=np.float64)
+        elif out.dtype != np.float64 or out.shape != (n,) or not out.flags.c_contiguous:
+            raise ValueError("out must be a contiguous float64 array of one score per object")
         if n == 0:
             return out
         import torch
@@ -221,6 +225,28 @@ class Evaluator:
             )
         )
         return out
+
+    def predict_device_marked(self, x, events, layout: Layout = Layout.OBJECT_MAJOR, out=None, workspace=None):
+        """``predict_device`` recording three ``_native.Event``s around the two kernels."""
+        import torch
+
+        n = x.shape[0] if layout is Layout.OBJECT_MAJOR else x.shape[1]
+        if out is None:
+            out = torch.empty(n, dtype=torch.float64, device=x.device)
+        ws_ptr, ws_bytes = (0, 0)
+        if workspace is not None:
+            ws_ptr, ws_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
+        stream = _native.current_stream_handle(x.device)
+        ev = [e.handle if e is not None else None for e in events]
+        _native.check(
+            self._dev._lib.obt_predict_dev_marked(
+                self._dev.handle, x.data_ptr(), n, layout_code(layout), out.data_ptr(), ws_ptr, ws_bytes, stream, *ev
+            )
+        )
+        return out
+
+    def last_launch_count(self) -> int:
+        return int(self._dev._lib.obt_last_launch_count())
 
     def workspace_bytes(self, n_objects: int) -> int:
         size = ctypes.c_size_t()

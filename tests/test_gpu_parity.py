@@ -221,3 +221,22 @@ def test_predict_deeper_than_reference(D):
     finally:
         lib.obt_model_destroy(h)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("source", ["param", "smem"])
+@pytest.mark.parametrize("strategy", [obt.LeafStrategy.NAIVE, obt.LeafStrategy.NAIVE16])
+def test_descriptor_sources_and_multi_launch_fold(monkeypatch, source, strategy):
+    """3,000 depth-6 trees exceed one launch's parameter bank (about 1,300 trees), so the
+    parameter path folds across 3 launches through the carried accumulators; the
+    shared-memory path streams all descriptors in one launch.  Both are bit-exact."""
+    monkeypatch.setenv("OBT_DESC_SOURCE", source)
+    model = _model(12, 50, 3001, 6, seed=77)
+    x = _features(model, 2500, seed=78)
+    prec = oracle.BINARY64 if strategy is obt.LeafStrategy.NAIVE else oracle.BINARY16
+    want = oracle.evaluate_scalar(oracle.flatten(model), x, oracle.OBJECT_MAJOR, prec)
+    ev = obt.Evaluator(model, obt.EvalConfig(strategy=strategy))
+    got = ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
+    assert np.array_equal(got, want)
+    idx = stages.as_uint16(stages.leaf_indices(model, torch.from_numpy(x).cuda(), tree_begin=1290, tree_end=1400))
+    fm = oracle.flatten(model)
+    assert np.array_equal(idx, oracle.leaf_indices(fm, oracle.quantize(fm, x))[1290:1400])
