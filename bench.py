@@ -248,6 +248,8 @@ def run_ours(args, world, rank, local):
     spec = synthetic.CONFIGS[args.config]
     if args.objects:
         spec = synthetic.WorkloadSpec(**{**spec.__dict__, "n_objects": args.objects})
+    if args.trees:
+        spec = synthetic.WorkloadSpec(**{**spec.__dict__, "n_trees": args.trees})
     device = local
     torch.cuda.set_device(device)
     model = synthetic.build_model(spec)
@@ -366,6 +368,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4])
     ap.add_argument("--objects", type=int, default=0, help="override objects per GPU")
+    ap.add_argument("--trees", type=int, default=0, help="override the tree count (experiments)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -47,6 +47,7 @@ int fail(int code, const char* fmt, ...) {
 constexpr int kMaxBorders = 254;  // model.py:21
 constexpr int kMaxDepth = 12;     // smem-staged leaf tables (2^12 fp32 = 16 KiB per tree)
 constexpr int kSentinel = 255;    // evaluate.py:32
+constexpr int kStages = 3;        // records in flight in the apply kernel's ring
 
 // Instantiated depths of the apply kernel; a model of depth D runs on the
 // smallest instantiation >= D with sentinel (never-true) padding splits.
@@ -191,15 +192,21 @@ size_t table_stride(const obt_model* m) {
   return (size_t)obt::leaf_table_stride(m->depth_inst, (int)leaf_size(m->leaf_storage));
 }
 
-// Chunk geometry: trees per record sized so one record is ~8 KiB (the ring holds
-// kStages of them next to the bucket tile); whole groups of obt::kTreeGroup trees,
-// the model padded with null trees to a multiple of the chunk.
+// Chunk geometry: the ring of kStages records gets what the bucket tile leaves of the
+// shared memory; records hold whole groups of obt::tree_group(depth) trees, and the
+// model is padded with null trees to a multiple of the chunk.
 void plan_chunks(obt_model* m) {
   const int DI = m->depth_inst;
   const size_t per_tree_desc = (size_t)obt::desc_words_per_tree(DI, m->compare_mode) * 4;
   const size_t per_tree = per_tree_desc + table_stride(m);
-  const int group = obt::kTreeGroup;
-  int ct = (int)std::max<size_t>(group, (8 * 1024) / per_tree / group * group);
+  const int group = obt::tree_group(DI);
+  // ring budget: what the bucket tile of the largest 256-quantum tile leaves over
+  const int64_t avail = (int64_t)m->smem_optin - 512;
+  const int64_t tile_cap = 4 * (obt::kApplyMaxThreads - obt::kApplyProducerThreads) / 256 * 256;
+  const int64_t tile_objs = std::min<int64_t>(
+      tile_cap, std::max<int64_t>(256, (avail - (int64_t)kStages * 4096) / m->n_features / 256 * 256));
+  const int64_t ring = std::max<int64_t>((int64_t)kStages * per_tree * group, avail - tile_objs * m->n_features);
+  int ct = (int)std::max<int64_t>(group, (ring / kStages - 512) / (int64_t)per_tree / group * group);
   ct = std::min(ct, 64);
   const int groups = (m->n_trees + group - 1) / group;
   if (groups > 0) ct = std::min(ct, groups * group);
@@ -210,23 +217,25 @@ void plan_chunks(obt_model* m) {
   m->chunk_bytes = (uint32_t)((m->desc_bytes + table_stride(m) * ct + 255) & ~(size_t)255);
 }
 
-// Descriptor words of tree t (padded trees are all-sentinel) for a given tile size.
+// Descriptor words of tree t (padded trees are all-sentinel) for a given tile size:
+// 7-bit compare {off, k replicated}; 8-bit compare {(off << 8) | k, s}.
 void tree_descriptors(const obt_model* m, int t, int tile, uint32_t* out) {
-  const int DI = m->depth_inst, dw = obt::desc_words(m->compare_mode);
+  const int DI = m->depth_inst;
   for (int d = 0; d < DI; ++d) {
     const int ord = t < m->n_trees ? m->split_ordinal[(size_t)t * DI + d] : kSentinel;
     uint32_t w0 = 0, w1 = 0;  // sentinel: offset 0, k 0 never carries into bit 7
     if (ord != kSentinel) {
       const uint32_t off = (uint32_t)m->split_feature[(size_t)t * DI + d] * (uint32_t)tile;
       if (m->compare_mode == 7) {
-        w0 = (off << 8) | (uint32_t)(127 - ord);             // q + 127 - ord >= 128 <=> q > ord
+        w0 = off;
+        w1 = (uint32_t)(127 - ord) * 0x01010101u;              // q + 127 - ord >= 128 <=> q > ord
       } else {
         w0 = (off << 8) | (uint32_t)(127 - (ord & 127));
         w1 = ord < 128 ? 0xFFFFFFFFu : 0u;                    // or-with-q vs and-with-q
       }
     }
-    out[d * dw] = w0;
-    if (dw == 2) out[d * dw + 1] = w1;
+    out[2 * d] = w0;
+    out[2 * d + 1] = w1;
   }
 }
 
@@ -240,13 +249,13 @@ int build_tile_plan(obt_model* m, int tile, TilePlan& out) {
   const int ct = m->chunk_trees;
   const size_t desc_bytes = m->desc_bytes, chunk_bytes = m->chunk_bytes;
   std::vector<uint8_t> host((size_t)std::max(m->n_chunks, 1) * chunk_bytes, 0);
-  out.param_desc.assign((size_t)m->padded_trees * dwt, 0u);
+  out.param_desc.assign((size_t)m->padded_trees * DI * 2, 0u);
   std::vector<uint32_t> words(dwt);
   for (int t = 0; t < m->padded_trees; ++t) {
     const int c = t / ct, tl = t % ct;
     uint8_t* rec = host.data() + (size_t)c * chunk_bytes;
     tree_descriptors(m, t, tile, words.data());
-    std::memcpy(out.param_desc.data() + (size_t)t * dwt, words.data(), (size_t)dwt * 4);
+    if (m->compare_mode == 7) std::memcpy(out.param_desc.data() + (size_t)t * DI * 2, words.data(), (size_t)DI * 8);
     // shared-memory copy: trees in groups of 4, each group's words contiguous
     std::memcpy(rec + (size_t)tl * dwt * 4, words.data(), (size_t)dwt * 4);
     uint8_t* leaf_dst = rec + desc_bytes + (size_t)tl * stride;
@@ -279,7 +288,6 @@ int get_tile_plan(obt_model* m, int tile, const TilePlan** out) {
   return OBT_OK;
 }
 
-constexpr int kStages = 3;
 // Tiles are whole multiples of the quantize kernel's 256-object CTA, so a CTA never
 // straddles two tiles; the apply kernel runs tile / 4 consumer threads + 1 producer warp.
 constexpr int kTileQuantum = obt::kQuantObjects;
@@ -294,7 +302,7 @@ constexpr int kMaxParamLaunches = 0;
 int plan_tile(const obt_model* m, int64_t n) {
   const int64_t fixed = 512 + (int64_t)kStages * m->chunk_bytes;
   int64_t tmax = (m->smem_optin - fixed) / m->n_features;
-  tmax = std::min<int64_t>(tmax / kTileQuantum * kTileQuantum, 3968);
+  tmax = std::min<int64_t>(tmax / kTileQuantum * kTileQuantum, 4 * (obt::kApplyMaxThreads - obt::kApplyProducerThreads) / kTileQuantum * kTileQuantum);
   if (tmax < kTileQuantum) return -1;
   int64_t want = (n + m->sm_count - 1) / m->sm_count;
   want = std::max<int64_t>(kTileQuantum, (want + kTileQuantum - 1) / kTileQuantum * kTileQuantum);
@@ -303,13 +311,14 @@ int plan_tile(const obt_model* m, int64_t n) {
 
 // Chunks one parameter-bank launch can cover.
 int param_chunks_per_launch(const obt_model* m) {
-  const int words_per_chunk = obt::desc_words_per_tree(m->depth_inst, m->compare_mode) * m->chunk_trees;
+  const int words_per_chunk = 2 * m->depth_inst * m->chunk_trees;
   return obt::kParamDescWords / words_per_chunk;
 }
 
 int use_param_descriptors(const obt_model* m) {
   const char* e = getenv("OBT_DESC_SOURCE");  // tuning override: "smem" or "param"
   if (e && !strcmp(e, "smem")) return 0;
+  if (m->compare_mode != 7) return 0;
   const int per = param_chunks_per_launch(m);
   if (per < 1) return 0;
   if (e && !strcmp(e, "param")) return 1;
@@ -373,14 +382,19 @@ ApplyKernel apply_leaf_w(int leaf, bool write_idx) {
 
 template <int DI, int CMP, int DSRC>
 ApplyKernel apply_leaf(int leaf, bool write_idx) {
-  return words_per_thread() == 2 && !write_idx ? apply_leaf_w<DI, CMP, DSRC, 2>(leaf, write_idx)
-                                               : apply_leaf_w<DI, CMP, DSRC, 1>(leaf, write_idx);
+  if constexpr (DSRC == 1) {
+    return apply_leaf_w<DI, CMP, 1, 1>(leaf, write_idx);
+  } else {
+    return words_per_thread() == 2 && !write_idx ? apply_leaf_w<DI, CMP, DSRC, 2>(leaf, write_idx)
+                                                 : apply_leaf_w<DI, CMP, DSRC, 1>(leaf, write_idx);
+  }
 }
 
 template <int DI>
 ApplyKernel apply_di(int cmp, int leaf, bool write_idx, int dsrc) {
+  // parameter-bank descriptors exist for the 7-bit compare only
   if (cmp == 7) return dsrc ? apply_leaf<DI, 7, 1>(leaf, write_idx) : apply_leaf<DI, 7, 0>(leaf, write_idx);
-  return dsrc ? apply_leaf<DI, 8, 1>(leaf, write_idx) : apply_leaf<DI, 8, 0>(leaf, write_idx);
+  return apply_leaf<DI, 8, 0>(leaf, write_idx);
 }
 
 ApplyKernel pick_apply(int di, int cmp, int leaf, bool write_idx, int dsrc) {
@@ -467,11 +481,9 @@ int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, double* ou
       auto* args = &m->param_args;  // scratch; the driver copies parameters at launch
       std::lock_guard<std::mutex> lock(m->mu);
       args->p = p;
-      const size_t words = (size_t)(p.chunk_end - p.chunk_begin) * m->chunk_trees *
-                           obt::desc_words_per_tree(m->depth_inst, m->compare_mode);
-      std::memcpy(args->desc, tp->param_desc.data() +
-                  (size_t)p.chunk_begin * m->chunk_trees * obt::desc_words_per_tree(m->depth_inst, m->compare_mode),
-                  words * 4);
+      const size_t per_tree = 2 * (size_t)m->depth_inst;
+      const size_t words = (size_t)(p.chunk_end - p.chunk_begin) * m->chunk_trees * per_tree;
+      std::memcpy(args->desc, tp->param_desc.data() + (size_t)p.chunk_begin * m->chunk_trees * per_tree, words * 4);
       void* kargs[] = {args};
       CUDA_TRY(cudaLaunchKernel(k.fn, grid, block, kargs, smem, stream));
     } else {

@@ -45,16 +45,31 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ uint32_t mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
+  return ok;
+}
+
+// Single-thread wait (the producer): back off with nanosleep so a waiting producer
+// does not steal issue slots from the consumer warps of its SM sub-partition.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try(bar, parity)) __nanosleep(64);
+}
+
+// Whole-warp wait whose retry branch is warp-uniform (vote), so code after it stays in
+// uniform control flow and loop counters can live in uniform registers.
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+  while (!__all_sync(0xffffffffu, mbar_try(bar, parity))) {
+  }
 }
 
 // global -> shared bulk copy; bytes % 16 == 0, both addresses 16-byte aligned.
@@ -220,8 +235,10 @@ __global__ void __launch_bounds__(kQuantThreads) quantize_kernel(QuantizeParams 
 // DSRC 0); the tree count is padded to a multiple of 4 with null trees whose splits
 // are sentinels and whose leaves are -0.0, and x + (-0.0) == x exactly for every x,
 // so padding never changes a bit of the fold.
-constexpr int kTreeGroup = 4;
-__host__ __device__ constexpr int desc_words(int cmp) { return cmp == 7 ? 1 : 2; }
+// 16 trees per group keep ~100 independent shared loads in flight per thread; deep
+// trees (large leaf tables) use groups of 4 so a chunk of them still fits the ring.
+__host__ __device__ constexpr int tree_group(int di) { return di <= 8 ? 16 : 4; }
+__host__ __device__ constexpr int desc_words(int cmp) { return 2; }
 __host__ __device__ constexpr int desc_words_per_tree(int di, int cmp) { return di * desc_words(cmp); }
 
 struct ApplyParams {
@@ -314,10 +331,13 @@ __host__ __device__ constexpr int leaf_table_stride(int di, int leaf_bytes) {
 }
 
 constexpr int kApplyProducerThreads = 32;
+// Block size cap: 128 registers per thread keep several tree groups of loads in flight.
+constexpr int kApplyMaxThreads = 512;
 
 template <int DI, int CMP, int LEAF, bool WRITE_IDX, int W, int DSRC>
-__global__ void __launch_bounds__(1024, 1) apply_kernel(const __grid_constant__ ApplyArgs<DSRC> args) {
+__global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid_constant__ ApplyArgs<DSRC> args) {
   const ApplyParams& p = args.p;
+  constexpr int kTreeGroup = tree_group(DI);
   using LT = LeafT<LEAF>;
   using acc_t = typename LT::Acc;
   constexpr int kDW = desc_words(CMP);
@@ -343,14 +363,17 @@ __global__ void __launch_bounds__(1024, 1) apply_kernel(const __grid_constant__ 
   if (tid == 0) {
     for (int i = 0; i < p.n_stages; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], n_consumer_warps);
+      mbar_init(&empty[i], n_consumer_warps * 32);  // every consumer thread arrives
     }
     mbar_init(tile_bar, 1);
     fence_mbar_init();
   }
   __syncthreads();
 
-  if (tid < kApplyProducerThreads) {
+  // warp index broadcast from lane 0: provably warp-uniform, so the role split below is
+  // a uniform branch and the consumer loop counters can live in uniform registers
+  const int warp_id = __shfl_sync(0xffffffffu, tid / 32, 0);
+  if (warp_id == 0) {
     // producer warp: the bucket tile once, then the leaf (+descriptor) ring
     if (tid == 0) {
       mbar_expect_tx(tile_bar, p.q_tile_bytes);
@@ -367,7 +390,6 @@ __global__ void __launch_bounds__(1024, 1) apply_kernel(const __grid_constant__ 
   }
 
   const int ctid = tid - kApplyProducerThreads;
-  const int lane = tid & 31;
   constexpr int kObj = 4 * W;                            // objects per thread
   const uint32_t my_q = smem_u32(qtile) + kObj * ctid;   // this thread's words in every row
   const int64_t obj0 = tile_idx * p.tile + kObj * ctid;
@@ -377,29 +399,28 @@ __global__ void __launch_bounds__(1024, 1) apply_kernel(const __grid_constant__ 
     // continue the fold of the previous launch (exact: the carry holds acc_t values)
     acc[k] = (p.first || WRITE_IDX || obj0 + k >= p.n) ? (acc_t)0 : (acc_t)p.out[obj0 + k];
   }
-  mbar_wait(tile_bar, 0);
+  mbar_wait_warp(tile_bar, 0);
 
-  const int launch_tree0 = p.chunk_begin * p.chunk_trees;
   for (int c = 0; c < n_chunks; ++c) {
     const int s = c % p.n_stages;
-    mbar_wait(&full[s], (uint32_t)(c / p.n_stages) & 1u);
+    mbar_wait_warp(&full[s], (uint32_t)(c / p.n_stages) & 1u);
     const unsigned char* st = stages + (size_t)s * p.chunk_bytes;
     const uint32_t leaf_base = smem_u32(st + p.desc_bytes);
     const int t_base = (p.chunk_begin + c) * p.chunk_trees;
     for (int g = 0; g < p.chunk_trees / kTreeGroup; ++g) {
-      uint32_t dw[kTreeGroup * DI * kDW];
+      uint32_t dw[DSRC == 0 ? kTreeGroup * DI * kDW : 1];
       if constexpr (DSRC == 0) {
         const uint4* dsrc = reinterpret_cast<const uint4*>(st + (size_t)g * kTreeGroup * DI * kDW * 4);
 #pragma unroll
-        for (int v = 0; v < DI * kDW; ++v) {
+        for (int v = 0; v < kTreeGroup * DI * kDW / 4; ++v) {
           const uint4 q4 = dsrc[v];
           dw[4 * v + 0] = q4.x; dw[4 * v + 1] = q4.y; dw[4 * v + 2] = q4.z; dw[4 * v + 3] = q4.w;
         }
-      } else {
-        const int base = (t_base - launch_tree0 + g * kTreeGroup) * DI * kDW;
-#pragma unroll
-        for (int v = 0; v < kTreeGroup * DI * kDW; ++v) dw[v] = args.desc[base + v];
       }
+      // parameter-bank descriptors of this group: {off, k replicated} word pairs; the
+      // index is a function of uniform loop counters only, so they load as LDCU.64 and
+      // feed LDS [R + UR] and IADD R, UR directly
+      const int gbase = (c * (p.chunk_trees / kTreeGroup) + g) * (kTreeGroup * DI * 2);
 #pragma unroll
       for (int tt = 0; tt < kTreeGroup; ++tt) {
         const int t = g * kTreeGroup + tt;
@@ -408,19 +429,32 @@ __global__ void __launch_bounds__(1024, 1) apply_kernel(const __grid_constant__ 
         for (int x = 0; x < W; ++x) { lo_even[x] = 0; lo_odd[x] = 0; hi[x] = 0; }
 #pragma unroll
         for (int d = 0; d < DI; ++d) {
-          const uint32_t ds = dw[(tt * DI + d) * kDW];
           uint32_t w[W];
-          lds_words<W>(my_q + (ds >> 8), w);
-          const uint32_t krep = __byte_perm(ds, 0u, 0x0000u);
+          uint32_t b7s[W];  // [q > ordinal] in bit 7 of each byte, garbage below
+          if constexpr (DSRC == 1) {
+            static_assert(CMP == 7 && W == 1, "parameter-bank descriptors: 7-bit compare, 4 objects per thread");
+            const uint32_t off = args.desc[gbase + 2 * (tt * DI + d)];
+            const uint32_t krep = args.desc[gbase + 2 * (tt * DI + d) + 1];
+            w[0] = lds_u32(my_q + off);
+            b7s[0] = w[0] + krep;
+          } else {
+            // shared-memory descriptors: 7-bit {off, k replicated}; 8-bit {(off << 8) | k, s}
+            const uint32_t d0 = dw[(tt * DI + d) * kDW], d1 = dw[(tt * DI + d) * kDW + 1];
+            if constexpr (CMP == 7) {
+              lds_words<W>(my_q + d0, w);
+#pragma unroll
+              for (int x = 0; x < W; ++x) b7s[x] = w[x] + d1;
+            } else {
+              lds_words<W>(my_q + (d0 >> 8), w);
+              const uint32_t k = __byte_perm(d0, 0u, 0x0000u) & 0x7f7f7f7fu;
+#pragma unroll
+              for (int x = 0; x < W; ++x) b7s[x] = maj3((w[x] & 0x7f7f7f7fu) + k, w[x], d1);
+            }
+          }
 #pragma unroll
           for (int x = 0; x < W; ++x) {
-            uint32_t b7;  // [q > ordinal] in bit 7 of each byte, garbage below
-            if constexpr (CMP == 7) {
-              b7 = w[x] + krep;
-            } else {
-              b7 = maj3((w[x] & 0x7f7f7f7fu) + (krep & 0x7f7f7f7fu), w[x], dw[(tt * DI + d) * kDW + 1]);
-            }
-            const int pos = d + kBitBase;  // target bit of condition d inside each byte
+            const uint32_t b7 = b7s[x];
+          const int pos = d + kBitBase;  // target bit of condition d inside each byte
             if (pos < 8) {
               const uint32_t term = (pos == 7 ? b7 : (b7 >> (7 - pos))) & (0x01010101u << pos);
               if (d & 1) lo_odd[x] |= term; else lo_even[x] |= term;
@@ -462,8 +496,7 @@ __global__ void __launch_bounds__(1024, 1) apply_kernel(const __grid_constant__ 
         }
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done reading stage s
+    mbar_arrive(&empty[s]);  // this thread is done reading stage s (no divergent branch)
   }
 
   if constexpr (!WRITE_IDX) {
