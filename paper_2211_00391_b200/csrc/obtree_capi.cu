@@ -426,9 +426,12 @@ int launch_quantize(const obt_model* m, const float* x, int64_t n, int layout, u
   p.eytz_pitch = m->eytz_pitch;
   p.out = out;
   p.tile = tile;
-  const size_t smem = obt::quantize_smem_bytes(m->eytz_pitch);
+  const int fc = obt::quantize_chunk_features(m->levels > 0 ? m->eytz_pitch : 0, m->n_features);
+  const size_t smem = m->levels > 0 ? (size_t)std::min(fc, m->n_features) * m->eytz_pitch * 4 : 16;
+  p.chunk_features = fc;
+  p.two = 2;
   CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid((unsigned)((n_slots + obt::kQuantObjects - 1) / obt::kQuantObjects));
+  dim3 grid((unsigned)((n_slots + obt::kQuantBlock - 1) / obt::kQuantBlock), (unsigned)((m->n_features + fc - 1) / fc));
   fn<<<grid, obt::kQuantThreads, smem, stream>>>(p);
   ++g_launches;
   CUDA_TRY(cudaGetLastError());

@@ -103,117 +103,129 @@ struct QuantizeParams {
   int32_t eytz_pitch;    // 2^levels - 1
   uint8_t* out;          // tiled [tile][F][TILE] or plain [F][n]
   int32_t tile;          // TILE (tiled output only)
+  int32_t chunk_features;  // features per CTA (grid.y chunks), a multiple of 8
+  int32_t two;             // the constant 2, passed at run time (see eytz_level)
 };
 
-constexpr int kQuantObjects = 256;    // objects per CTA: 8 per lane, 8 independent searches
-constexpr int kQuantChunk = 16;       // features staged per pass
-constexpr int kQuantThreads = 256;
+constexpr int kQuantObjects = 256;    // tile quantum: tiles are whole multiples of this
+constexpr int kQuantThreads = 256;    // 8 warps x 128 objects = 1024 objects per CTA
+constexpr int kQuantBlock = 1024;
+constexpr int kQuantSmem = 48 * 1024; // Eytzinger arrays of one feature chunk
 
-__host__ __device__ constexpr size_t quantize_smem_bytes(int eytz_pitch) {
-  return (size_t)kQuantObjects * (kQuantChunk + 1) * 4      // raw values, odd pitch
-         + (size_t)kQuantChunk * eytz_pitch * 4             // the chunk's Eytzinger arrays
-         + (size_t)kQuantChunk * kQuantObjects;             // bucket rows
+// Features per CTA chunk (grid.y): as many whole quads as fit kQuantSmem.
+__host__ __device__ constexpr int quantize_chunk_features(int eytz_pitch, int n_features) {
+  return eytz_pitch <= 0 ? ((n_features + 7) / 8 * 8)
+         : (kQuantSmem / (eytz_pitch * 4) / 8 * 8 > 0 ? kQuantSmem / (eytz_pitch * 4) / 8 * 8 : 8);
 }
 
-// One CTA: 256 objects x all features, 16 features per pass.  Raw values and the
-// pass's Eytzinger arrays are staged in shared memory with coalesced loads; each lane
-// then runs 8 branchless searches (i <- 2i + 1 + [x > e_i], L levels) in lockstep, so
-// the dependent smem loads of one search overlap the other seven.  Bucket rows are
-// staged and leave as 16-byte stores into the tile-blocked matrix.
-template <int L, int LAYOUT, bool TILED>
-__global__ void __launch_bounds__(kQuantThreads) quantize_kernel(QuantizeParams p) {
-  extern __shared__ __align__(16) unsigned char qsm[];
-  constexpr int kPitch = kQuantChunk + 1;
-  constexpr int kPer = kQuantObjects / 32;
-  constexpr int kE = (1 << L) - 1;
-  float* xs = reinterpret_cast<float*>(qsm);
-  float* ey = xs + kQuantObjects * kPitch;
-  uint8_t* qs = reinterpret_cast<uint8_t*>(ey + (size_t)kQuantChunk * (kE > 0 ? kE : 1));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t o0 = (int64_t)blockIdx.x * kQuantObjects;
-  const int F = p.n_features;
+// One level of the branchless Eytzinger walk, on byte offsets o = 4i into the shared
+// array: i' = 2i + 1 + [x > e_i]  <=>  o' = two * o + (x > e_i ? 8 : 4).  `two` is the
+// runtime value 2 (a kernel parameter) so the update is an IMAD on the FMA pipe; plain
+// C++ (no asm) lets the compiler interleave the independent searches of a lane.
+// NaN compares false and walks left, giving bucket 0 (quantize.py:171).
+__device__ __forceinline__ uint32_t eytz_level(uint32_t o, float x, const float* e, uint32_t two) {
+  const float b = *reinterpret_cast<const float*>(reinterpret_cast<const unsigned char*>(e) + o);
+  return o * two + (x > b ? 8u : 4u);
+}
 
-  for (int f0 = 0; f0 < F; f0 += kQuantChunk) {
-    const int nf = min(kQuantChunk, F - f0);
-    if (LAYOUT == 0) {
-      // rows of the object-major matrix: lanes 0..15 read one object's chunk, 16..31 the next
-      for (int r = threadIdx.x >> 4; r < kQuantObjects; r += kQuantThreads / 16) {
-        const int c = threadIdx.x & 15;
-        const int64_t o = o0 + r;
-        float v = 0.0f;
-        if (c < nf && o < p.n) v = __ldg(p.x + o * F + f0 + c);
-        xs[r * kPitch + c] = v;
-      }
-    } else {
-      for (int fl = warp; fl < nf; fl += kQuantThreads / 32) {
-        const float* row = p.x + (int64_t)(f0 + fl) * p.n;
+constexpr int kQuantStep = 8;  // features per step: two 16-byte loads = one 32-byte sector per row
+
+// One CTA: 1024 objects (8 warps x 32 lanes x 4 objects) x one chunk of features
+// (grid.y).  The chunk's Eytzinger arrays are staged in shared memory once; each lane
+// then walks its 4 objects x 8 features per step: full 32-byte sectors of the raw values
+// straight from HBM, 32 independent searches, 8 packed 32-bit bucket stores (each warp
+// writes 128 contiguous bytes of a feature row of the tile-blocked matrix).
+template <int L, int LAYOUT, bool TILED>
+__global__ void __launch_bounds__(kQuantThreads, 2) quantize_kernel(QuantizeParams p) {
+  extern __shared__ __align__(16) unsigned char qsm[];
+  constexpr int kE = (1 << L) - 1;
+  constexpr int S = kQuantStep;
+  float* ey = reinterpret_cast<float*>(qsm);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int F = p.n_features;
+  const int fc = p.chunk_features;
+  const int f0 = blockIdx.y * fc;
+  const int nf = min(fc, F - f0);
+  if (kE > 0) {
+    const float* src = p.eytz + (int64_t)f0 * kE;
+    for (int i = threadIdx.x; i < nf * kE; i += kQuantThreads) ey[i] = __ldg(src + i);
+  }
+  __syncthreads();
+
+  const int64_t ob = (int64_t)blockIdx.x * kQuantBlock + warp * 128 + 4 * lane;  // first of my 4 objects
+  if (ob >= p.n_slots) return;  // past the last tile (no barrier follows)
+  const bool full_objs = ob + 3 < p.n;
+  const bool vec_rows = LAYOUT == 0 ? ((F & 3) == 0 && (f0 & 3) == 0) : ((p.n & 3) == 0);
+  const uint32_t two = (uint32_t)p.two;
+  for (int fq = 0; fq < nf; fq += S) {
+    // raw values v[j][k]: object ob + k, feature f0 + fq + j
+    float v[S][4];
+    if (full_objs && vec_rows && fq + S <= nf) {
+      if (LAYOUT == 0) {
 #pragma unroll
-        for (int j = 0; j < kPer; ++j) {
-          const int64_t o = o0 + lane + 32 * j;
-          xs[(lane + 32 * j) * kPitch + fl] = (o < p.n) ? __ldg(row + o) : 0.0f;
+        for (int k = 0; k < 4; ++k) {
+          const float4* row = reinterpret_cast<const float4*>(p.x + (ob + k) * F + f0 + fq);
+#pragma unroll
+          for (int h = 0; h < S / 4; ++h) {
+            const float4 q = __ldg(row + h);
+            v[4 * h + 0][k] = q.x; v[4 * h + 1][k] = q.y; v[4 * h + 2][k] = q.z; v[4 * h + 3][k] = q.w;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+          const float4 q = __ldg(reinterpret_cast<const float4*>(p.x + (int64_t)(f0 + fq + j) * p.n + ob));
+          v[j][0] = q.x; v[j][1] = q.y; v[j][2] = q.z; v[j][3] = q.w;
         }
       }
-    }
-    if (kE > 0) {
-      const float* src = p.eytz + (int64_t)f0 * p.eytz_pitch;
-      for (int i = threadIdx.x; i < nf * kE; i += kQuantThreads) ey[i] = __ldg(src + i);
-    }
-    __syncthreads();
-    for (int fl = warp; fl < nf; fl += kQuantThreads / 32) {
-      // branchless Eytzinger walk on absolute shared addresses: with a = base + 4i,
-      // i' = 2i + 1 + [x > e_i]  <=>  a' = 2a + (4 - base) + 4[x > e_i]
-      const uint32_t base = smem_u32(ey) + 4u * (uint32_t)(fl * kE);
-      const uint32_t c0 = 4u - base, c1 = 8u - base;
-      float x[kPer];
-      uint32_t a[kPer];
-#pragma unroll
-      for (int j = 0; j < kPer; ++j) { x[j] = xs[(lane + 32 * j) * kPitch + fl]; a[j] = base; }
-#pragma unroll
-      for (int l = 0; l < L; ++l) {
-#pragma unroll
-        for (int j = 0; j < kPer; ++j) {
-          // LDS, FSETP, SEL, IADD3: one search level
-          asm volatile(
-              "{\n"
-              ".reg .pred gt;\n"
-              ".reg .f32 b;\n"
-              ".reg .u32 t;\n"
-              "ld.shared.f32 b, [%0];\n"
-              "setp.gt.f32 gt, %1, b;\n"
-              "selp.u32 t, %2, %3, gt;\n"
-              "add.u32 %0, %0, %0;\n"
-              "add.u32 %0, %0, t;\n"
-              "}\n"
-              : "+r"(a[j])
-              : "f"(x[j]), "r"(c1), "r"(c0));
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < kPer; ++j) {
-        const int64_t o = o0 + lane + 32 * j;
-        const uint32_t i = (a[j] - base) >> 2;  // leaf position E..2E of the implicit tree
-        const uint32_t q = (o < p.n) ? i - (uint32_t)kE : 0u;  // padding slots are zero (quantize.py:172)
-        qs[fl * kQuantObjects + lane + 32 * j] = (uint8_t)q;
-      }
-    }
-    __syncthreads();
-    if (TILED) {
-      // 16-byte stores: each feature row of the CTA is 256 contiguous bytes of the tile
-      const int64_t t = o0 / p.tile, w = o0 - t * p.tile;
-      for (int v = threadIdx.x; v < nf * (kQuantObjects / 16); v += kQuantThreads) {
-        const int fl = v / (kQuantObjects / 16), c = v % (kQuantObjects / 16);
-        const uint4 val = reinterpret_cast<const uint4*>(qs + fl * kQuantObjects)[c];
-        uint8_t* dst = p.out + (t * F + f0 + fl) * (int64_t)p.tile + w + 16 * c;
-        *reinterpret_cast<uint4*>(dst) = val;
-      }
     } else {
-      for (int v = threadIdx.x; v < nf * kQuantObjects; v += kQuantThreads) {
-        const int fl = v / kQuantObjects, c = v % kQuantObjects;
-        const int64_t o = o0 + c;
-        if (o < p.n) p.out[(int64_t)(f0 + fl) * p.n + o] = qs[v];
+#pragma unroll
+      for (int j = 0; j < S; ++j)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const bool in = ob + k < p.n && fq + j < nf;
+          const int64_t idx = LAYOUT == 0 ? (ob + k) * F + f0 + fq + j : (int64_t)(f0 + fq + j) * p.n + ob + k;
+          v[j][k] = in ? __ldg(p.x + idx) : 0.0f;
+        }
+    }
+    uint32_t o[S][4];
+#pragma unroll
+    for (int j = 0; j < S; ++j)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) o[j][k] = 0;
+#pragma unroll
+    for (int l = 0; l < L; ++l)
+#pragma unroll
+      for (int j = 0; j < S; ++j) {
+        const float* e = ey + min(fq + j, nf - 1) * kE;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) o[j][k] = eytz_level(o[j][k], v[j][k], e, two);
+      }
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      if (fq + j >= nf) break;
+      uint32_t word = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        // bucket = leaf position - E; padding objects are zero (quantize.py:172)
+        const uint32_t q = (o[j][k] >> 2) - (uint32_t)kE;
+        word |= q << (8 * k);
+      }
+      if (!full_objs) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (ob + k >= p.n) word &= ~(0xFFu << (8 * k));
+      }
+      const int f = f0 + fq + j;
+      if (TILED) {
+        const int64_t t = ob / p.tile, w = ob - t * p.tile;
+        *reinterpret_cast<uint32_t*>(p.out + (t * F + f) * (int64_t)p.tile + w) = word;
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (ob + k < p.n) p.out[(int64_t)f * p.n + ob + k] = (uint8_t)(word >> (8 * k));
       }
     }
-    __syncthreads();
   }
 }
 
