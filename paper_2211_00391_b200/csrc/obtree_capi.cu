@@ -554,6 +554,15 @@ int obt_model_create(const obt_model_desc* d, int device, obt_model** out) {
   m->bias = d->bias;
   m->depth_inst = d->n_trees > 0 ? instantiated_depth(d->max_depth) : 1;
   CUDA_TRY(cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount, device));
+  {
+    // keep stream-ordered workspace allocations cached between calls instead of
+    // returning them to the driver at every synchronisation
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   CUDA_TRY(cudaDeviceGetAttribute(&m->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
 
   // borders -> Eytzinger arrays
