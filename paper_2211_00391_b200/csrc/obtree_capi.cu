@@ -58,6 +58,12 @@ int instantiated_depth(int d) {
   return -1;
 }
 
+struct BorderTable {
+  float* d = nullptr;  // [F][pitch] Eytzinger order, +inf padded
+  int levels = 0;
+  int pitch = 1;
+};
+
 struct TilePlan {
   uint8_t* d_chunks = nullptr;          // [n_chunks][chunk_bytes] descriptor + leaf records
   std::vector<uint32_t> param_desc;     // [padded_trees][words per tree] for the parameter bank
@@ -72,10 +78,9 @@ struct obt_model {
   int precision = OBT_PRECISION_BINARY64;
   int leaf_storage = 1;      // 0 fp64, 1 fp32, 2 fp16
   int compare_mode = 7;      // 7: all buckets < 128; 8: full byte compare
-  int levels = 0;            // Eytzinger levels
-  int eytz_pitch = 0;
+  BorderTable full;          // every border: obt_quantize_dev (reference buckets)
+  BorderTable used;          // borders referenced by splits: the predict path
   double scale = 1.0, bias = 0.0;
-  float* d_eytz = nullptr;   // [F][eytz_pitch]
   // host copies used to (re)build descriptor records for a tile size
   std::vector<int32_t> split_feature;   // [T][DI]
   std::vector<uint8_t> split_ordinal;   // [T][DI]
@@ -91,7 +96,8 @@ struct obt_model {
   obt::ApplyArgs<1> param_args;  // launch-parameter staging (32 KB), guarded by mu
   ~obt_model() {
     for (auto& kv : plans) cudaFree(kv.second.d_chunks);
-    if (d_eytz) cudaFree(d_eytz);
+    if (full.d) cudaFree(full.d);
+    if (used.d) cudaFree(used.d);
   }
 };
 
@@ -139,6 +145,25 @@ void eytzinger_fill(const float* sorted, int n, float* out, int pitch, int& pos,
   out[node] = pos < n ? sorted[pos] : INFINITY;
   ++pos;
   eytzinger_fill(sorted, n, out, pitch, pos, 2 * node + 2);
+}
+
+int build_border_table(const float* borders, const int32_t* counts, int F, int stride, BorderTable& out) {
+  int bmax = 0;
+  for (int f = 0; f < F; ++f) bmax = std::max(bmax, (int)counts[f]);
+  int levels = 0;
+  while (((1 << levels) - 1) < bmax) ++levels;
+  out.levels = levels;
+  out.pitch = std::max(1, (1 << levels) - 1);
+  std::vector<float> eytz((size_t)F * out.pitch, INFINITY);
+  for (int f = 0; f < F; ++f) {
+    int pos = 0;
+    if (levels > 0)
+      eytzinger_fill(borders + (size_t)f * stride, counts[f], eytz.data() + (size_t)f * out.pitch,
+                     (1 << levels) - 1, pos, 0);
+  }
+  CUDA_TRY(cudaMalloc(&out.d, eytz.size() * sizeof(float)));
+  CUDA_TRY(cudaMemcpy(out.d, eytz.data(), eytz.size() * sizeof(float), cudaMemcpyHostToDevice));
+  return OBT_OK;
 }
 
 int validate(const obt_model_desc* d) {
@@ -202,9 +227,9 @@ void plan_chunks(obt_model* m) {
   const int group = obt::tree_group(DI);
   // ring budget: what the bucket tile of the largest 256-quantum tile leaves over
   const int64_t avail = (int64_t)m->smem_optin - 512;
-  const int64_t tile_cap = 4 * (obt::kApplyMaxThreads - obt::kApplyProducerThreads) / 256 * 256;
+  const int64_t tile_cap = 4 * (obt::kApplyMaxThreads - obt::kApplyProducerThreads) / 128 * 128;
   const int64_t tile_objs = std::min<int64_t>(
-      tile_cap, std::max<int64_t>(256, (avail - (int64_t)kStages * 4096) / m->n_features / 256 * 256));
+      tile_cap, std::max<int64_t>(128, (avail - (int64_t)kStages * 4096) / m->n_features / 128 * 128));
   const int64_t ring = std::max<int64_t>((int64_t)kStages * per_tree * group, avail - tile_objs * m->n_features);
   int ct = (int)std::max<int64_t>(group, (ring / kStages - 512) / (int64_t)per_tree / group * group);
   ct = std::min(ct, 64);
@@ -356,6 +381,7 @@ struct ApplyKernel {
   const void* fn = nullptr;
   int dsrc = 0;
   int words = 1;
+  int tpw = 1;
 };
 
 // bucket words (4 objects each) per apply thread: 1, or 2 (8 objects per thread: half
@@ -397,6 +423,57 @@ ApplyKernel apply_di(int cmp, int leaf, bool write_idx, int dsrc) {
   return apply_leaf<DI, 8, 0>(leaf, write_idx);
 }
 
+template <int DI, int CMP, int TPW>
+ApplyKernel split_leaf(int leaf) {
+  ApplyKernel k;
+  k.tpw = TPW;
+  if (leaf == 0) k.fn = (const void*)obt::apply_split_kernel<DI, CMP, 0, TPW>;
+  else if (leaf == 1) k.fn = (const void*)obt::apply_split_kernel<DI, CMP, 1, TPW>;
+  else k.fn = (const void*)obt::apply_split_kernel<DI, CMP, 2, TPW>;
+  return k;
+}
+
+template <int DI, int TPW>
+ApplyKernel split_cmp(int cmp, int leaf) {
+  return cmp == 7 ? split_leaf<DI, 7, TPW>(leaf) : split_leaf<DI, 8, TPW>(leaf);
+}
+
+// Depth-split kernel for depth <= 8: TPW lanes per bucket word (TPW | depth).
+ApplyKernel pick_split(int di, int cmp, int leaf, int tpw) {
+  if (tpw == 2) {
+    switch (di) {
+      case 2: return split_cmp<2, 2>(cmp, leaf);
+      case 4: return split_cmp<4, 2>(cmp, leaf);
+      case 6: return split_cmp<6, 2>(cmp, leaf);
+      case 8: return split_cmp<8, 2>(cmp, leaf);
+    }
+  } else if (tpw == 4) {
+    switch (di) {
+      case 4: return split_cmp<4, 4>(cmp, leaf);
+      case 8: return split_cmp<8, 4>(cmp, leaf);
+    }
+  }
+  return ApplyKernel{};
+}
+
+// Lanes per bucket word (measured on B200): depth-split lanes add descriptor and shuffle
+// traffic to the shared-memory pipe, so they pay only when the tile -- F bytes per
+// object -- leaves few warps (F = 500: 2 lanes); subject to TPW | depth.  OBT_TPW overrides.
+int choose_tpw(const obt_model* m, int tile, bool write_idx, int dsrc) {
+  if (write_idx || dsrc || m->depth_inst > 8) return 1;
+  const int words = tile / 4;
+  const int cap = obt::kApplyMaxThreads - obt::kApplyProducerThreads;
+  const char* e = getenv("OBT_TPW");
+  if (e) {
+    const int t = atoi(e);
+    if ((t == 2 || t == 4) && m->depth_inst % t == 0 && words * t <= cap) return t;
+    return 1;
+  }
+  // measured at config 4 (F = 500, 4-8 warps): TPW 2 beats 1 by 1.6x and 4 by 1.3x
+  if (words >= 192) return 1;
+  return (m->depth_inst % 2 == 0 && words * 2 <= cap) ? 2 : 1;
+}
+
 ApplyKernel pick_apply(int di, int cmp, int leaf, bool write_idx, int dsrc) {
   switch (di) {
     case 1: return apply_di<1>(cmp, leaf, write_idx, dsrc);
@@ -413,21 +490,24 @@ ApplyKernel pick_apply(int di, int cmp, int leaf, bool write_idx, int dsrc) {
   }
 }
 
+// tiled (predict path): against the used-border table; plain (obt_quantize_dev): against
+// every border, returning the reference's buckets.
 int launch_quantize(const obt_model* m, const float* x, int64_t n, int layout, uint8_t* out, bool tiled,
                     int tile, int64_t n_slots, cudaStream_t stream) {
-  QuantFn fn = pick_quant(m->levels, layout, tiled);
-  if (!fn) return fail(OBT_E_UNSUPPORTED, "no quantize kernel for %d levels", m->levels);
+  const BorderTable& bt = tiled ? m->used : m->full;
+  QuantFn fn = pick_quant(bt.levels, layout, tiled);
+  if (!fn) return fail(OBT_E_UNSUPPORTED, "no quantize kernel for %d levels", bt.levels);
   obt::QuantizeParams p{};
   p.x = x;
   p.n = n;
   p.n_slots = n_slots;
   p.n_features = m->n_features;
-  p.eytz = m->d_eytz;
-  p.eytz_pitch = m->eytz_pitch;
+  p.eytz = bt.d;
+  p.eytz_pitch = bt.pitch;
   p.out = out;
   p.tile = tile;
-  const int fc = obt::quantize_chunk_features(m->levels > 0 ? m->eytz_pitch : 0, m->n_features);
-  const size_t smem = m->levels > 0 ? (size_t)std::min(fc, m->n_features) * m->eytz_pitch * 4 : 16;
+  const int fc = obt::quantize_chunk_features(bt.levels > 0 ? bt.pitch : 0, m->n_features);
+  const size_t smem = bt.levels > 0 ? (size_t)std::min(fc, m->n_features) * bt.pitch * 4 : 16;
   p.chunk_features = fc;
   p.two = 2;
   CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -448,7 +528,9 @@ int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, double* ou
   int rc = get_tile_plan(m, tile, &tp);
   if (rc != OBT_OK) return rc;
   const int dsrc = use_param_descriptors(m);
-  ApplyKernel k = pick_apply(m->depth_inst, m->compare_mode, m->leaf_storage, write_idx, dsrc);
+  const int tpw = choose_tpw(m, tile, write_idx, dsrc);
+  ApplyKernel k = tpw > 1 ? pick_split(m->depth_inst, m->compare_mode, m->leaf_storage, tpw)
+                          : pick_apply(m->depth_inst, m->compare_mode, m->leaf_storage, write_idx, dsrc);
   if (!k.fn) return fail(OBT_E_UNSUPPORTED, "no apply kernel for depth %d", m->depth_inst);
   const int64_t n_tiles = (n + tile - 1) / tile;
   const size_t smem = 512 + (size_t)kStages * m->chunk_bytes + (size_t)m->n_features * tile;
@@ -472,7 +554,8 @@ int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, double* ou
   p.tree_end = tree_end;
   p.scale = m->scale;
   p.bias = m->bias;
-  const dim3 grid((unsigned)n_tiles), block((unsigned)(obt::kApplyProducerThreads + tile / (4 * k.words)));
+  const dim3 grid((unsigned)n_tiles),
+      block((unsigned)(obt::kApplyProducerThreads + tile / (4 * k.words) * k.tpw));
   const int per = dsrc ? param_chunks_per_launch(m) : std::max(m->n_chunks, 1);
   const int n_launch = m->n_chunks == 0 ? 1 : (m->n_chunks + per - 1) / per;
   for (int l = 0; l < n_launch; ++l) {
@@ -565,32 +648,56 @@ int obt_model_create(const obt_model_desc* d, int device, obt_model** out) {
   }
   CUDA_TRY(cudaDeviceGetAttribute(&m->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
 
-  // borders -> Eytzinger arrays
-  int bmax = 0;
-  for (int f = 0; f < d->n_features; ++f) bmax = std::max(bmax, d->border_counts[f]);
-  m->compare_mode = bmax <= 127 ? 7 : 8;
-  int levels = 0;
-  while (((1 << levels) - 1) < bmax) ++levels;
-  m->levels = levels;
-  m->eytz_pitch = std::max(1, (1 << levels) - 1);
-  std::vector<float> eytz((size_t)d->n_features * m->eytz_pitch, INFINITY);
-  for (int f = 0; f < d->n_features; ++f) {
-    int pos = 0;
-    if (levels > 0)
-      eytzinger_fill(d->borders + (size_t)f * d->border_stride, d->border_counts[f],
-                     eytz.data() + (size_t)f * m->eytz_pitch, (1 << levels) - 1, pos, 0);
-  }
-  CUDA_TRY(cudaMalloc(&m->d_eytz, eytz.size() * sizeof(float)));
-  CUDA_TRY(cudaMemcpy(m->d_eytz, eytz.data(), eytz.size() * sizeof(float), cudaMemcpyHostToDevice));
-
-  // splits, padded from Dmax to the instantiated depth with sentinels
+  // Two border tables.  `full` holds every border (obt_quantize_dev returns the
+  // reference's buckets).  `used` holds, per feature, only the borders some split
+  // references: with R_f the sorted used borders, x > b[u_j] <=> #{i : x > R_f[i]} > j,
+  // so the predict path quantizes against R_f and compares with the split's rank j.
+  // Fewer borders mean fewer search levels, and <= 127 used borders per feature keep
+  // the 7-bit SWAR compare even when a feature has up to 254 borders.
   const int D = m->max_depth, DI = m->depth_inst;
+  std::vector<std::vector<int>> used(d->n_features);
+  for (int t = 0; t < m->n_trees; ++t)
+    for (int s = 0; s < D; ++s) {
+      const int ord = d->split_ordinal[(size_t)t * D + s];
+      if (ord != kSentinel) used[d->split_feature[(size_t)t * D + s]].push_back(ord);
+    }
+  const char* no_remap = getenv("OBT_NO_REMAP");  // A/B knob: quantize against every border
+  std::vector<std::vector<int>> rank(d->n_features);  // ordinal -> rank in R_f
+  std::vector<float> used_borders((size_t)d->n_features * std::max(1, d->border_stride), INFINITY);
+  std::vector<int32_t> used_counts(d->n_features, 0);
+  for (int f = 0; f < d->n_features; ++f) {
+    auto& u = used[f];
+    if (no_remap && atoi(no_remap)) {
+      u.resize(d->border_counts[f]);
+      for (int k = 0; k < d->border_counts[f]; ++k) u[k] = k;
+    }
+    std::sort(u.begin(), u.end());
+    u.erase(std::unique(u.begin(), u.end()), u.end());
+    rank[f].assign(256, -1);
+    for (size_t j = 0; j < u.size(); ++j) {
+      rank[f][u[j]] = (int)j;
+      used_borders[(size_t)f * d->border_stride + j] = d->borders[(size_t)f * d->border_stride + u[j]];
+    }
+    used_counts[f] = (int32_t)u.size();
+  }
+  int rc2 = build_border_table(d->borders, d->border_counts, d->n_features, d->border_stride, m->full);
+  if (rc2 != OBT_OK) return rc2;
+  rc2 = build_border_table(used_borders.data(), used_counts.data(), d->n_features, d->border_stride, m->used);
+  if (rc2 != OBT_OK) return rc2;
+  int umax = 0;
+  for (int f = 0; f < d->n_features; ++f) umax = std::max(umax, (int)used_counts[f]);
+  m->compare_mode = umax <= 127 ? 7 : 8;
+
+  // splits (ordinals as ranks among the used borders), padded to the instantiated
+  // depth with sentinels
   m->split_feature.assign((size_t)m->n_trees * DI, 0);
   m->split_ordinal.assign((size_t)m->n_trees * DI, (uint8_t)kSentinel);
   for (int t = 0; t < m->n_trees; ++t)
     for (int s = 0; s < D; ++s) {
-      m->split_feature[(size_t)t * DI + s] = d->split_feature[(size_t)t * D + s];
-      m->split_ordinal[(size_t)t * DI + s] = d->split_ordinal[(size_t)t * D + s];
+      const int f = d->split_feature[(size_t)t * D + s];
+      const int ord = d->split_ordinal[(size_t)t * D + s];
+      m->split_feature[(size_t)t * DI + s] = f;
+      m->split_ordinal[(size_t)t * DI + s] = ord == kSentinel ? (uint8_t)kSentinel : (uint8_t)rank[f][ord];
     }
 
   // leaf bank: binary16 bits, or binary64 stored as fp32 when that is exact

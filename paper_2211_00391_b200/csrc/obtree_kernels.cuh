@@ -107,7 +107,7 @@ struct QuantizeParams {
   int32_t two;             // the constant 2, passed at run time (see eytz_level)
 };
 
-constexpr int kQuantObjects = 256;    // tile quantum: tiles are whole multiples of this
+constexpr int kQuantObjects = 128;    // tile quantum: a quantize warp's 128 objects never straddle tiles
 constexpr int kQuantThreads = 256;    // 8 warps x 128 objects = 1024 objects per CTA
 constexpr int kQuantBlock = 1024;
 constexpr int kQuantSmem = 48 * 1024; // Eytzinger arrays of one feature chunk
@@ -247,9 +247,10 @@ __global__ void __launch_bounds__(kQuantThreads, 2) quantize_kernel(QuantizePara
 // DSRC 0); the tree count is padded to a multiple of 4 with null trees whose splits
 // are sentinels and whose leaves are -0.0, and x + (-0.0) == x exactly for every x,
 // so padding never changes a bit of the fold.
-// 16 trees per group keep ~100 independent shared loads in flight per thread; deep
-// trees (large leaf tables) use groups of 4 so a chunk of them still fits the ring.
-__host__ __device__ constexpr int tree_group(int di) { return di <= 8 ? 16 : 4; }
+// 16 trees per group keep ~100 independent shared loads in flight per thread; deeper
+// trees (larger leaf tables) use groups of 8 / 4 so a chunk still fits the ring without
+// shrinking the bucket tile.
+__host__ __device__ constexpr int tree_group(int di) { return di <= 6 ? 16 : di <= 8 ? 8 : 4; }
 __host__ __device__ constexpr int desc_words(int cmp) { return 2; }
 __host__ __device__ constexpr int desc_words_per_tree(int di, int cmp) { return di * desc_words(cmp); }
 
@@ -344,7 +345,7 @@ __host__ __device__ constexpr int leaf_table_stride(int di, int leaf_bytes) {
 
 constexpr int kApplyProducerThreads = 32;
 // Block size cap: 128 registers per thread keep several tree groups of loads in flight.
-constexpr int kApplyMaxThreads = 512;
+constexpr int kApplyMaxThreads = 544;  // 16 consumer warps + the producer
 
 template <int DI, int CMP, int LEAF, bool WRITE_IDX, int W, int DSRC>
 __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid_constant__ ApplyArgs<DSRC> args) {
@@ -519,6 +520,133 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid
         p.out[obj0 + k] = p.last ? __dadd_rn(__dmul_rn((double)acc[k], p.scale), p.bias) : (double)acc[k];
       }
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2s: depth-split tree apply.  TPW adjacent lanes share one 4-object bucket word:
+// lane part p evaluates depths [p*DI/TPW, (p+1)*DI/TPW) of every tree, the partial
+// index words are OR-combined with butterfly shuffles, and lane p then gathers and
+// folds objects [p*4/TPW, (p+1)*4/TPW) of the word.  Every accumulator still sees
+// the trees in order (the fold stays bit-exact) while the CTA runs TPW times more
+// warps over the same bucket tile -- the lever against the latency bound when the
+// tile (F bytes per object) limits the objects an SM can hold.  Descriptors come from
+// the shared-memory ring ({off, k} / {(off << 8) | k, s}, 8 bytes each).
+template <int DI, int CMP, int LEAF, int TPW>
+__global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_split_kernel(const __grid_constant__ ApplyArgs<0> args) {
+  static_assert(DI <= 8 && DI % TPW == 0, "depth-split needs TPW | DI and one index byte");
+  const ApplyParams& p = args.p;
+  using LT = LeafT<LEAF>;
+  using acc_t = typename LT::Acc;
+  constexpr int kTreeGroup = tree_group(DI);
+  constexpr int kDPT = DI / TPW;        // depths per lane
+  constexpr int kOPT = 4 / TPW;         // objects folded per lane
+  constexpr bool kPrescaled = (DI + LT::kShift) <= 8;
+  constexpr int kBitBase = kPrescaled ? LT::kShift : 0;
+  constexpr int kTabStride = leaf_table_stride(DI, (int)sizeof(typename LT::T));
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((256u - (smem_u32(smem_raw) & 255u)) & 255u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + 8;
+  uint64_t* tile_bar = full + 16;
+  unsigned char* stages = smem + 256;
+  unsigned char* qtile = stages + (size_t)p.n_stages * p.chunk_bytes;
+
+  const int tid = threadIdx.x;
+  const int n_consumers = blockDim.x - kApplyProducerThreads;
+  const int64_t tile_idx = blockIdx.x;
+  const int n_chunks = p.chunk_end - p.chunk_begin;
+  if (tid == 0) {
+    for (int i = 0; i < p.n_stages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], n_consumers);
+    }
+    mbar_init(tile_bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int warp_id = __shfl_sync(0xffffffffu, tid / 32, 0);
+  if (warp_id == 0) {
+    if (tid == 0) {
+      mbar_expect_tx(tile_bar, p.q_tile_bytes);
+      bulk_g2s_split(qtile, p.q + tile_idx * (int64_t)p.q_tile_bytes, p.q_tile_bytes, tile_bar);
+      for (int c = 0; c < n_chunks; ++c) {
+        const int s = c % p.n_stages;
+        if (c >= p.n_stages) mbar_wait(&empty[s], (uint32_t)(c / p.n_stages - 1) & 1u);
+        mbar_expect_tx(&full[s], p.chunk_bytes);
+        bulk_g2s_split(stages + (size_t)s * p.chunk_bytes,
+                       p.chunks + (size_t)(p.chunk_begin + c) * p.chunk_bytes, p.chunk_bytes, &full[s]);
+      }
+    }
+    return;
+  }
+
+  const int ctid = tid - kApplyProducerThreads;
+  const int word = ctid / TPW, part = ctid % TPW;
+  const uint32_t my_q = smem_u32(qtile) + 4 * word;
+  const int64_t obj0 = tile_idx * p.tile + 4 * word + part * kOPT;
+  // per-lane constants: the index bits this lane owns and the bytes it gathers
+  uint32_t shift[kDPT], mask[kDPT];
+#pragma unroll
+  for (int i = 0; i < kDPT; ++i) {
+    const int pos = part * kDPT + i + kBitBase;
+    shift[i] = 7u - (uint32_t)pos;
+    mask[i] = 0x01010101u << pos;
+  }
+  uint32_t sel[kOPT];
+#pragma unroll
+  for (int k = 0; k < kOPT; ++k) sel[k] = kPrescaled ? (0x7650u | (uint32_t)(part * kOPT + k)) : (0x4440u | (uint32_t)(part * kOPT + k));
+  acc_t acc[kOPT];
+#pragma unroll
+  for (int k = 0; k < kOPT; ++k) acc[k] = (p.first || obj0 + k >= p.n) ? (acc_t)0 : (acc_t)p.out[obj0 + k];
+  mbar_wait_warp(tile_bar, 0);
+
+  const uint32_t my_desc = (uint32_t)(part * kDPT) * 8u;  // this lane's first descriptor in a tree
+  for (int c = 0; c < n_chunks; ++c) {
+    const int s = c % p.n_stages;
+    mbar_wait_warp(&full[s], (uint32_t)(c / p.n_stages) & 1u);
+    const unsigned char* st = stages + (size_t)s * p.chunk_bytes;
+    const uint32_t leaf_base = smem_u32(st + p.desc_bytes);
+    const uint32_t desc_base = smem_u32(st) + my_desc;
+    for (int g = 0; g < p.chunk_trees / kTreeGroup; ++g) {
+#pragma unroll
+      for (int tt = 0; tt < kTreeGroup; ++tt) {
+        const int t = g * kTreeGroup + tt;
+        const uint32_t tree_desc = desc_base + (uint32_t)t * (uint32_t)(DI * 8);
+        uint32_t part_a = 0, part_b = 0;
+#pragma unroll
+        for (int i = 0; i < kDPT; ++i) {
+          uint32_t d0, d1;
+          asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(d0), "=r"(d1) : "r"(tree_desc + 8u * i));
+          uint32_t b7;
+          if constexpr (CMP == 7) {
+            b7 = lds_u32(my_q + d0) + d1;
+          } else {
+            const uint32_t w = lds_u32(my_q + (d0 >> 8));
+            b7 = maj3((w & 0x7f7f7f7fu) + (__byte_perm(d0, 0u, 0x0000u) & 0x7f7f7f7fu), w, d1);
+          }
+          const uint32_t term = (b7 >> shift[i]) & mask[i];
+          if (i & 1) part_b |= term; else part_a |= term;
+        }
+        uint32_t lo = part_a | part_b;
+        if constexpr (TPW >= 2) lo |= __shfl_xor_sync(0xffffffffu, lo, 1);
+        if constexpr (TPW >= 4) lo |= __shfl_xor_sync(0xffffffffu, lo, 2);
+        const uint32_t tab = leaf_base + (uint32_t)t * kTabStride;
+#pragma unroll
+        for (int k = 0; k < kOPT; ++k) {
+          uint32_t addr;
+          if constexpr (kPrescaled) addr = __byte_perm(lo, tab, sel[k]);
+          else addr = tab + (__byte_perm(lo, 0u, sel[k]) << LT::kShift);
+          acc[k] += LT::widen(lds_leaf<LEAF>(addr));
+        }
+      }
+    }
+    mbar_arrive(&empty[s]);
+  }
+#pragma unroll
+  for (int k = 0; k < kOPT; ++k) {
+    if (obj0 + k < p.n) p.out[obj0 + k] = p.last ? __dadd_rn(__dmul_rn((double)acc[k], p.scale), p.bias) : (double)acc[k];
   }
 }
 

@@ -34,6 +34,14 @@ KEYS = {
     "launch__block_size": "block",
     "launch__grid_size": "grid",
     "lts__t_bytes.sum": "l2_bytes",
+    "l1tex__throughput.avg.pct_of_peak_sustained_active": "l1tex_pct",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed": "smem_wf_pct",
+    "l1tex__data_pipe_lsu_wavefronts.sum.pct_of_peak_sustained_elapsed": "lsu_wf_pct",
+    "smsp__inst_executed_op_shared_ld.sum": "lds_inst",
+    "sm__mio_inst_issued.avg.pct_of_peak_sustained_active": "mio_issue_pct",
+    "sm__mio2rf_writeback_active.avg.pct_of_peak_sustained_active": "mio2rf_pct",
+    "smsp__inst_executed_op_shfl.sum": "shfl_inst",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_throughput_pct",
 }
 
 
