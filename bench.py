@@ -142,6 +142,22 @@ def roofline_terms(spec) -> dict:
     }
 
 
+def flat_model(model):
+    """The oracle's flat layout for an ObliviousModel or a multiclass.MultiOutputModel."""
+    import numpy as np
+
+    import oracle
+
+    if not hasattr(model, "subset"):
+        return oracle.flatten(model)
+    counts = np.array([b.size for b in model.borders], np.int32)
+    borders = np.full((model.n_features, max(1, int(counts.max()))), np.inf, np.float32)
+    for f, b in enumerate(model.borders):
+        borders[f, : b.size] = b
+    return oracle.FlatModel(borders, counts, np.full(model.n_trees, model.depth, np.int32), model.split_feature,
+                            model.split_ordinal, model.leaves, model.scale, model.bias)
+
+
 def cpu_baseline(spec, model, seconds: float, verify_fn=None) -> dict:
     """The C oracle port of the reference algorithm on this host's cores, on a bounded
     prefix sample of the same workload (doubling until the run takes >= `seconds`/4)."""
@@ -150,7 +166,7 @@ def cpu_baseline(spec, model, seconds: float, verify_fn=None) -> dict:
     import oracle
     from paper_2211_00391_b200 import synthetic
 
-    fm = oracle.flatten(model)
+    fm = flat_model(model)
     threads = oracle.max_threads()
     n = 4096
     best = None
@@ -208,8 +224,13 @@ def run_reference(args, world, rank):
     from paper_2211_00391_b200 import synthetic
 
     spec = synthetic.CONFIGS[args.config]
-    model = synthetic.build_model(spec)
-    fm = oracle.flatten(model)
+    if spec.n_outputs > 1:
+        from paper_2211_00391_b200 import multiclass
+
+        model = multiclass.from_arrays(synthetic.model_arrays(spec))
+    else:
+        model = synthetic.build_model(spec)
+    fm = flat_model(model)
     prec = oracle.BINARY16 if spec.half_leaves else oracle.BINARY64
     n = args.ref_sample
     x = synthetic.host_features(spec, n_objects=n, seed=spec.data_seed + 7)
@@ -252,12 +273,24 @@ def run_ours(args, world, rank, local):
         spec = synthetic.WorkloadSpec(**{**spec.__dict__, "n_trees": args.trees})
     device = local
     torch.cuda.set_device(device)
-    model = synthetic.build_model(spec)
-    strategy = obt.LeafStrategy.NAIVE16 if spec.half_leaves else obt.LeafStrategy.NAIVE
-    ev = obt.Evaluator(model, obt.EvalConfig(strategy=strategy), device=device)
-    x = synthetic.device_features(spec, seed=spec.data_seed + 1000 * rank, device=f"cuda:{device}")
+    multi = spec.n_outputs > 1
+    if multi:
+        # config 5: tree-sharded across ranks (each rank folds its trees for all objects,
+        # partial sums reduced after the timed region); at N=1 the whole model
+        from paper_2211_00391_b200 import multiclass, sharding
+
+        full_model = multiclass.from_arrays(synthetic.model_arrays(spec))
+        tb, te = sharding.tree_shard(full_model.n_trees, rank, world)
+        model = full_model.subset(tb, te, raw=world > 1) if world > 1 else full_model
+        ev = multiclass.MultiOutputEvaluator(model, device=device)
+    else:
+        model = synthetic.build_model(spec)
+        strategy = obt.LeafStrategy.NAIVE16 if spec.half_leaves else obt.LeafStrategy.NAIVE
+        ev = obt.Evaluator(model, obt.EvalConfig(strategy=strategy), device=device)
+    data_seed = spec.data_seed + (0 if multi else 1000 * rank)  # tree sharding: same objects on every rank
+    x = synthetic.device_features(spec, seed=data_seed, device=f"cuda:{device}")
     N = spec.n_objects
-    out = torch.empty(N, dtype=torch.float64, device=x.device)
+    out = torch.empty((N, spec.n_outputs) if multi else N, dtype=torch.float64, device=x.device)
     ws = torch.empty(ev.workspace_bytes(N), dtype=torch.uint8, device=x.device)
 
     for _ in range(args.warmup):
@@ -288,11 +321,23 @@ def run_ours(args, world, rank, local):
     q_ms = sum(m[0].elapsed_ms(m[1]) for m in marks) / K
     a_ms = sum(m[1].elapsed_ms(m[2]) for m in marks) / K
     step_s = elapsed_ms / K / 1e3
-    value = world * N * spec.n_trees / step_s
+    # object sharding: every rank folds all trees for its own N objects; tree sharding
+    # (config 5): every rank folds its share of the trees for the same N objects
+    value = (N * spec.n_trees if multi else world * N * spec.n_trees) / step_s
+    reduce_ms = None
+    if multi and world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.synchronize()
+        r0 = time.perf_counter()
+        dist.all_reduce(out, op=dist.ReduceOp.SUM)  # the NCCL reduce of per-object partial sums
+        out.mul_(full_model.scale).add_(full_model.bias)
+        torch.cuda.synchronize()
+        reduce_ms = (time.perf_counter() - r0) * 1e3
 
     # end to end through the public API: pinned host features -> scores in pinned host memory
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not multi:
         xh = torch.empty((N, spec.n_features), dtype=torch.float32, pin_memory=True)
         xh.copy_(x)
         oh = torch.empty(N, dtype=torch.float64, pin_memory=True)
@@ -352,10 +397,14 @@ def run_ours(args, world, rank, local):
                     "apply_ms": a_ms},
         "clocks": clk,
     }
+    if multi:
+        line["config"]["outputs"] = spec.n_outputs
+        line["config"]["parallelism"] = f"trees sharded over {world} GPU(s); NCCL all_reduce of fp64 partials"
+        line["scaling"] = "strong"
+        line["nccl_reduce_ms"] = reduce_ms
     if world == 1 and not args.no_cpu_baseline:
         def verify(xs):
-            got = ev.predict(obt.FeatureMatrix(xs, obt.Layout.OBJECT_MAJOR))
-            return got
+            return ev.predict(obt.FeatureMatrix(xs, obt.Layout.OBJECT_MAJOR))
 
         line["cpu_baseline"] = cpu_baseline(spec, model, args.cpu_seconds, verify)
     print(json.dumps(line), flush=True)
@@ -366,7 +415,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--objects", type=int, default=0, help="override objects per GPU")
     ap.add_argument("--trees", type=int, default=0, help="override the tree count (experiments)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")

@@ -1,0 +1,28 @@
+// dispatch.h -- kernel selection across the per-family translation units (k_*.cu).
+#pragma once
+
+#include "obtree_kernels.cuh"
+
+namespace obt {
+
+using QuantFn = void (*)(QuantizeParams);
+
+struct ApplyKernel {
+  const void* fn = nullptr;
+  int dsrc = 0;   // 0: descriptors in the shared-memory ring, 1: parameter bank
+  int words = 1;  // bucket words per thread
+  int tpw = 1;    // lanes per bucket word (depth-split kernel when > 1)
+};
+
+// K1, levels 0..8
+QuantFn pick_quant(int levels, int layout, bool tiled);
+// K2, depths {1..8, 10, 12}
+ApplyKernel pick_apply(int di, int cmp, int leaf, bool write_idx, int dsrc);
+// K2s, depth-split (tpw 2: depths 2/4/6/8, tpw 4: depths 4/8)
+ApplyKernel pick_split(int di, int cmp, int leaf, int tpw);
+// K4 multi-output: depths {4, 6, 8, 10, 12}, outputs <= 16; returns the depth / output
+// capacity it was instantiated for through *di_out / *c_out
+const void* pick_multi(int di, int cmp, int leaf, int c, int* di_out);
+int multi_depth(int d);
+
+}  // namespace obt

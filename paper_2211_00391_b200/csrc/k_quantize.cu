@@ -1,0 +1,27 @@
+// k_quantize.cu -- instantiations of K1 (quantize_kernel) for 0..8 search levels.
+#include "dispatch.h"
+
+namespace obt {
+
+template <int L>
+static QuantFn quant_fn(int layout, bool tiled) {
+  if (layout == 0) return tiled ? quantize_kernel<L, 0, true> : quantize_kernel<L, 0, false>;
+  return tiled ? quantize_kernel<L, 1, true> : quantize_kernel<L, 1, false>;
+}
+
+QuantFn pick_quant(int levels, int layout, bool tiled) {
+  switch (levels) {
+    case 0: return quant_fn<0>(layout, tiled);
+    case 1: return quant_fn<1>(layout, tiled);
+    case 2: return quant_fn<2>(layout, tiled);
+    case 3: return quant_fn<3>(layout, tiled);
+    case 4: return quant_fn<4>(layout, tiled);
+    case 5: return quant_fn<5>(layout, tiled);
+    case 6: return quant_fn<6>(layout, tiled);
+    case 7: return quant_fn<7>(layout, tiled);
+    case 8: return quant_fn<8>(layout, tiled);
+    default: return nullptr;
+  }
+}
+
+}  // namespace obt

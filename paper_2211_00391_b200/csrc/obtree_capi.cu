@@ -20,6 +20,13 @@
 
 #include "../../include/obtree_b200.h"
 #include "obtree_kernels.cuh"
+#include "dispatch.h"
+
+using obt::ApplyKernel;
+using obt::QuantFn;
+using obt::pick_apply;
+using obt::pick_quant;
+using obt::pick_split;
 
 namespace {
 
@@ -48,6 +55,8 @@ constexpr int kMaxBorders = 254;  // model.py:21
 constexpr int kMaxDepth = 12;     // smem-staged leaf tables (2^12 fp32 = 16 KiB per tree)
 constexpr int kSentinel = 255;    // evaluate.py:32
 constexpr int kStages = 3;        // records in flight in the apply kernel's ring
+constexpr int kMaxOutputs = 16;   // multi-output kernel instantiations
+constexpr int kMultiTile = 4 * obt::kMultiThreads;  // objects per multi-output CTA
 
 // Instantiated depths of the apply kernel; a model of depth D runs on the
 // smallest instantiation >= D with sentinel (never-true) padding splits.
@@ -80,6 +89,8 @@ struct obt_model {
   int compare_mode = 7;      // 7: all buckets < 128; 8: full byte compare
   BorderTable full;          // every border: obt_quantize_dev (reference buckets)
   BorderTable used;          // borders referenced by splits: the predict path
+  void* d_multi_leaves = nullptr;   // multi-output records [T][2^DI][CP]
+  uint32_t* d_multi_desc = nullptr; // multi-output descriptors [T][DI][2] for kMultiTile
   double scale = 1.0, bias = 0.0;
   // host copies used to (re)build descriptor records for a tile size
   std::vector<int32_t> split_feature;   // [T][DI]
@@ -97,6 +108,8 @@ struct obt_model {
   ~obt_model() {
     for (auto& kv : plans) cudaFree(kv.second.d_chunks);
     if (full.d) cudaFree(full.d);
+    if (d_multi_leaves) cudaFree(d_multi_leaves);
+    if (d_multi_desc) cudaFree(d_multi_desc);
     if (used.d) cudaFree(used.d);
   }
 };
@@ -170,8 +183,10 @@ int validate(const obt_model_desc* d) {
   if (!d) return fail(OBT_E_INVALID, "invalid model: null description");
   if (d->n_features < 1) return fail(OBT_E_INVALID, "invalid model: model: at least one float feature is required");
   if (d->n_trees < 0) return fail(OBT_E_INVALID, "invalid model: negative tree count");
-  if (d->n_outputs != 1)
-    return fail(OBT_E_UNSUPPORTED, "n_outputs=%d: multi-output leaves are not implemented by this build", d->n_outputs);
+  if (d->n_outputs < 1 || d->n_outputs > kMaxOutputs)
+    return fail(OBT_E_UNSUPPORTED, "n_outputs=%d outside 1..%d", d->n_outputs, kMaxOutputs);
+  if (d->n_outputs > 1 && d->precision != OBT_PRECISION_BINARY64)
+    return fail(OBT_E_UNSUPPORTED, "multi-output models support the binary64 family only");
   if (d->n_trees > 0 && (d->max_depth < 1 || d->max_depth > 16))
     return fail(OBT_E_INVALID, "invalid model: max_depth %d outside 1..16", d->max_depth);
   if (d->n_trees > 0 && instantiated_depth(d->max_depth) < 0)
@@ -205,8 +220,8 @@ int validate(const obt_model_desc* d) {
                       "invalid model: trees[%d].splits[%d]: border ordinal out of range (%d vs %d borders on feature %d)",
                       t, s, ord, d->border_counts[f], f);
       }
-      const double* lv = d->leaves + ((size_t)t << D);
-      for (size_t j = 0; j < ((size_t)1 << D); ++j)
+      const double* lv = d->leaves + (((size_t)t * d->n_outputs) << D);
+      for (size_t j = 0; j < ((size_t)d->n_outputs << D); ++j)
         if (std::isnan(lv[j])) return fail(OBT_E_INVALID, "invalid model: trees[%d]: NaN leaf value", t);
     }
   }
@@ -325,6 +340,7 @@ constexpr int kMaxParamLaunches = 0;
 // Largest tile (multiple of 256 objects) whose bucket tile fits next to the stage ring;
 // then shrink for small batches so the grid still covers the SMs.
 int plan_tile(const obt_model* m, int64_t n) {
+  if (m->n_outputs > 1) return kMultiTile;  // the multi-output kernel reads buckets through L1
   const int64_t fixed = 512 + (int64_t)kStages * m->chunk_bytes;
   int64_t tmax = (m->smem_optin - fixed) / m->n_features;
   tmax = std::min<int64_t>(tmax / kTileQuantum * kTileQuantum, 4 * (obt::kApplyMaxThreads - obt::kApplyProducerThreads) / kTileQuantum * kTileQuantum);
@@ -351,111 +367,7 @@ int use_param_descriptors(const obt_model* m) {
 }
 
 // ---------------------------------------------------------------------------
-// kernel dispatch
-using QuantFn = void (*)(obt::QuantizeParams);
-
-template <int L>
-QuantFn quant_fn(int layout, bool tiled) {
-  if (layout == 0) return tiled ? obt::quantize_kernel<L, 0, true> : obt::quantize_kernel<L, 0, false>;
-  return tiled ? obt::quantize_kernel<L, 1, true> : obt::quantize_kernel<L, 1, false>;
-}
-
-QuantFn pick_quant(int levels, int layout, bool tiled) {
-  switch (levels) {
-    case 0: return quant_fn<0>(layout, tiled);
-    case 1: return quant_fn<1>(layout, tiled);
-    case 2: return quant_fn<2>(layout, tiled);
-    case 3: return quant_fn<3>(layout, tiled);
-    case 4: return quant_fn<4>(layout, tiled);
-    case 5: return quant_fn<5>(layout, tiled);
-    case 6: return quant_fn<6>(layout, tiled);
-    case 7: return quant_fn<7>(layout, tiled);
-    case 8: return quant_fn<8>(layout, tiled);
-    default: return nullptr;
-  }
-}
-
-// Both descriptor sources behind one pointer type: the kernel takes ApplyArgs<DSRC>
-// by value; launches go through cudaLaunchKernel with a pointer to the right struct.
-struct ApplyKernel {
-  const void* fn = nullptr;
-  int dsrc = 0;
-  int words = 1;
-  int tpw = 1;
-};
-
-// bucket words (4 objects each) per apply thread: 1, or 2 (8 objects per thread: half
-// the threads, each with twice the independent work); OBT_WORDS_PER_THREAD overrides
-int words_per_thread() {
-  static const int w = [] {
-    const char* e = getenv("OBT_WORDS_PER_THREAD");
-    return (e && atoi(e) == 2) ? 2 : 1;
-  }();
-  return w;
-}
-
-template <int DI, int CMP, int DSRC, int W>
-ApplyKernel apply_leaf_w(int leaf, bool write_idx) {
-  ApplyKernel k;
-  k.dsrc = DSRC;
-  k.words = W;
-  if (write_idx) k.fn = (const void*)obt::apply_kernel<DI, CMP, 1, true, W, DSRC>;
-  else if (leaf == 0) k.fn = (const void*)obt::apply_kernel<DI, CMP, 0, false, W, DSRC>;
-  else if (leaf == 1) k.fn = (const void*)obt::apply_kernel<DI, CMP, 1, false, W, DSRC>;
-  else k.fn = (const void*)obt::apply_kernel<DI, CMP, 2, false, W, DSRC>;
-  return k;
-}
-
-template <int DI, int CMP, int DSRC>
-ApplyKernel apply_leaf(int leaf, bool write_idx) {
-  if constexpr (DSRC == 1) {
-    return apply_leaf_w<DI, CMP, 1, 1>(leaf, write_idx);
-  } else {
-    return words_per_thread() == 2 && !write_idx ? apply_leaf_w<DI, CMP, DSRC, 2>(leaf, write_idx)
-                                                 : apply_leaf_w<DI, CMP, DSRC, 1>(leaf, write_idx);
-  }
-}
-
-template <int DI>
-ApplyKernel apply_di(int cmp, int leaf, bool write_idx, int dsrc) {
-  // parameter-bank descriptors exist for the 7-bit compare only
-  if (cmp == 7) return dsrc ? apply_leaf<DI, 7, 1>(leaf, write_idx) : apply_leaf<DI, 7, 0>(leaf, write_idx);
-  return apply_leaf<DI, 8, 0>(leaf, write_idx);
-}
-
-template <int DI, int CMP, int TPW>
-ApplyKernel split_leaf(int leaf) {
-  ApplyKernel k;
-  k.tpw = TPW;
-  if (leaf == 0) k.fn = (const void*)obt::apply_split_kernel<DI, CMP, 0, TPW>;
-  else if (leaf == 1) k.fn = (const void*)obt::apply_split_kernel<DI, CMP, 1, TPW>;
-  else k.fn = (const void*)obt::apply_split_kernel<DI, CMP, 2, TPW>;
-  return k;
-}
-
-template <int DI, int TPW>
-ApplyKernel split_cmp(int cmp, int leaf) {
-  return cmp == 7 ? split_leaf<DI, 7, TPW>(leaf) : split_leaf<DI, 8, TPW>(leaf);
-}
-
-// Depth-split kernel for depth <= 8: TPW lanes per bucket word (TPW | depth).
-ApplyKernel pick_split(int di, int cmp, int leaf, int tpw) {
-  if (tpw == 2) {
-    switch (di) {
-      case 2: return split_cmp<2, 2>(cmp, leaf);
-      case 4: return split_cmp<4, 2>(cmp, leaf);
-      case 6: return split_cmp<6, 2>(cmp, leaf);
-      case 8: return split_cmp<8, 2>(cmp, leaf);
-    }
-  } else if (tpw == 4) {
-    switch (di) {
-      case 4: return split_cmp<4, 4>(cmp, leaf);
-      case 8: return split_cmp<8, 4>(cmp, leaf);
-    }
-  }
-  return ApplyKernel{};
-}
-
+// kernel dispatch: the instantiations live in k_*.cu (compiled in parallel)
 // Lanes per bucket word (measured on B200): depth-split lanes add descriptor and shuffle
 // traffic to the shared-memory pipe, so they pay only when the tile -- F bytes per
 // object -- leaves few warps (F = 500: 2 lanes); subject to TPW | depth.  OBT_TPW overrides.
@@ -474,24 +386,6 @@ int choose_tpw(const obt_model* m, int tile, bool write_idx, int dsrc) {
   return (m->depth_inst % 2 == 0 && words * 2 <= cap) ? 2 : 1;
 }
 
-ApplyKernel pick_apply(int di, int cmp, int leaf, bool write_idx, int dsrc) {
-  switch (di) {
-    case 1: return apply_di<1>(cmp, leaf, write_idx, dsrc);
-    case 2: return apply_di<2>(cmp, leaf, write_idx, dsrc);
-    case 3: return apply_di<3>(cmp, leaf, write_idx, dsrc);
-    case 4: return apply_di<4>(cmp, leaf, write_idx, dsrc);
-    case 5: return apply_di<5>(cmp, leaf, write_idx, dsrc);
-    case 6: return apply_di<6>(cmp, leaf, write_idx, dsrc);
-    case 7: return apply_di<7>(cmp, leaf, write_idx, dsrc);
-    case 8: return apply_di<8>(cmp, leaf, write_idx, dsrc);
-    case 10: return apply_di<10>(cmp, leaf, write_idx, dsrc);
-    case 12: return apply_di<12>(cmp, leaf, write_idx, dsrc);
-    default: return ApplyKernel{};
-  }
-}
-
-// tiled (predict path): against the used-border table; plain (obt_quantize_dev): against
-// every border, returning the reference's buckets.
 int launch_quantize(const obt_model* m, const float* x, int64_t n, int layout, uint8_t* out, bool tiled,
                     int tile, int64_t n_slots, cudaStream_t stream) {
   const BorderTable& bt = tiled ? m->used : m->full;
@@ -582,6 +476,33 @@ int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, double* ou
   return OBT_OK;
 }
 
+int launch_multi(obt_model* m, const uint8_t* q, int64_t n, double* out, cudaStream_t stream) {
+  int di = 0;
+  const void* fn = obt::pick_multi(m->depth_inst, m->compare_mode, m->leaf_storage, m->n_outputs, &di);
+  if (!fn || di != m->depth_inst) return fail(OBT_E_UNSUPPORTED, "no multi-output kernel for depth %d, %d outputs",
+                                             m->depth_inst, m->n_outputs);
+  obt::MultiParams p{};
+  p.q = q;
+  p.desc = m->d_multi_desc;
+  p.leaves = m->d_multi_leaves;
+  p.out = out;
+  p.n = n;
+  p.n_features = m->n_features;
+  p.tile = kMultiTile;
+  p.n_outputs = m->n_outputs;
+  p.tree_begin = 0;
+  p.tree_end = m->n_trees;
+  p.first = 1;
+  p.last = 1;
+  p.scale = m->scale;
+  p.bias = m->bias;
+  void* kargs[] = {&p};
+  const dim3 grid((unsigned)((n + kMultiTile - 1) / kMultiTile)), block(obt::kMultiThreads);
+  CUDA_TRY(cudaLaunchKernel(fn, grid, block, kargs, 0, stream));
+  ++g_launches;
+  return OBT_OK;
+}
+
 struct DeviceGuard {
   int prev = -1;
   explicit DeviceGuard(int dev) {
@@ -635,7 +556,9 @@ int obt_model_create(const obt_model_desc* d, int device, obt_model** out) {
   m->precision = d->precision;
   m->scale = d->scale;
   m->bias = d->bias;
-  m->depth_inst = d->n_trees > 0 ? instantiated_depth(d->max_depth) : 1;
+  m->depth_inst = d->n_trees > 0 ? (d->n_outputs > 1 ? obt::multi_depth(d->max_depth)
+                                                      : instantiated_depth(d->max_depth))
+                                  : (d->n_outputs > 1 ? 4 : 1);
   CUDA_TRY(cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount, device));
   {
     // keep stream-ordered workspace allocations cached between calls instead of
@@ -702,11 +625,12 @@ int obt_model_create(const obt_model_desc* d, int device, obt_model** out) {
 
   // leaf bank: binary16 bits, or binary64 stored as fp32 when that is exact
   const size_t per_tree_in = (size_t)1 << D, per_tree = (size_t)1 << DI;
+  const int C = d->n_outputs;
   if (d->precision == OBT_PRECISION_BINARY16) {
     m->leaf_storage = 2;
   } else {
     bool exact32 = true;
-    for (size_t i = 0; i < (size_t)m->n_trees * per_tree_in && exact32; ++i) {
+    for (size_t i = 0; i < (size_t)m->n_trees * C * per_tree_in && exact32; ++i) {
       const double v = d->leaves[i];
       const float f = (float)v;
       exact32 = std::isfinite(f) && (double)f == v && !(v == 0.0 && std::signbit(v) != std::signbit(f));
@@ -714,6 +638,28 @@ int obt_model_create(const obt_model_desc* d, int device, obt_model** out) {
     m->leaf_storage = exact32 ? 1 : 0;
   }
   const size_t ls = leaf_size(m->leaf_storage);
+  if (C > 1) {
+    // multi-output records [T][2^DI][CP]: one leaf's C values contiguous, rows of 16 bytes
+    const int CP = m->leaf_storage == 1 ? (C + 3) / 4 * 4 : (C + 1) / 2 * 2;
+    std::vector<uint8_t> rec((size_t)std::max(m->n_trees, 1) * per_tree * CP * ls, 0);
+    for (int t = 0; t < m->n_trees; ++t)
+      for (int c = 0; c < C; ++c)
+        for (size_t j = 0; j < per_tree_in; ++j) {
+          const double v = d->leaves[(((size_t)t * C + c) << D) + j];
+          uint8_t* dst = rec.data() + (((size_t)t * per_tree + j) * CP + c) * ls;
+          if (m->leaf_storage == 0) std::memcpy(dst, &v, 8);
+          else { const float f = (float)v; std::memcpy(dst, &f, 4); }
+        }
+    CUDA_TRY(cudaMalloc(&m->d_multi_leaves, rec.size()));
+    CUDA_TRY(cudaMemcpy(m->d_multi_leaves, rec.data(), rec.size(), cudaMemcpyHostToDevice));
+    // descriptors for the fixed multi-output tile
+    std::vector<uint32_t> desc((size_t)std::max(m->n_trees, 1) * DI * 2, 0);
+    for (int t = 0; t < m->n_trees; ++t) tree_descriptors(m.get(), t, kMultiTile, desc.data() + (size_t)t * DI * 2);
+    CUDA_TRY(cudaMalloc(&m->d_multi_desc, desc.size() * 4));
+    CUDA_TRY(cudaMemcpy(m->d_multi_desc, desc.data(), desc.size() * 4, cudaMemcpyHostToDevice));
+    *out = m.release();
+    return OBT_OK;
+  }
   m->leaf_bytes.assign((size_t)m->n_trees * per_tree * ls, 0);
   for (int t = 0; t < m->n_trees; ++t) {
     for (size_t j = 0; j < per_tree_in; ++j) {
@@ -781,7 +727,14 @@ static int predict_impl(obt_model* m, const float* x, int64_t n, int32_t layout,
   if (ev_begin) CUDA_TRY(cudaEventRecord(ev_begin, stream));
   int rc = launch_quantize(m, x, n, layout, q, true, tile, n_slots, stream);
   if (rc == OBT_OK && ev_mid) CUDA_TRY(cudaEventRecord(ev_mid, stream));
-  if (rc == OBT_OK) rc = launch_apply(m, q, n, tile, out, idx_out, tree_begin, tree_end, stream);
+  if (rc == OBT_OK) {
+    if (m->n_outputs > 1) {
+      rc = idx_out ? fail(OBT_E_UNSUPPORTED, "leaf-index dumps are implemented for single-output models")
+                   : launch_multi(m, q, n, out, stream);
+    } else {
+      rc = launch_apply(m, q, n, tile, out, idx_out, tree_begin, tree_end, stream);
+    }
+  }
   if (rc == OBT_OK && ev_end) CUDA_TRY(cudaEventRecord(ev_end, stream));
   if (owned) cudaFreeAsync(q, stream);
   return rc;
@@ -887,13 +840,14 @@ int obt_predict_host(const obt_model* mc, const float* x_host, int64_t n, int32_
   float* x_dev = nullptr;
   double* out_dev = nullptr;
   CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&x_dev), xbytes, stream));
-  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&out_dev), (size_t)n * sizeof(double), stream));
+  const size_t out_bytes = (size_t)n * m->n_outputs * sizeof(double);
+  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&out_dev), out_bytes, stream));
   rc = OBT_OK;
   cudaError_t e = cudaMemcpyAsync(x_dev, x_host, xbytes, cudaMemcpyHostToDevice, stream);
   if (e != cudaSuccess) rc = fail(OBT_E_CUDA, "host->device copy failed: %s", cudaGetErrorString(e));
   if (rc == OBT_OK) rc = predict_impl(m, x_dev, n, layout, out_dev, nullptr, 0, 0, nullptr, 0, stream);
   if (rc == OBT_OK) {
-    e = cudaMemcpyAsync(out_host, out_dev, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, stream);
+    e = cudaMemcpyAsync(out_host, out_dev, out_bytes, cudaMemcpyDeviceToHost, stream);
     if (e != cudaSuccess) rc = fail(OBT_E_CUDA, "device->host copy failed: %s", cudaGetErrorString(e));
   }
   cudaFreeAsync(x_dev, stream);

@@ -650,4 +650,90 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_split_kernel(const 
   }
 }
 
+// ---------------------------------------------------------------------------
+// K4: multi-output apply (C > 1 outputs per leaf; BASELINE config 5: C = 10, depth 10).
+// A leaf record is C values (40 bytes at C = 10, fp32), so per-tile staging of leaf
+// tables (40 KB per tree) cannot amortise; instead the tables stay in global memory and
+// every CTA walks the trees in the same order, so the active window of tables stays
+// L2-resident (with tree sharding across GPUs each GPU's tables fit L2 outright).
+// No shared memory: many CTAs per SM hide the L2 latency.  Each thread owns 4 objects
+// (one SWAR bucket word read from the tile-blocked matrix through L1), builds their
+// leaf indices exactly as K2, then gathers each object's C-value record and folds every
+// output in tree order in binary64.
+struct MultiParams {
+  const uint8_t* q;        // tiled buckets [n_tiles][F][tile]
+  const uint32_t* desc;    // [T_pad][DI][2] {off = f * tile, k replicated} (7-bit) or {(off<<8)|k, s}
+  const void* leaves;      // [T_pad][2^DI][CP] fp32 or fp64
+  double* out;             // [n][C] predictions / fold carry
+  int64_t n;
+  int32_t n_features, tile, n_outputs;
+  int32_t tree_begin, tree_end;  // trees folded by this launch
+  int32_t first, last;
+  double scale, bias;
+};
+
+constexpr int kMultiThreads = 128;  // 512 objects per CTA = one tile
+
+template <int DI, int CMP, int LEAF, int C>
+__global__ void __launch_bounds__(kMultiThreads) apply_multi_kernel(const __grid_constant__ MultiParams p) {
+  using leaf_t = typename LeafT<LEAF>::T;
+  constexpr int CP = LEAF == 1 ? (C + 3) / 4 * 4 : (C + 1) / 2 * 2;  // record stride (16-byte rows)
+  const int word = threadIdx.x;
+  const int64_t tile_idx = blockIdx.x;
+  const uint8_t* qrow0 = p.q + tile_idx * (int64_t)p.n_features * p.tile + 4 * word;
+  const int64_t obj0 = tile_idx * p.tile + 4 * word;
+  double acc[4][C];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+      acc[k][c] = (p.first || obj0 + k >= p.n) ? 0.0 : p.out[(obj0 + k) * C + c];
+  for (int t = p.tree_begin; t < p.tree_end; ++t) {
+    const uint2* ds = reinterpret_cast<const uint2*>(p.desc) + (size_t)t * DI;
+    uint32_t lo = 0, hi = 0;
+#pragma unroll
+    for (int d = 0; d < DI; ++d) {
+      const uint2 dd = __ldg(ds + d);  // warp-uniform address: one broadcast
+      uint32_t b7;
+      if constexpr (CMP == 7) {
+        b7 = __ldg(reinterpret_cast<const uint32_t*>(qrow0 + dd.x)) + dd.y;
+      } else {
+        const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(qrow0 + (dd.x >> 8)));
+        b7 = maj3((w & 0x7f7f7f7fu) + (__byte_perm(dd.x, 0u, 0x0000u) & 0x7f7f7f7fu), w, dd.y);
+      }
+      if (d < 8) lo |= (b7 >> (7 - d)) & (0x01010101u << d);
+      else hi |= (b7 >> (15 - d)) & (0x01010101u << (d - 8));
+    }
+    const leaf_t* tab = reinterpret_cast<const leaf_t*>(p.leaves) + ((size_t)t << DI) * CP;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t idx = ((lo >> (8 * k)) & 0xffu) | (DI > 8 ? ((hi >> (8 * k)) & 0xffu) << 8 : 0u);
+      const leaf_t* rec = tab + (size_t)idx * CP;
+      leaf_t v[CP];
+      if constexpr (LEAF == 1) {
+#pragma unroll
+        for (int c4 = 0; c4 < CP / 4; ++c4) {
+          const float4 q4 = __ldg(reinterpret_cast<const float4*>(rec) + c4);
+          v[4 * c4 + 0] = q4.x; v[4 * c4 + 1] = q4.y; v[4 * c4 + 2] = q4.z; v[4 * c4 + 3] = q4.w;
+        }
+      } else {
+#pragma unroll
+        for (int c2 = 0; c2 < CP / 2; ++c2) {
+          const double2 q2 = __ldg(reinterpret_cast<const double2*>(rec) + c2);
+          v[2 * c2 + 0] = q2.x; v[2 * c2 + 1] = q2.y;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < C; ++c) acc[k][c] += (double)v[c];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (obj0 + k >= p.n) continue;
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+      p.out[(obj0 + k) * C + c] = p.last ? __dadd_rn(__dmul_rn(acc[k][c], p.scale), p.bias) : acc[k][c];
+  }
+}
+
 }  // namespace obt

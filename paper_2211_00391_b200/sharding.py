@@ -51,8 +51,11 @@ def tree_shard(n_trees: int, rank: int, world: int) -> tuple:
     return balanced_ranges(n_trees, world, quantum=4)[rank]
 
 
-def tree_submodel(model: ObliviousModel, begin: int, end: int) -> ObliviousModel:
-    """The trees [begin, end) with scale 1 / bias 0: its predictions are raw partial sums."""
+def tree_submodel(model, begin: int, end: int):
+    """The trees [begin, end) with scale 1 / bias 0: its predictions are raw partial sums.
+    Works for ObliviousModel and multiclass.MultiOutputModel."""
+    if hasattr(model, "subset"):
+        return model.subset(begin, end, raw=True)
     return ObliviousModel(model.float_features, model.trees[begin:end], scale=1.0, bias=0.0)
 
 
@@ -130,9 +133,14 @@ class TreeShardedEvaluator:
         self.tree_range = (b, e)
         self.submodel = tree_submodel(model, b, e)
         if local_predict is None:
-            from .evaluate import Evaluator
+            if hasattr(self.submodel, "subset"):
+                from .multiclass import MultiOutputEvaluator
 
-            ev = Evaluator(self.submodel, config, device=device)
+                ev = MultiOutputEvaluator(self.submodel, device=device)
+            else:
+                from .evaluate import Evaluator
+
+                ev = Evaluator(self.submodel, config, device=device)
             local_predict = lambda m, x: ev.predict(x)  # noqa: E731
             reduce_device = reduce_device or f"cuda:{ev.device}"
         self._predict = local_predict

@@ -240,3 +240,41 @@ def test_descriptor_sources_and_multi_launch_fold(monkeypatch, source, strategy)
     idx = stages.as_uint16(stages.leaf_indices(model, torch.from_numpy(x).cuda(), tree_begin=1290, tree_end=1400))
     fm = oracle.flatten(model)
     assert np.array_equal(idx, oracle.leaf_indices(fm, oracle.quantize(fm, x))[1290:1400])
+
+
+@pytest.mark.parametrize("D,C,F,B", [(10, 10, 40, 254), (6, 3, 17, 64), (8, 16, 9, 128), (3, 2, 5, 7)])
+def test_multi_output_bit_exact(D, C, F, B):
+    """Multi-output (config 5 shape family): K4 against the oracle restatement."""
+    from paper_2211_00391_b200 import multiclass
+
+    spec = synthetic.WorkloadSpec("m", 1, F, B, 57, D, 0.01, n_outputs=C, cfg=5)
+    arrays = synthetic.model_arrays(spec, seed=D * 100 + C, affine=True)
+    model = multiclass.from_arrays(arrays)
+    x = _features(obt.ObliviousModel(tuple(obt.FloatFeatureBorders(f, b) for f, b in enumerate(arrays["borders"])),
+                                      (), 1.0, 0.0), 1031, seed=D + C)
+    fm = oracle.FlatModel(np.stack(arrays["borders"]), np.full(F, B, np.int32), np.full(57, D, np.int32),
+                          arrays["split_feature"], arrays["split_ordinal"], arrays["leaves"], model.scale, model.bias)
+    want = oracle.evaluate_scalar(fm, x)
+    ev = multiclass.MultiOutputEvaluator(model)
+    got = ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
+    assert got.shape == (1031, C)
+    assert np.array_equal(got, want)
+    dev = ev.predict_device(torch.from_numpy(np.ascontiguousarray(x.T)).cuda(), obt.Layout.FEATURE_MAJOR).cpu().numpy()
+    assert np.array_equal(dev, want)
+
+
+def test_multi_output_tree_shard_partials_sum_to_prediction():
+    """Tree sharding of a multi-output model: partial sums of the shards (scale 1, bias 0)
+    reduce to the full prediction within binary64 reassociation."""
+    from paper_2211_00391_b200 import multiclass, sharding
+
+    spec = synthetic.WorkloadSpec("m", 1, 30, 100, 203, 10, 0.01, n_outputs=10, cfg=5)
+    model = multiclass.from_arrays(synthetic.model_arrays(spec, seed=5, affine=True))
+    x = np.random.default_rng(1).standard_normal((777, 30)).astype(np.float32)
+    full = multiclass.MultiOutputEvaluator(model).predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
+    parts = []
+    for r in range(4):
+        b, e = sharding.tree_shard(model.n_trees, r, 4)
+        parts.append(multiclass.MultiOutputEvaluator(model.subset(b, e)).predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR)))
+    combined = sum(parts) * model.scale + model.bias
+    assert np.max(np.abs(combined - full) / np.maximum(np.abs(full), 1e-300)) < 1e-12

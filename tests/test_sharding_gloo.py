@@ -23,9 +23,17 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
+def _flat(model):
+    if not hasattr(model, "subset"):
+        return oracle.flatten(model)
+    return oracle.FlatModel(np.stack(model.borders), np.array([b.size for b in model.borders], np.int32),
+                            np.full(model.n_trees, model.depth, np.int32), model.split_feature, model.split_ordinal,
+                            model.leaves, model.scale, model.bias)
+
+
 def _oracle_predict(model, matrix):
     layout = oracle.OBJECT_MAJOR if matrix.layout is obt.Layout.OBJECT_MAJOR else oracle.FEATURE_MAJOR
-    return oracle.evaluate_scalar(oracle.flatten(model), matrix.values, layout)
+    return oracle.evaluate_scalar(_flat(model), matrix.values, layout)
 
 
 def _worker(rank, world, port, case):
@@ -49,6 +57,17 @@ def _worker(rank, world, port, case):
                 local = ev.predict(m, gather=False)
                 b, e = sharding.object_shard(x.shape[0], rank, world)
                 assert np.array_equal(local, full[b:e])
+        elif case == "trees_multi":
+            from paper_2211_00391_b200 import multiclass, synthetic
+
+            spec = synthetic.WorkloadSpec("m", 1, 9, 40, 101, 10, 0.01, n_outputs=10, cfg=5)
+            mm = multiclass.from_arrays(synthetic.model_arrays(spec, seed=3, affine=True))
+            full_m = oracle.evaluate_scalar(_flat(mm), x)
+            ev = sharding.TreeShardedEvaluator(mm, local_predict=_oracle_predict, reduce_device="cpu")
+            got = ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
+            assert got.shape == full_m.shape == (x.shape[0], 10)
+            rel = np.abs(got - full_m) / np.maximum(np.maximum(np.abs(got), np.abs(full_m)), 1e-300)
+            assert rel.max() <= 1e-12, rel.max()
         else:
             ev = sharding.TreeShardedEvaluator(model, local_predict=_oracle_predict, reduce_device="cpu")
             got = ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
@@ -60,7 +79,7 @@ def _worker(rank, world, port, case):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case", ["objects", "trees"])
+@pytest.mark.parametrize("case", ["objects", "trees", "trees_multi"])
 def test_two_rank_gloo(case):
     mp.spawn(_worker, args=(2, _free_port(), case), nprocs=2, join=True)
 
