@@ -400,7 +400,11 @@ int launch_quantize(const obt_model* m, const float* x, int64_t n, int layout, u
   p.eytz_pitch = bt.pitch;
   p.out = out;
   p.tile = tile;
-  const int fc = obt::quantize_chunk_features(bt.levels > 0 ? bt.pitch : 0, m->n_features);
+  int fc = obt::quantize_chunk_features(bt.levels > 0 ? bt.pitch : 0, m->n_features);
+  // small batches: split the features finer (multiples of the 8-feature step) until the
+  // grid has ~2 CTAs per SM, so a 10k-object batch is not quantized by 10 CTAs
+  const int64_t blocks = (n_slots + obt::kQuantBlock - 1) / obt::kQuantBlock;
+  while (fc > 8 && blocks * ((m->n_features + fc - 1) / fc) < 2 * m->sm_count) fc = std::max(8, (fc / 2 + 7) / 8 * 8);
   const size_t smem = bt.levels > 0 ? (size_t)std::min(fc, m->n_features) * bt.pitch * 4 : 16;
   p.chunk_features = fc;
   p.two = 2;
@@ -836,24 +840,70 @@ int obt_predict_host(const obt_model* mc, const float* x_host, int64_t n, int32_
   if (!x_host || !out_host) return fail(OBT_E_INVALID, "null feature or output pointer");
   DeviceGuard guard(m->device);
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
-  const size_t xbytes = (size_t)n * m->n_features * sizeof(float);
-  float* x_dev = nullptr;
-  double* out_dev = nullptr;
-  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&x_dev), xbytes, stream));
-  const size_t out_bytes = (size_t)n * m->n_outputs * sizeof(double);
-  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&out_dev), out_bytes, stream));
+  const int F = m->n_features, C = m->n_outputs;
+  // Chunked pipeline: the features of chunk i+1 cross PCIe on a copy stream while chunk
+  // i is quantized and applied on `stream`; each chunk's scores go back right behind its
+  // compute.  Two device buffers per side; chunks are whole 1024-object blocks of about
+  // 128 MB of features (a single chunk when the batch is small).
+  int64_t rows = std::max<int64_t>(1024, ((int64_t)128 << 20) / ((int64_t)F * 4) / 1024 * 1024);
+  rows = std::min(rows, n);
+  const int64_t n_chunks = (n + rows - 1) / rows;
+  const int nbuf = n_chunks > 1 ? 2 : 1;
+  float* x_dev[2] = {nullptr, nullptr};
+  double* out_dev[2] = {nullptr, nullptr};
+  cudaStream_t copy = nullptr;
+  cudaEvent_t copied[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
   rc = OBT_OK;
-  cudaError_t e = cudaMemcpyAsync(x_dev, x_host, xbytes, cudaMemcpyHostToDevice, stream);
-  if (e != cudaSuccess) rc = fail(OBT_E_CUDA, "host->device copy failed: %s", cudaGetErrorString(e));
-  if (rc == OBT_OK) rc = predict_impl(m, x_dev, n, layout, out_dev, nullptr, 0, 0, nullptr, 0, stream);
-  if (rc == OBT_OK) {
-    e = cudaMemcpyAsync(out_host, out_dev, out_bytes, cudaMemcpyDeviceToHost, stream);
-    if (e != cudaSuccess) rc = fail(OBT_E_CUDA, "device->host copy failed: %s", cudaGetErrorString(e));
+  auto cuda_ok = [&](cudaError_t e, const char* what) {
+    if (e != cudaSuccess && rc == OBT_OK) rc = fail(OBT_E_CUDA, "%s failed: %s", what, cudaGetErrorString(e));
+    return rc == OBT_OK;
+  };
+  cuda_ok(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking), "copy stream");
+  for (int b = 0; b < nbuf && rc == OBT_OK; ++b) {
+    cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&x_dev[b]), (size_t)rows * F * 4, stream), "feature buffer");
+    cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&out_dev[b]), (size_t)rows * C * 8, stream), "score buffer");
+    cuda_ok(cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming), "event");
+    cuda_ok(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming), "event");
   }
-  cudaFreeAsync(x_dev, stream);
-  cudaFreeAsync(out_dev, stream);
-  e = cudaStreamSynchronize(stream);
+  // the copy stream must not start before the buffers exist on `stream`
+  cudaEvent_t ready = nullptr;
+  if (cuda_ok(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event")) {
+    cuda_ok(cudaEventRecord(ready, stream), "event record");
+    cuda_ok(cudaStreamWaitEvent(copy, ready, 0), "stream wait");
+  }
+  int launches = 0;
+  for (int64_t i = 0; i < n_chunks && rc == OBT_OK; ++i) {
+    const int b = (int)(i % nbuf);
+    const int64_t o0 = i * rows, ni = std::min(rows, n - o0);
+    if (i >= nbuf) cuda_ok(cudaStreamWaitEvent(copy, done[b], 0), "stream wait");  // buffer b free again
+    if (layout == OBT_LAYOUT_OBJECT_MAJOR) {
+      cuda_ok(cudaMemcpyAsync(x_dev[b], x_host + o0 * F, (size_t)ni * F * 4, cudaMemcpyHostToDevice, copy), "H2D");
+    } else {  // feature-major: ni columns of every feature row
+      cuda_ok(cudaMemcpy2DAsync(x_dev[b], (size_t)ni * 4, x_host + o0, (size_t)n * 4, (size_t)ni * 4, F,
+                                cudaMemcpyHostToDevice, copy), "H2D");
+    }
+    cuda_ok(cudaEventRecord(copied[b], copy), "event record");
+    cuda_ok(cudaStreamWaitEvent(stream, copied[b], 0), "stream wait");
+    if (rc != OBT_OK) break;
+    rc = predict_impl(m, x_dev[b], ni, layout, out_dev[b], nullptr, 0, 0, nullptr, 0, stream);
+    launches += g_launches;
+    cuda_ok(cudaMemcpyAsync(out_host + o0 * C, out_dev[b], (size_t)ni * C * 8, cudaMemcpyDeviceToHost, stream), "D2H");
+    cuda_ok(cudaEventRecord(done[b], stream), "event record");
+  }
+  g_launches = launches;
+  for (int b = 0; b < nbuf; ++b) {
+    if (x_dev[b]) cudaFreeAsync(x_dev[b], stream);
+    if (out_dev[b]) cudaFreeAsync(out_dev[b], stream);
+  }
+  const cudaError_t e = cudaStreamSynchronize(stream);
   if (rc == OBT_OK && e != cudaSuccess) rc = fail(OBT_E_CUDA, "stream synchronize failed: %s", cudaGetErrorString(e));
+  cudaStreamSynchronize(copy);
+  for (int b = 0; b < nbuf; ++b) {
+    if (copied[b]) cudaEventDestroy(copied[b]);
+    if (done[b]) cudaEventDestroy(done[b]);
+  }
+  if (ready) cudaEventDestroy(ready);
+  if (copy) cudaStreamDestroy(copy);
   return rc;
 }
 
