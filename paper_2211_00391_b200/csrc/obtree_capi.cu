@@ -283,19 +283,22 @@ void tree_descriptors(const obt_model* m, int t, int tile, uint32_t* out) {
 // descriptor path, and the flat descriptor stream for the parameter-bank path.
 int build_tile_plan(obt_model* m, int tile, TilePlan& out) {
   const int DI = m->depth_inst;
-  const int dwt = obt::desc_words_per_tree(DI, m->compare_mode);
+  const int dwt = obt::desc_words_per_tree(DI, m->compare_mode);  // words in the smem records
   const size_t per_tree_leaf = leaf_size(m->leaf_storage) << DI;  // bytes of real leaves
   const size_t stride = table_stride(m);                           // their slot in the record
   const int ct = m->chunk_trees;
   const size_t desc_bytes = m->desc_bytes, chunk_bytes = m->chunk_bytes;
   std::vector<uint8_t> host((size_t)std::max(m->n_chunks, 1) * chunk_bytes, 0);
   out.param_desc.assign((size_t)m->padded_trees * DI * 2, 0u);
-  std::vector<uint32_t> words(dwt);
+  std::vector<uint32_t> words((size_t)DI * 2);
   for (int t = 0; t < m->padded_trees; ++t) {
     const int c = t / ct, tl = t % ct;
     uint8_t* rec = host.data() + (size_t)c * chunk_bytes;
     tree_descriptors(m, t, tile, words.data());
     if (m->compare_mode == 7) std::memcpy(out.param_desc.data() + (size_t)t * DI * 2, words.data(), (size_t)DI * 8);
+    if (dwt == DI) {  // packed 7-bit records: (off << 8) | k
+      for (int d = 0; d < DI; ++d) words[d] = (words[2 * d] << 8) | (words[2 * d + 1] & 0xFFu);
+    }
     // shared-memory copy: trees in groups of 4, each group's words contiguous
     std::memcpy(rec + (size_t)tl * dwt * 4, words.data(), (size_t)dwt * 4);
     uint8_t* leaf_dst = rec + desc_bytes + (size_t)tl * stride;

@@ -251,7 +251,12 @@ __global__ void __launch_bounds__(kQuantThreads, 2) quantize_kernel(QuantizePara
 // trees (larger leaf tables) use groups of 8 / 4 so a chunk still fits the ring without
 // shrinking the bucket tile.
 __host__ __device__ constexpr int tree_group(int di) { return di <= 6 ? 16 : di <= 8 ? 8 : 4; }
-__host__ __device__ constexpr int desc_words(int cmp) { return 2; }
+#ifndef OBT_PACKED_DESC
+#define OBT_PACKED_DESC 0
+#endif
+// Shared-memory descriptor words per split: 7-bit compare {off, k replicated} (2 words,
+// or 1 packed word (off << 8) | k with OBT_PACKED_DESC), 8-bit {(off << 8) | k, s}.
+__host__ __device__ constexpr int desc_words(int cmp) { return (cmp == 7 && OBT_PACKED_DESC) ? 1 : 2; }
 __host__ __device__ constexpr int desc_words_per_tree(int di, int cmp) { return di * desc_words(cmp); }
 
 struct ApplyParams {
@@ -452,8 +457,13 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid
             b7s[0] = w[0] + krep;
           } else {
             // shared-memory descriptors: 7-bit {off, k replicated}; 8-bit {(off << 8) | k, s}
-            const uint32_t d0 = dw[(tt * DI + d) * kDW], d1 = dw[(tt * DI + d) * kDW + 1];
-            if constexpr (CMP == 7) {
+            const uint32_t d0 = dw[(tt * DI + d) * kDW], d1 = dw[(tt * DI + d) * kDW + (kDW - 1)];
+            if constexpr (CMP == 7 && kDW == 1) {
+              lds_words<W>(my_q + (d0 >> 8), w);
+              const uint32_t krep = __byte_perm(d0, 0u, 0x0000u);
+#pragma unroll
+              for (int x = 0; x < W; ++x) b7s[x] = w[x] + krep;
+            } else if constexpr (CMP == 7) {
               lds_words<W>(my_q + d0, w);
 #pragma unroll
               for (int x = 0; x < W; ++x) b7s[x] = w[x] + d1;
@@ -602,7 +612,8 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_split_kernel(const 
   for (int k = 0; k < kOPT; ++k) acc[k] = (p.first || obj0 + k >= p.n) ? (acc_t)0 : (acc_t)p.out[obj0 + k];
   mbar_wait_warp(tile_bar, 0);
 
-  const uint32_t my_desc = (uint32_t)(part * kDPT) * 8u;  // this lane's first descriptor in a tree
+  constexpr int kDW = desc_words(CMP);
+  const uint32_t my_desc = (uint32_t)(part * kDPT) * 4u * kDW;  // this lane's first descriptor in a tree
   for (int c = 0; c < n_chunks; ++c) {
     const int s = c % p.n_stages;
     mbar_wait_warp(&full[s], (uint32_t)(c / p.n_stages) & 1u);
@@ -613,14 +624,20 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_split_kernel(const 
 #pragma unroll
       for (int tt = 0; tt < kTreeGroup; ++tt) {
         const int t = g * kTreeGroup + tt;
-        const uint32_t tree_desc = desc_base + (uint32_t)t * (uint32_t)(DI * 8);
+        const uint32_t tree_desc = desc_base + (uint32_t)t * (uint32_t)(DI * 4 * kDW);
         uint32_t part_a = 0, part_b = 0;
 #pragma unroll
         for (int i = 0; i < kDPT; ++i) {
-          uint32_t d0, d1;
-          asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(d0), "=r"(d1) : "r"(tree_desc + 8u * i));
+          uint32_t d0, d1 = 0;
+          if constexpr (kDW == 2) {
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(d0), "=r"(d1) : "r"(tree_desc + 8u * i));
+          } else {
+            d0 = lds_u32(tree_desc + 4u * i);
+          }
           uint32_t b7;
-          if constexpr (CMP == 7) {
+          if constexpr (CMP == 7 && kDW == 1) {
+            b7 = lds_u32(my_q + (d0 >> 8)) + __byte_perm(d0, 0u, 0x0000u);
+          } else if constexpr (CMP == 7) {
             b7 = lds_u32(my_q + d0) + d1;
           } else {
             const uint32_t w = lds_u32(my_q + (d0 >> 8));
