@@ -278,3 +278,37 @@ def test_multi_output_tree_shard_partials_sum_to_prediction():
         parts.append(multiclass.MultiOutputEvaluator(model.subset(b, e)).predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR)))
     combined = sum(parts) * model.scale + model.bias
     assert np.max(np.abs(combined - full) / np.maximum(np.abs(full), 1e-300)) < 1e-12
+
+
+@pytest.mark.parametrize("n", [1, 129, 1000, 4097])
+@pytest.mark.parametrize("tpw", ["1", "2"])
+def test_no_writes_outside_outputs_and_workspace(monkeypatch, n, tpw):
+    """compute-sanitizer is unavailable on this pool: guard regions around the score
+    vector and the bucket workspace must be untouched after a predict (ragged n, both
+    apply kernels), and results must still match the oracle."""
+    monkeypatch.setenv("OBT_TPW", tpw)
+    model = _model(24, 60, 75, 6, seed=n)
+    x = _features(model, n, seed=n)
+    ev = obt.Evaluator(model)
+    guard = 64
+    out = torch.full((n + guard,), 12345.0, dtype=torch.float64, device="cuda")
+    ws_bytes = ev.workspace_bytes(n)
+    ws = torch.full((ws_bytes + 4096,), 0xAB, dtype=torch.uint8, device="cuda")
+    ev.predict_device(torch.from_numpy(x).cuda(), out=out[:n], workspace=ws[:ws_bytes])
+    torch.cuda.synchronize()
+    assert torch.all(out[n:] == 12345.0)
+    assert torch.all(ws[ws_bytes:] == 0xAB)
+    assert np.array_equal(out[:n].cpu().numpy(), oracle.evaluate_scalar(oracle.flatten(model), x))
+
+
+def test_multi_output_no_writes_outside_output():
+    from paper_2211_00391_b200 import multiclass
+
+    spec = synthetic.WorkloadSpec("m", 1, 11, 30, 21, 10, 0.01, n_outputs=10, cfg=5)
+    mm = multiclass.from_arrays(synthetic.model_arrays(spec, seed=9))
+    n = 777
+    x = torch.randn(n, 11, device="cuda")
+    big = torch.full((n * 10 + 80,), -7.0, dtype=torch.float64, device="cuda")
+    multiclass.MultiOutputEvaluator(mm).predict_device(x, out=big[: n * 10].view(n, 10))
+    torch.cuda.synchronize()
+    assert torch.all(big[n * 10:] == -7.0)
