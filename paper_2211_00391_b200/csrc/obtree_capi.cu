@@ -348,6 +348,10 @@ int plan_tile(const obt_model* m, int64_t n) {
   int64_t tmax = (m->smem_optin - fixed) / m->n_features;
   tmax = std::min<int64_t>(tmax / kTileQuantum * kTileQuantum, 4 * (obt::kApplyMaxThreads - obt::kApplyProducerThreads) / kTileQuantum * kTileQuantum);
   if (tmax < kTileQuantum) return -1;
+  if (const char* e = getenv("OBT_TILE")) {  // tuning override (multiple of 128, within the cap)
+    const int64_t t = atoll(e);
+    if (t >= kTileQuantum && t % kTileQuantum == 0 && t <= tmax) return (int)t;
+  }
   int64_t want = (n + m->sm_count - 1) / m->sm_count;
   want = std::max<int64_t>(kTileQuantum, (want + kTileQuantum - 1) / kTileQuantum * kTileQuantum);
   return (int)std::min(tmax, want);

@@ -128,13 +128,8 @@ __device__ __forceinline__ uint32_t eytz_level(uint32_t o, float x, const float*
   return o * two + (x > b ? 8u : 4u);
 }
 
-constexpr int kQuantStep = 8;  // features per step: two 16-byte loads = one 32-byte sector per row
+constexpr int kQuantStep = 8;  // features per step: one 32-byte sector per row
 
-// One CTA: 1024 objects (8 warps x 32 lanes x 4 objects) x one chunk of features
-// (grid.y).  The chunk's Eytzinger arrays are staged in shared memory once; each lane
-// then walks its 4 objects x 8 features per step: full 32-byte sectors of the raw values
-// straight from HBM, 32 independent searches, 8 packed 32-bit bucket stores (each warp
-// writes 128 contiguous bytes of a feature row of the tile-blocked matrix).
 template <int L, int LAYOUT, bool TILED>
 __global__ void __launch_bounds__(kQuantThreads, 2) quantize_kernel(QuantizeParams p) {
   extern __shared__ __align__(16) unsigned char qsm[];
@@ -156,12 +151,25 @@ __global__ void __launch_bounds__(kQuantThreads, 2) quantize_kernel(QuantizePara
   if (ob >= p.n_slots) return;  // past the last tile (no barrier follows)
   const bool full_objs = ob + 3 < p.n;
   const bool vec_rows = LAYOUT == 0 ? ((F & 3) == 0 && (f0 & 3) == 0) : ((p.n & 3) == 0);
+  static_assert(kQuantStep == 8, "a 256-bit row load covers exactly one step");
+  const bool sector_rows = LAYOUT == 0 && (F & 7) == 0 && (reinterpret_cast<uintptr_t>(p.x) & 31) == 0;
   const uint32_t two = (uint32_t)p.two;
-  for (int fq = 0; fq < nf; fq += S) {
-    // raw values v[j][k]: object ob + k, feature f0 + fq + j
-    float v[S][4];
+  // raw values v[j][k] of one step: object ob + k, feature f0 + fq + j
+  auto load_step = [&](float (&v)[S][4], int fq) {
     if (full_objs && vec_rows && fq + S <= nf) {
-      if (LAYOUT == 0) {
+      if (LAYOUT == 0 && sector_rows) {
+        // one 256-bit load per row: the lane takes a whole 32-byte sector at once (two
+        // 128-bit loads per sector measured 43% excess L2 sectors: the second half
+        // often missed L1 again)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float* row = p.x + (ob + k) * F + f0 + fq;
+          asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                       : "=f"(v[0][k]), "=f"(v[1][k]), "=f"(v[2][k]), "=f"(v[3][k]),
+                         "=f"(v[4][k]), "=f"(v[5][k]), "=f"(v[6][k]), "=f"(v[7][k])
+                       : "l"(row));
+        }
+      } else if (LAYOUT == 0) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const float4* row = reinterpret_cast<const float4*>(p.x + (ob + k) * F + f0 + fq);
@@ -188,13 +196,40 @@ __global__ void __launch_bounds__(kQuantThreads, 2) quantize_kernel(QuantizePara
           v[j][k] = in ? __ldg(p.x + idx) : 0.0f;
         }
     }
+  };
+
+  // the 32 searches of one step and its 8 packed bucket-word stores
+  auto search_store = [&](const float (&v)[S][4], int fq) {
     uint32_t o[S][4];
 #pragma unroll
     for (int j = 0; j < S; ++j)
 #pragma unroll
       for (int k = 0; k < 4; ++k) o[j][k] = 0;
+    // levels 0-2 from registers: the feature's 7 top nodes are loaded once (three
+    // broadcast loads) and serve the lane's 4 objects, so each value makes L - 3
+    // dependent shared-memory lookups instead of L
+    constexpr int kTop = L >= 4 ? 3 : 0;
+    if constexpr (kTop == 3) {
 #pragma unroll
-    for (int l = 0; l < L; ++l)
+      for (int j = 0; j < S; ++j) {
+        const float* e = ey + min(fq + j, nf - 1) * kE;
+        float n[7];
+#pragma unroll
+        for (int i = 0; i < 7; ++i) n[i] = e[i];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float x = v[j][k];
+          const bool c0 = x > n[0];
+          const bool c1 = x > (c0 ? n[2] : n[1]);
+          const float b2 = c0 ? (c1 ? n[6] : n[5]) : (c1 ? n[4] : n[3]);
+          const bool c2 = x > b2;
+          // Eytzinger position after three levels: 7 + 4 c0 + 2 c1 + c2 (byte offset x4)
+          o[j][k] = 28u + (c0 ? 16u : 0u) + (c1 ? 8u : 0u) + (c2 ? 4u : 0u);
+        }
+      }
+    }
+#pragma unroll
+    for (int l = kTop; l < L; ++l)
 #pragma unroll
       for (int j = 0; j < S; ++j) {
         const float* e = ey + min(fq + j, nf - 1) * kE;
@@ -226,6 +261,12 @@ __global__ void __launch_bounds__(kQuantThreads, 2) quantize_kernel(QuantizePara
           if (ob + k < p.n) p.out[(int64_t)f * p.n + ob + k] = (uint8_t)(word >> (8 * k));
       }
     }
+  };
+
+  for (int fq = 0; fq < nf; fq += S) {
+    float v[S][4];
+    load_step(v, fq);
+    search_store(v, fq);
   }
 }
 
