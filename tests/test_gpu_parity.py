@@ -312,3 +312,49 @@ def test_multi_output_no_writes_outside_output():
     multiclass.MultiOutputEvaluator(mm).predict_device(x, out=big[: n * 10].view(n, 10))
     torch.cuda.synchronize()
     assert torch.all(big[n * 10:] == -7.0)
+
+
+def test_reference_corpus_on_gpu():
+    """The reference's 100-model acceptance corpus (tests/golden/corpus.npz, written by
+    running the reference itself): GPU predictions equal the reference's outputs bit for
+    bit in both precision families, and GPU buckets / leaf indices equal its panels."""
+    from pathlib import Path
+
+    corpus = np.load(Path(__file__).parent / "golden" / "corpus.npz")
+    families = ((obt.LeafStrategy.NAIVE, "oracle64"), (obt.LeafStrategy.NAIVE16, "oracle16"))
+    off = 0
+    for i, (F, B, T, D, seed) in enumerate(corpus["specs"]):
+        model = oracle.to_model(oracle.synthetic_model(int(F), int(B), int(T), int(D), int(seed)), obt)
+        evs = [(obt.Evaluator(model, obt.EvalConfig(strategy=s)), key) for s, key in families]
+        for batch in corpus["batch_sizes"]:
+            x = oracle.feature_matrix(int(batch), int(F), int(seed) * 13 + int(batch), nan_fraction=0.02,
+                                      inf_fraction=0.01)
+            for ev, key in evs:
+                got = ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
+                assert np.array_equal(got, corpus[key][off: off + int(batch)]), (i, int(batch), key)
+            off += int(batch)
+    assert off == corpus["oracle64"].size
+    for name in corpus.files:
+        if not name.startswith("q"):
+            continue
+        i = int(name[1:])
+        F, B, T, D, seed = (int(v) for v in corpus["specs"][i])
+        model = oracle.to_model(oracle.synthetic_model(F, B, T, D, seed), obt)
+        x = torch.from_numpy(oracle.feature_matrix(257, F, seed * 13 + 257, nan_fraction=0.02, inf_fraction=0.01))
+        assert np.array_equal(stages.quantize(model, x.cuda()).cpu().numpy(), corpus[name])
+        assert np.array_equal(stages.as_uint16(stages.leaf_indices(model, x.cuda())), corpus[f"i{i}"].astype(np.uint16))
+
+
+@pytest.mark.parametrize("tpw", ["2", "4"])
+@pytest.mark.parametrize("D", [4, 8])
+@pytest.mark.parametrize("F,B,T", [(29, 100, 70), (3, 254, 200)])  # 7-bit / 8-bit compare after remap
+def test_depth_split_lanes_bit_exact(monkeypatch, tpw, D, F, B, T):
+    """K2s: TPW lanes per bucket word (OBT_TPW forces it) keep the tree-order fold exact."""
+    monkeypatch.setenv("OBT_TPW", tpw)
+    model = _model(F, B, T, D, seed=D * 100 + F)
+    x = _features(model, 3001, seed=D + F)
+    fm = oracle.flatten(model)
+    for strategy, prec in ((obt.LeafStrategy.NAIVE, oracle.BINARY64), (obt.LeafStrategy.NAIVE16, oracle.BINARY16)):
+        got = obt.Evaluator(model, obt.EvalConfig(strategy=strategy)).predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
+        want = oracle.evaluate_scalar(fm, x, oracle.OBJECT_MAJOR, prec)
+        assert np.array_equal(got, want), (strategy, int(np.count_nonzero(got != want)))
