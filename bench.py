@@ -99,6 +99,11 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(inside)}
 
 
+# NCCL on GPUs.  OBT_BENCH_DIST_BACKEND=gloo is a functional check of the multi-rank code
+# path on a box with fewer GPUs than ranks (ranks then share devices: never a measurement).
+DIST_BACKEND = os.environ.get("OBT_BENCH_DIST_BACKEND", "nccl")
+
+
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -107,10 +112,18 @@ def dist_setup():
         import torch
         import torch.distributed as dist
 
+        local = local % max(1, torch.cuda.device_count())
         torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if DIST_BACKEND == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(DIST_BACKEND)
     return world, rank, local
+
+
+def reduce_device() -> str:
+    return "cuda" if DIST_BACKEND == "nccl" else "cpu"
 
 
 def max_over_ranks(value: float, world: int) -> float:
@@ -119,7 +132,7 @@ def max_over_ranks(value: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    t = torch.tensor([value], dtype=torch.float64, device=reduce_device())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -167,6 +180,7 @@ def cpu_baseline(spec, model, seconds: float, verify_fn=None) -> dict:
     from paper_2211_00391_b200 import synthetic
 
     fm = flat_model(model)
+    oracle.set_threads(oracle.host_cores())  # all host cores, whatever OMP_NUM_THREADS says
     threads = oracle.max_threads()
     n = 4096
     best = None
@@ -231,6 +245,7 @@ def run_reference(args, world, rank):
     else:
         model = synthetic.build_model(spec)
     fm = flat_model(model)
+    oracle.set_threads(oracle.host_cores())  # torchrun exports OMP_NUM_THREADS=1; use every core
     prec = oracle.BINARY16 if spec.half_leaves else oracle.BINARY64
     n = args.ref_sample
     x = synthetic.host_features(spec, n_objects=n, seed=spec.data_seed + 7)
@@ -330,7 +345,10 @@ def run_ours(args, world, rank, local):
 
         torch.cuda.synchronize()
         r0 = time.perf_counter()
-        dist.all_reduce(out, op=dist.ReduceOp.SUM)  # the NCCL reduce of per-object partial sums
+        red = out if reduce_device() == "cuda" else out.cpu()
+        dist.all_reduce(red, op=dist.ReduceOp.SUM)  # the NCCL reduce of per-object partial sums
+        if red is not out:
+            out.copy_(red)
         out.mul_(full_model.scale).add_(full_model.bias)
         torch.cuda.synchronize()
         reduce_ms = (time.perf_counter() - r0) * 1e3

@@ -71,6 +71,8 @@ def lib() -> ctypes.CDLL:
         L.orc_xoshiro_next.restype = ctypes.c_uint64
         L.orc_xoshiro_next.argtypes = [vp]
         L.orc_max_threads.restype = ctypes.c_int
+        L.orc_set_threads.restype = None
+        L.orc_set_threads.argtypes = [i32]
         _lib = L
     return _lib
 
@@ -272,3 +274,18 @@ def model_digest(model) -> str:
 
 def max_threads() -> int:
     return int(lib().orc_max_threads())
+
+
+def set_threads(n: int) -> None:
+    """OpenMP threads for the oracle's parallel loops (overrides OMP_NUM_THREADS)."""
+    lib().orc_set_threads(int(n))
+
+
+def host_cores() -> int:
+    """Cores this process may run on."""
+    import os
+
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover - non-Linux
+        return os.cpu_count() or 1

@@ -42,6 +42,16 @@ static inline float feature_at(const float* x, int64_t n, int32_t n_features, in
 
 int orc_version(void) { return 1; }
 
+/* Thread count for the parallel loops (launchers such as torchrun export
+   OMP_NUM_THREADS=1; the CPU baseline sets the host's core count explicitly). */
+void orc_set_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+
 int orc_max_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

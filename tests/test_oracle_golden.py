@@ -182,3 +182,15 @@ def test_multi_output_restatement_matches_single_output_slices():
         single = oracle.FlatModel(base.borders, base.border_counts, base.depths, base.split_feature,
                                   base.split_ordinal, leaves[:, c: c + 1, :].copy(), 1.5, -0.25)
         assert np.array_equal(got[:, c], oracle.evaluate_scalar(single, x))
+
+
+def test_oracle_thread_count_overrides_environment():
+    """The CPU baseline must use every host core even under torchrun (OMP_NUM_THREADS=1)."""
+    before = oracle.max_threads()
+    try:
+        oracle.set_threads(2)
+        assert oracle.max_threads() == 2
+        oracle.set_threads(oracle.host_cores())
+        assert oracle.max_threads() == oracle.host_cores()
+    finally:
+        oracle.set_threads(before)
