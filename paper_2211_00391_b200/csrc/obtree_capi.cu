@@ -237,7 +237,9 @@ size_t table_stride(const obt_model* m) {
 // model is padded with null trees to a multiple of the chunk.
 void plan_chunks(obt_model* m) {
   const int DI = m->depth_inst;
-  const size_t per_tree_desc = (size_t)obt::desc_words_per_tree(DI, m->compare_mode) * 4;
+  // descriptor region sized for the larger of the K2 ({off, k}) and K2s (16-byte) formats
+  const size_t per_tree_desc = std::max<size_t>((size_t)obt::desc_words_per_tree(DI, m->compare_mode) * 4,
+                                                (size_t)DI * obt::kSplitDescBytes);
   const size_t per_tree = per_tree_desc + table_stride(m);
   const int group = obt::tree_group(DI);
   // ring budget: what the bucket tile of the largest 256-quantum tile leaves over
@@ -279,9 +281,56 @@ void tree_descriptors(const obt_model* m, int t, int tile, uint32_t* out) {
   }
 }
 
-// Per-tile-size state: device records (descriptors + leaves) for the shared-memory
-// descriptor path, and the flat descriptor stream for the parameter-bank path.
-int build_tile_plan(obt_model* m, int tile, TilePlan& out) {
+// Null tree: every leaf is -0.0, the exact identity of IEEE addition.
+void write_null_leaves(const obt_model* m, uint8_t* dst) {
+  for (size_t j = 0; j < ((size_t)1 << m->depth_inst); ++j) {
+    if (m->leaf_storage == 0) { const double z = -0.0; std::memcpy(dst + j * 8, &z, 8); }
+    else if (m->leaf_storage == 1) { const float z = -0.0f; std::memcpy(dst + j * 4, &z, 4); }
+    else { const uint16_t z = 0x8000u; std::memcpy(dst + j * 2, &z, 2); }
+  }
+}
+
+// K2s level order for tree t: perm[j] = the original level evaluated as depth j.  Lane
+// part 0 evaluates depths [0, DI/2), part 1 [DI/2, DI); at step i they read the rows of
+// depths i and DI/2 + i, which are conflict-free when the rows differ in parity (the
+// swizzled bucket layout).  Levels are paired even-odd first; sentinel levels read no
+// meaningful bucket, so they take whichever row parity their partner needs
+// (wild_color[j] = the row parity for a sentinel at depth j).
+void split_level_order(const obt_model* m, int t, int* perm, int* wild_color) {
+  const int DI = m->depth_inst, half = DI / 2;
+  for (int j = 0; j < DI; ++j) { perm[j] = j; wild_color[j] = 0; }
+  if (DI < 2 || DI % 2 || t >= m->n_trees) return;
+  std::vector<int> even, odd, wild;
+  for (int d = 0; d < DI; ++d) {
+    const size_t i = (size_t)t * DI + d;
+    if (m->split_ordinal[i] == kSentinel) wild.push_back(d);
+    else if (m->split_feature[i] & 1) odd.push_back(d);
+    else even.push_back(d);
+  }
+  const int c_wild_odd = m->n_features > 1 ? 1 : 0;  // row 1 exists only with >= 2 features
+  std::vector<std::pair<int, int>> p0, p1;  // (level, sentinel row parity) per part
+  auto take = [](std::vector<int>& v) { const int x = v.back(); v.pop_back(); return x; };
+  while (!even.empty() && !odd.empty()) { p0.push_back({take(even), 0}); p1.push_back({take(odd), 0}); }
+  while (!even.empty() && !wild.empty()) { p0.push_back({take(even), 0}); p1.push_back({take(wild), c_wild_odd}); }
+  while (!odd.empty() && !wild.empty()) { p0.push_back({take(odd), 0}); p1.push_back({take(wild), 0}); }
+  while (wild.size() >= 2) { p0.push_back({take(wild), 0}); p1.push_back({take(wild), c_wild_odd}); }
+  std::vector<int> rest;  // same-parity leftovers: pair among themselves (conflicting)
+  for (int d : even) rest.push_back(d);
+  for (int d : odd) rest.push_back(d);
+  for (int d : wild) rest.push_back(d);
+  for (size_t i = 0; i + 1 < rest.size(); i += 2) { p0.push_back({rest[i], 0}); p1.push_back({rest[i + 1], 0}); }
+  for (int j = 0; j < half; ++j) {
+    perm[j] = p0[j].first;
+    wild_color[j] = p0[j].second;
+    perm[half + j] = p1[j].first;
+    wild_color[half + j] = p1[j].second;
+  }
+}
+
+// Per-(tile size, variant) state: device records (descriptors + leaves) for the
+// shared-memory descriptor path (variant 0: K2, variant 1: K2s with swizzled rows and
+// paired level order), and the flat descriptor stream for the parameter-bank path.
+int build_tile_plan(obt_model* m, int tile, int variant, TilePlan& out) {
   const int DI = m->depth_inst;
   const int dwt = obt::desc_words_per_tree(DI, m->compare_mode);  // words in the smem records
   const size_t per_tree_leaf = leaf_size(m->leaf_storage) << DI;  // bytes of real leaves
@@ -291,11 +340,48 @@ int build_tile_plan(obt_model* m, int tile, TilePlan& out) {
   std::vector<uint8_t> host((size_t)std::max(m->n_chunks, 1) * chunk_bytes, 0);
   out.param_desc.assign((size_t)m->padded_trees * DI * 2, 0u);
   std::vector<uint32_t> words((size_t)DI * 2);
+  std::vector<int> perm(DI), wild(DI);
+  std::vector<uint8_t> permuted(per_tree_leaf);
   for (int t = 0; t < m->padded_trees; ++t) {
     const int c = t / ct, tl = t % ct;
     uint8_t* rec = host.data() + (size_t)c * chunk_bytes;
     tree_descriptors(m, t, tile, words.data());
     if (m->compare_mode == 7) std::memcpy(out.param_desc.data() + (size_t)t * DI * 2, words.data(), (size_t)DI * 8);
+    if (variant == 1) {
+      // K2s: 16 bytes per split in paired level order, row offsets +- 64 for odd rows
+      split_level_order(m, t, perm.data(), wild.data());
+      uint32_t* dst = reinterpret_cast<uint32_t*>(rec + (size_t)tl * DI * obt::kSplitDescBytes);
+      for (int j = 0; j < DI; ++j) {
+        const int d = perm[j];
+        const bool sentinel = t >= m->n_trees || m->split_ordinal[(size_t)t * DI + d] == kSentinel;
+        const int row = sentinel ? wild[j] : m->split_feature[(size_t)t * DI + d];
+        const uint32_t off = (uint32_t)row * (uint32_t)tile, sw = (row & 1) ? 64u : 0u;
+        const uint32_t kpart = m->compare_mode == 7 ? 0u : (words[2 * d] & 0xFFu);  // 8-bit: k in byte 0
+        const uint32_t w1 = sentinel ? 0u : words[2 * d + 1];
+        const uint32_t k7 = sentinel ? 0u : kpart;
+        if (m->compare_mode == 7) {
+          dst[4 * j + 0] = off + sw; dst[4 * j + 1] = w1; dst[4 * j + 2] = off - sw; dst[4 * j + 3] = w1;
+        } else {
+          dst[4 * j + 0] = ((off + sw) << 8) | k7; dst[4 * j + 1] = w1;
+          dst[4 * j + 2] = ((off - sw) << 8) | k7; dst[4 * j + 3] = w1;
+        }
+      }
+      uint8_t* leaf_dst = rec + desc_bytes + (size_t)tl * stride;
+      if (t < m->n_trees) {
+        // leaf i' of the permuted tree is leaf i of the original, i = sum_j bit_j(i') << perm[j]
+        const size_t ls = leaf_size(m->leaf_storage);
+        const uint8_t* src = m->leaf_bytes.data() + (size_t)t * per_tree_leaf;
+        for (size_t ip = 0; ip < ((size_t)1 << DI); ++ip) {
+          size_t i = 0;
+          for (int j = 0; j < DI; ++j) i |= ((ip >> j) & 1u) << perm[j];
+          std::memcpy(permuted.data() + ip * ls, src + i * ls, ls);
+        }
+        std::memcpy(leaf_dst, permuted.data(), per_tree_leaf);
+      } else {
+        write_null_leaves(m, leaf_dst);
+      }
+      continue;
+    }
     if (dwt == DI) {  // packed 7-bit records: (off << 8) | k
       for (int d = 0; d < DI; ++d) words[d] = (words[2 * d] << 8) | (words[2 * d + 1] & 0xFFu);
     }
@@ -305,12 +391,7 @@ int build_tile_plan(obt_model* m, int tile, TilePlan& out) {
     if (t < m->n_trees) {
       std::memcpy(leaf_dst, m->leaf_bytes.data() + (size_t)t * per_tree_leaf, per_tree_leaf);
     } else {
-      // null tree: every leaf is -0.0, the exact identity of IEEE addition
-      for (size_t j = 0; j < ((size_t)1 << DI); ++j) {
-        if (m->leaf_storage == 0) { const double z = -0.0; std::memcpy(leaf_dst + j * 8, &z, 8); }
-        else if (m->leaf_storage == 1) { const float z = -0.0f; std::memcpy(leaf_dst + j * 4, &z, 4); }
-        else { const uint16_t z = 0x8000u; std::memcpy(leaf_dst + j * 2, &z, 2); }
-      }
+      write_null_leaves(m, leaf_dst);
     }
   }
   CUDA_TRY(cudaMalloc(&out.d_chunks, host.size()));
@@ -318,14 +399,15 @@ int build_tile_plan(obt_model* m, int tile, TilePlan& out) {
   return OBT_OK;
 }
 
-int get_tile_plan(obt_model* m, int tile, const TilePlan** out) {
+int get_tile_plan(obt_model* m, int tile, int variant, const TilePlan** out) {
   std::lock_guard<std::mutex> lock(m->mu);
-  auto it = m->plans.find(tile);
+  const int key = tile * 2 + variant;
+  auto it = m->plans.find(key);
   if (it == m->plans.end()) {
     TilePlan tp;
-    const int rc = build_tile_plan(m, tile, tp);
+    const int rc = build_tile_plan(m, tile, variant, tp);
     if (rc != OBT_OK) return rc;
-    it = m->plans.emplace(tile, std::move(tp)).first;
+    it = m->plans.emplace(key, std::move(tp)).first;
   }
   *out = &it->second;
   return OBT_OK;
@@ -393,8 +475,15 @@ int choose_tpw(const obt_model* m, int tile, bool write_idx, int dsrc) {
   return (m->depth_inst % 2 == 0 && words * 2 <= cap) ? 2 : 1;
 }
 
+// Lanes per bucket word for one predict, decided once (the quantize launch lays the
+// buckets out for it).
+int apply_lanes(const obt_model* m, int tile, bool write_idx) {
+  if (m->n_outputs > 1) return 1;
+  return choose_tpw(m, tile, write_idx, use_param_descriptors(m));
+}
+
 int launch_quantize(const obt_model* m, const float* x, int64_t n, int layout, uint8_t* out, bool tiled,
-                    int tile, int64_t n_slots, cudaStream_t stream) {
+                    int tile, int64_t n_slots, bool swizzle, cudaStream_t stream) {
   const BorderTable& bt = tiled ? m->used : m->full;
   QuantFn fn = pick_quant(bt.levels, layout, tiled);
   if (!fn) return fail(OBT_E_UNSUPPORTED, "no quantize kernel for %d levels", bt.levels);
@@ -415,6 +504,7 @@ int launch_quantize(const obt_model* m, const float* x, int64_t n, int layout, u
   const size_t smem = bt.levels > 0 ? (size_t)std::min(fc, m->n_features) * bt.pitch * 4 : 16;
   p.chunk_features = fc;
   p.two = 2;
+  p.swizzle = swizzle ? 1 : 0;
   CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid((unsigned)((n_slots + obt::kQuantBlock - 1) / obt::kQuantBlock), (unsigned)((m->n_features + fc - 1) / fc));
   fn<<<grid, obt::kQuantThreads, smem, stream>>>(p);
@@ -426,14 +516,15 @@ int launch_quantize(const obt_model* m, const float* x, int64_t n, int layout, u
 // One or more launches of the apply kernel folding all trees in order; with the
 // parameter-bank path each launch carries its trees' descriptors, and launches after
 // the first continue the fold from the accumulators the previous one left in `out`.
-int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, double* out, uint16_t* idx_out,
+// `tpw` (lanes per bucket word, from apply_lanes) must match the layout the quantize
+// launch wrote: tpw > 1 reads the swizzled K2s layout.
+int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, int tpw, double* out, uint16_t* idx_out,
                  int tree_begin, int tree_end, cudaStream_t stream) {
   const bool write_idx = idx_out != nullptr;
-  const TilePlan* tp = nullptr;
-  int rc = get_tile_plan(m, tile, &tp);
-  if (rc != OBT_OK) return rc;
   const int dsrc = use_param_descriptors(m);
-  const int tpw = choose_tpw(m, tile, write_idx, dsrc);
+  const TilePlan* tp = nullptr;
+  int rc = get_tile_plan(m, tile, tpw > 1 ? 1 : 0, &tp);
+  if (rc != OBT_OK) return rc;
   ApplyKernel k = tpw > 1 ? pick_split(m->depth_inst, m->compare_mode, m->leaf_storage, tpw)
                           : pick_apply(m->depth_inst, m->compare_mode, m->leaf_storage, write_idx, dsrc);
   if (!k.fn) return fail(OBT_E_UNSUPPORTED, "no apply kernel for depth %d", m->depth_inst);
@@ -736,14 +827,15 @@ static int predict_impl(obt_model* m, const float* x, int64_t n, int32_t layout,
   }
   const int64_t n_slots = ((n + tile - 1) / tile) * (int64_t)tile;
   if (ev_begin) CUDA_TRY(cudaEventRecord(ev_begin, stream));
-  int rc = launch_quantize(m, x, n, layout, q, true, tile, n_slots, stream);
+  const int tpw = apply_lanes(m, tile, idx_out != nullptr);
+  int rc = launch_quantize(m, x, n, layout, q, true, tile, n_slots, tpw > 1, stream);
   if (rc == OBT_OK && ev_mid) CUDA_TRY(cudaEventRecord(ev_mid, stream));
   if (rc == OBT_OK) {
     if (m->n_outputs > 1) {
       rc = idx_out ? fail(OBT_E_UNSUPPORTED, "leaf-index dumps are implemented for single-output models")
                    : launch_multi(m, q, n, out, stream);
     } else {
-      rc = launch_apply(m, q, n, tile, out, idx_out, tree_begin, tree_end, stream);
+      rc = launch_apply(m, q, n, tile, tpw, out, idx_out, tree_begin, tree_end, stream);
     }
   }
   if (rc == OBT_OK && ev_end) CUDA_TRY(cudaEventRecord(ev_end, stream));
@@ -832,7 +924,7 @@ int obt_quantize_dev(const obt_model* m, const float* x, int64_t n, int32_t layo
   if (n == 0) return OBT_OK;
   if (!x || !buckets) return fail(OBT_E_INVALID, "null feature or bucket pointer");
   DeviceGuard guard(m->device);
-  return launch_quantize(m, x, n, layout, buckets, false, 0, n, static_cast<cudaStream_t>(stream));
+  return launch_quantize(m, x, n, layout, buckets, false, 0, n, false, static_cast<cudaStream_t>(stream));
 }
 
 int obt_predict_host(const obt_model* mc, const float* x_host, int64_t n, int32_t layout, double* out_host,

@@ -105,6 +105,7 @@ struct QuantizeParams {
   int32_t tile;          // TILE (tiled output only)
   int32_t chunk_features;  // features per CTA (grid.y chunks), a multiple of 8
   int32_t two;             // the constant 2, passed at run time (see eytz_level)
+  int32_t swizzle;         // tiled: odd feature rows XOR object byte offsets with 64 (K2s layout)
 };
 
 constexpr int kQuantObjects = 128;    // tile quantum: a quantize warp's 128 objects never straddle tiles
@@ -253,7 +254,7 @@ __global__ void __launch_bounds__(kQuantThreads, 2) quantize_kernel(QuantizePara
       }
       const int f = f0 + fq + j;
       if (TILED) {
-        const int64_t t = ob / p.tile, w = ob - t * p.tile;
+        const int64_t t = ob / p.tile, w = (ob - t * p.tile) ^ ((p.swizzle && (f & 1)) ? 64 : 0);
         *reinterpret_cast<uint32_t*>(p.out + (t * F + f) * (int64_t)p.tile + w) = word;
       } else {
 #pragma unroll
@@ -581,8 +582,20 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid
 // folds objects [p*4/TPW, (p+1)*4/TPW) of the word.  Every accumulator still sees
 // the trees in order (the fold stays bit-exact) while the CTA runs TPW times more
 // warps over the same bucket tile -- the lever against the latency bound when the
-// tile (F bytes per object) limits the objects an SM can hold.  Descriptors come from
-// the shared-memory ring ({off, k} / {(off << 8) | k, s}, 8 bytes each).
+// tile (F bytes per object) limits the objects an SM can hold.
+//
+// Bank conflicts: the TPW lanes of a word read different feature rows at the same word
+// offset, and rows start on 128-byte boundaries, so without care they hit the same bank.
+// The K2s bucket layout therefore XORs the object byte offset of odd feature rows with
+// 64 (the quantize kernel writes it so): a warp's 16 words (TPW 2) then sit in one bank
+// half for even rows and in the other for odd rows, and the host orders each tree's
+// levels so the two lanes of a pair read rows of opposite parity wherever the tree
+// allows (the leaf table is permuted to match; the selected leaf is unchanged).
+// Descriptors come from the shared-memory ring as 16 bytes per split,
+// {off+, k, off-, k} (7-bit) or {(off+ << 8) | k, s, (off- << 8) | k, s} (8-bit):
+// off+- = row offset +- 64 for odd rows, and a lane takes the half that matches bit 6
+// of its own word offset (warp-uniform), so the swizzle costs no instruction.
+constexpr int kSplitDescBytes = 16;
 template <int DI, int CMP, int LEAF, int TPW>
 __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_split_kernel(const __grid_constant__ ApplyArgs<0> args) {
   static_assert(DI <= 8 && DI % TPW == 0, "depth-split needs TPW | DI and one index byte");
@@ -653,8 +666,8 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_split_kernel(const 
   for (int k = 0; k < kOPT; ++k) acc[k] = (p.first || obj0 + k >= p.n) ? (acc_t)0 : (acc_t)p.out[obj0 + k];
   mbar_wait_warp(tile_bar, 0);
 
-  constexpr int kDW = desc_words(CMP);
-  const uint32_t my_desc = (uint32_t)(part * kDPT) * 4u * kDW;  // this lane's first descriptor in a tree
+  // this lane's first descriptor in a tree: its part's first split, the half for its bit 6
+  const uint32_t my_desc = (uint32_t)(part * kDPT) * kSplitDescBytes + (((4u * word) >> 6) & 1u) * 8u;
   for (int c = 0; c < n_chunks; ++c) {
     const int s = c % p.n_stages;
     mbar_wait_warp(&full[s], (uint32_t)(c / p.n_stages) & 1u);
@@ -665,20 +678,14 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_split_kernel(const 
 #pragma unroll
       for (int tt = 0; tt < kTreeGroup; ++tt) {
         const int t = g * kTreeGroup + tt;
-        const uint32_t tree_desc = desc_base + (uint32_t)t * (uint32_t)(DI * 4 * kDW);
+        const uint32_t tree_desc = desc_base + (uint32_t)t * (uint32_t)(DI * kSplitDescBytes);
         uint32_t part_a = 0, part_b = 0;
 #pragma unroll
         for (int i = 0; i < kDPT; ++i) {
-          uint32_t d0, d1 = 0;
-          if constexpr (kDW == 2) {
-            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(d0), "=r"(d1) : "r"(tree_desc + 8u * i));
-          } else {
-            d0 = lds_u32(tree_desc + 4u * i);
-          }
+          uint32_t d0, d1;
+          asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(d0), "=r"(d1) : "r"(tree_desc + (uint32_t)kSplitDescBytes * i));
           uint32_t b7;
-          if constexpr (CMP == 7 && kDW == 1) {
-            b7 = lds_u32(my_q + (d0 >> 8)) + __byte_perm(d0, 0u, 0x0000u);
-          } else if constexpr (CMP == 7) {
+          if constexpr (CMP == 7) {
             b7 = lds_u32(my_q + d0) + d1;
           } else {
             const uint32_t w = lds_u32(my_q + (d0 >> 8));
