@@ -662,15 +662,6 @@ int obt_model_create(const obt_model_desc* d, int device, obt_model** out) {
                                                       : instantiated_depth(d->max_depth))
                                   : (d->n_outputs > 1 ? 4 : 1);
   CUDA_TRY(cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount, device));
-  {
-    // keep stream-ordered workspace allocations cached between calls instead of
-    // returning them to the driver at every synchronisation
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-      uint64_t keep = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-  }
   CUDA_TRY(cudaDeviceGetAttribute(&m->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
 
   // Two border tables.  `full` holds every border (obt_quantize_dev returns the
@@ -812,6 +803,37 @@ int obt_workspace_size(const obt_model* m, int64_t n, size_t* bytes) {
   return OBT_OK;
 }
 
+// The library's own stream-ordered pool per device: workspace and staging buffers stay
+// cached between calls (no driver round trip at every synchronisation) without touching
+// the device's default pool, which belongs to the application.
+static cudaMemPool_t workspace_pool(int device) {
+  static std::mutex mu;
+  static std::map<int, cudaMemPool_t> pools;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = pools.find(device);
+  if (it != pools.end()) return it->second;
+  cudaMemPoolProps props{};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.handleTypes = cudaMemHandleTypeNone;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = device;
+  cudaMemPool_t pool = nullptr;
+  if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+    cudaGetLastError();
+    pool = nullptr;  // fall back to the default pool
+  } else {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  pools[device] = pool;
+  return pool;
+}
+
+static cudaError_t pool_alloc(void** ptr, size_t bytes, int device, cudaStream_t stream) {
+  cudaMemPool_t pool = workspace_pool(device);
+  return pool ? cudaMallocFromPoolAsync(ptr, bytes, pool, stream) : cudaMallocAsync(ptr, bytes, stream);
+}
+
 static int predict_impl(obt_model* m, const float* x, int64_t n, int32_t layout, double* out, uint16_t* idx_out,
                         int tree_begin, int tree_end, void* ws, size_t ws_bytes, cudaStream_t stream,
                         cudaEvent_t ev_begin = nullptr, cudaEvent_t ev_mid = nullptr, cudaEvent_t ev_end = nullptr) {
@@ -822,7 +844,7 @@ static int predict_impl(obt_model* m, const float* x, int64_t n, int32_t layout,
   bool owned = false;
   if (!q || ws_bytes < need) {
     if (ws && ws_bytes < need) return fail(OBT_E_INVALID, "workspace of %zu bytes, need %zu", ws_bytes, need);
-    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&q), need, stream));
+    CUDA_TRY(pool_alloc(reinterpret_cast<void**>(&q), need, m->device, stream));
     owned = true;
   }
   const int64_t n_slots = ((n + tile - 1) / tile) * (int64_t)tile;
@@ -959,8 +981,8 @@ int obt_predict_host(const obt_model* mc, const float* x_host, int64_t n, int32_
   };
   cuda_ok(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking), "copy stream");
   for (int b = 0; b < nbuf && rc == OBT_OK; ++b) {
-    cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&x_dev[b]), (size_t)rows * F * 4, stream), "feature buffer");
-    cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&out_dev[b]), (size_t)rows * C * 8, stream), "score buffer");
+    cuda_ok(pool_alloc(reinterpret_cast<void**>(&x_dev[b]), (size_t)rows * F * 4, m->device, stream), "feature buffer");
+    cuda_ok(pool_alloc(reinterpret_cast<void**>(&out_dev[b]), (size_t)rows * C * 8, m->device, stream), "score buffer");
     cuda_ok(cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming), "event");
     cuda_ok(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming), "event");
   }
@@ -990,6 +1012,9 @@ int obt_predict_host(const obt_model* mc, const float* x_host, int64_t n, int32_
     cuda_ok(cudaEventRecord(done[b], stream), "event record");
   }
   g_launches = launches;
+  // the stream-ordered frees below must also follow every copy issued on `copy` (an
+  // error may have left a copy that `stream` never waited for)
+  if (ready && copy && cudaEventRecord(ready, copy) == cudaSuccess) cudaStreamWaitEvent(stream, ready, 0);
   for (int b = 0; b < nbuf; ++b) {
     if (x_dev[b]) cudaFreeAsync(x_dev[b], stream);
     if (out_dev[b]) cudaFreeAsync(out_dev[b], stream);

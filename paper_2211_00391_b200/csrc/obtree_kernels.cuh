@@ -292,7 +292,10 @@ __global__ void __launch_bounds__(kQuantThreads, 2) quantize_kernel(QuantizePara
 // 16 trees per group keep ~100 independent shared loads in flight per thread; deeper
 // trees (larger leaf tables) use groups of 8 / 4 so a chunk still fits the ring without
 // shrinking the bucket tile.
-__host__ __device__ constexpr int tree_group(int di) { return di <= 6 ? 16 : di <= 8 ? 8 : 4; }
+#ifndef OBT_GROUP_SHALLOW
+#define OBT_GROUP_SHALLOW 16
+#endif
+__host__ __device__ constexpr int tree_group(int di) { return di <= 6 ? OBT_GROUP_SHALLOW : di <= 8 ? 8 : 4; }
 #ifndef OBT_PACKED_DESC
 #define OBT_PACKED_DESC 0
 #endif
@@ -392,7 +395,10 @@ __host__ __device__ constexpr int leaf_table_stride(int di, int leaf_bytes) {
 
 constexpr int kApplyProducerThreads = 32;
 // Block size cap: 128 registers per thread keep several tree groups of loads in flight.
-constexpr int kApplyMaxThreads = 544;  // 16 consumer warps + the producer
+#ifndef OBT_APPLY_MAXT
+#define OBT_APPLY_MAXT 544
+#endif
+constexpr int kApplyMaxThreads = OBT_APPLY_MAXT;  // 16 consumer warps + the producer
 
 template <int DI, int CMP, int LEAF, bool WRITE_IDX, int W, int DSRC>
 __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid_constant__ ApplyArgs<DSRC> args) {

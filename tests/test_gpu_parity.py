@@ -358,3 +358,21 @@ def test_depth_split_lanes_bit_exact(monkeypatch, tpw, D, F, B, T):
         got = obt.Evaluator(model, obt.EvalConfig(strategy=strategy)).predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
         want = oracle.evaluate_scalar(fm, x, oracle.OBJECT_MAJOR, prec)
         assert np.array_equal(got, want), (strategy, int(np.count_nonzero(got != want)))
+
+
+def test_default_mempool_left_alone():
+    """Workspace and staging buffers come from the library's own pool: the device's
+    default pool (the application's) keeps its release threshold."""
+    rt = pytest.importorskip("cuda.bindings.runtime")
+    err, pool = rt.cudaDeviceGetDefaultMemPool(0)
+    assert err == rt.cudaError_t.cudaSuccess
+    attr = rt.cudaMemPoolAttr.cudaMemPoolAttrReleaseThreshold
+    err, before = rt.cudaMemPoolGetAttribute(pool, attr)
+    model = _model(11, 20, 30, 6, seed=5)
+    x = _features(model, 5000, seed=6)
+    ev = obt.Evaluator(model)
+    ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
+    ev.predict_device(torch.from_numpy(x).cuda())
+    torch.cuda.synchronize()
+    err, after = rt.cudaMemPoolGetAttribute(pool, attr)
+    assert int(after) == int(before)
