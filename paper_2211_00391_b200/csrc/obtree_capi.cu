@@ -505,7 +505,9 @@ int launch_quantize(const obt_model* m, const float* x, int64_t n, int layout, u
   p.chunk_features = fc;
   p.two = 2;
   p.swizzle = swizzle ? 1 : 0;
-  CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // the opt-in maximum, not this launch's size: the attribute is per function and
+  // process-wide, so every caller must set the same value (concurrent launches race otherwise)
+  CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, m->smem_optin));
   dim3 grid((unsigned)((n_slots + obt::kQuantBlock - 1) / obt::kQuantBlock), (unsigned)((m->n_features + fc - 1) / fc));
   fn<<<grid, obt::kQuantThreads, smem, stream>>>(p);
   ++g_launches;
@@ -532,7 +534,7 @@ int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, int tpw, d
   const size_t smem = 512 + (size_t)kStages * m->chunk_bytes + (size_t)m->n_features * tile;
   if (smem > (size_t)m->smem_optin)
     return fail(OBT_E_UNSUPPORTED, "tile of %d objects needs %zu bytes of shared memory", tile, smem);
-  CUDA_TRY(cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CUDA_TRY(cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, m->smem_optin));
 
   obt::ApplyParams p{};
   p.q = q;

@@ -376,3 +376,40 @@ def test_default_mempool_left_alone():
     torch.cuda.synchronize()
     err, after = rt.cudaMemPoolGetAttribute(pool, attr)
     assert int(after) == int(before)
+
+
+def test_concurrent_predicts_from_threads():
+    """Reentrancy: host threads predicting concurrently on their own streams,
+    with batch sizes that give different tiles and shared-memory sizes, all bit-exact."""
+    import threading
+
+    cases = []
+    for i, (F, n) in enumerate([(13, 700), (40, 90000), (13, 33000), (77, 5000)]):
+        model = _model(F, 50, 120, 6 if i % 2 else 5, seed=40 + i)
+        x = _features(model, n, seed=50 + i)
+        cases.append((model, x, oracle.evaluate_scalar(oracle.flatten(model), x)))
+    errors = []
+
+    def worker(model, x, want):
+        try:
+            ev = obt.Evaluator(model)
+            xd = torch.from_numpy(x).cuda()
+            torch.cuda.current_stream().synchronize()  # the copy ran on this thread's default stream
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for _ in range(6):
+                    got = ev.predict_device(xd)
+                    s.synchronize()
+                    if not np.array_equal(got.cpu().numpy(), want):
+                        errors.append("device path mismatch")
+                    if not np.array_equal(ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR)), want):
+                        errors.append("host path mismatch")
+        except Exception as e:  # noqa: BLE001 - reported below
+            errors.append(repr(e))
+
+    threads = [threading.Thread(target=worker, args=c) for c in cases]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors[:3]
