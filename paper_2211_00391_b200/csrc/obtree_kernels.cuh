@@ -93,6 +93,16 @@ __device__ __forceinline__ void bulk_g2s_split(void* dst, const void* src, uint3
 }
 
 // ---------------------------------------------------------------------------
+// Tile layout of the bucket matrix Q[tile][F][TILE]: within each 128-object block of a
+// tile, bucket word p (bytes 4p..4p+3 of every feature row) holds objects p, p+32, p+64,
+// p+96 (byte k -> object p + 32k).  A quantize lane then owns objects one apart from its
+// neighbours' (coalesced feature-major loads, conflict-free staged rows) and apply
+// threads write consecutive outputs.  wi = word index within the tile.
+__device__ __forceinline__ int64_t word_object(int64_t tile_base, int wi, int k) {
+  return tile_base + (int64_t)((wi >> 5) * 128 + (wi & 31) + 32 * k);
+}
+
+// ---------------------------------------------------------------------------
 // K1: quantize.
 struct QuantizeParams {
   const float* x;        // features, layout per template
@@ -148,14 +158,16 @@ __global__ void __launch_bounds__(kQuantThreads, 2) quantize_kernel(QuantizePara
   }
   __syncthreads();
 
-  const int64_t ob = (int64_t)blockIdx.x * kQuantBlock + warp * 128 + 4 * lane;  // first of my 4 objects
-  if (ob >= p.n_slots) return;  // past the last tile (no barrier follows)
-  const bool full_objs = ob + 3 < p.n;
-  const bool vec_rows = LAYOUT == 0 ? ((F & 3) == 0 && (f0 & 3) == 0) : ((p.n & 3) == 0);
+  // this lane's objects: base + lane + 32k (the tile layout's word `lane` of this block)
+  const int64_t base = (int64_t)blockIdx.x * kQuantBlock + warp * 128;
+  if (base >= p.n_slots) return;  // past the last tile (no barrier follows)
+  const int64_t ob = base + lane;
+  const bool full_objs = ob + 96 < p.n;
+  const bool vec_rows = LAYOUT == 0 ? ((F & 3) == 0 && (f0 & 3) == 0) : true;
   static_assert(kQuantStep == 8, "a 256-bit row load covers exactly one step");
   const bool sector_rows = LAYOUT == 0 && (F & 7) == 0 && (reinterpret_cast<uintptr_t>(p.x) & 31) == 0;
   const uint32_t two = (uint32_t)p.two;
-  // raw values v[j][k] of one step: object ob + k, feature f0 + fq + j
+  // raw values v[j][k] of one step: object ob + 32k, feature f0 + fq + j
   auto load_step = [&](float (&v)[S][4], int fq) {
     if (full_objs && vec_rows && fq + S <= nf) {
       if (LAYOUT == 0 && sector_rows) {
@@ -164,7 +176,7 @@ __global__ void __launch_bounds__(kQuantThreads, 2) quantize_kernel(QuantizePara
         // often missed L1 again)
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const float* row = p.x + (ob + k) * F + f0 + fq;
+          const float* row = p.x + (ob + 32 * k) * F + f0 + fq;
           asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
                        : "=f"(v[0][k]), "=f"(v[1][k]), "=f"(v[2][k]), "=f"(v[3][k]),
                          "=f"(v[4][k]), "=f"(v[5][k]), "=f"(v[6][k]), "=f"(v[7][k])
@@ -173,7 +185,7 @@ __global__ void __launch_bounds__(kQuantThreads, 2) quantize_kernel(QuantizePara
       } else if (LAYOUT == 0) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const float4* row = reinterpret_cast<const float4*>(p.x + (ob + k) * F + f0 + fq);
+          const float4* row = reinterpret_cast<const float4*>(p.x + (ob + 32 * k) * F + f0 + fq);
 #pragma unroll
           for (int h = 0; h < S / 4; ++h) {
             const float4 q = __ldg(row + h);
@@ -181,19 +193,19 @@ __global__ void __launch_bounds__(kQuantThreads, 2) quantize_kernel(QuantizePara
           }
         }
       } else {
+        // feature-major: each load is one row segment shared by the warp's 32 lanes
 #pragma unroll
-        for (int j = 0; j < S; ++j) {
-          const float4 q = __ldg(reinterpret_cast<const float4*>(p.x + (int64_t)(f0 + fq + j) * p.n + ob));
-          v[j][0] = q.x; v[j][1] = q.y; v[j][2] = q.z; v[j][3] = q.w;
-        }
+        for (int j = 0; j < S; ++j)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) v[j][k] = __ldg(p.x + (int64_t)(f0 + fq + j) * p.n + ob + 32 * k);
       }
     } else {
 #pragma unroll
       for (int j = 0; j < S; ++j)
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const bool in = ob + k < p.n && fq + j < nf;
-          const int64_t idx = LAYOUT == 0 ? (ob + k) * F + f0 + fq + j : (int64_t)(f0 + fq + j) * p.n + ob + k;
+          const bool in = ob + 32 * k < p.n && fq + j < nf;
+          const int64_t idx = LAYOUT == 0 ? (ob + 32 * k) * F + f0 + fq + j : (int64_t)(f0 + fq + j) * p.n + ob + 32 * k;
           v[j][k] = in ? __ldg(p.x + idx) : 0.0f;
         }
     }
@@ -250,16 +262,16 @@ __global__ void __launch_bounds__(kQuantThreads, 2) quantize_kernel(QuantizePara
       if (!full_objs) {
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          if (ob + k >= p.n) word &= ~(0xFFu << (8 * k));
+          if (ob + 32 * k >= p.n) word &= ~(0xFFu << (8 * k));
       }
       const int f = f0 + fq + j;
       if (TILED) {
-        const int64_t t = ob / p.tile, w = (ob - t * p.tile) ^ ((p.swizzle && (f & 1)) ? 64 : 0);
+        const int64_t t = base / p.tile, w = (base - t * p.tile + 4 * lane) ^ ((p.swizzle && (f & 1)) ? 64 : 0);
         *reinterpret_cast<uint32_t*>(p.out + (t * F + f) * (int64_t)p.tile + w) = word;
       } else {
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          if (ob + k < p.n) p.out[(int64_t)f * p.n + ob + k] = (uint8_t)(word >> (8 * k));
+          if (ob + 32 * k < p.n) p.out[(int64_t)f * p.n + ob + 32 * k] = (uint8_t)(word >> (8 * k));
       }
     }
   };
@@ -458,12 +470,15 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid
   const int ctid = tid - kApplyProducerThreads;
   constexpr int kObj = 4 * W;                            // objects per thread
   const uint32_t my_q = smem_u32(qtile) + kObj * ctid;   // this thread's words in every row
-  const int64_t obj0 = tile_idx * p.tile + kObj * ctid;
+  const int64_t tile_base = tile_idx * p.tile;
+  // accumulator 4x + k: byte k of this thread's word x
+  auto obj_of = [&](int x, int k) { return word_object(tile_base, W * ctid + x, k); };
   acc_t acc[kObj];
 #pragma unroll
   for (int k = 0; k < kObj; ++k) {
     // continue the fold of the previous launch (exact: the carry holds acc_t values)
-    acc[k] = (p.first || WRITE_IDX || obj0 + k >= p.n) ? (acc_t)0 : (acc_t)p.out[obj0 + k];
+    const int64_t o = obj_of(k / 4, k % 4);
+    acc[k] = (p.first || WRITE_IDX || o >= p.n) ? (acc_t)0 : (acc_t)p.out[o];
   }
   mbar_wait_warp(tile_bar, 0);
 
@@ -544,7 +559,8 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
                 const uint32_t idx = ((lo >> (8 * k)) & 0xffu) | (DI > 8 ? ((hi[x] >> (8 * k)) & 0xffu) << 8 : 0u);
-                if (obj0 + 4 * x + k < p.n) row[obj0 + 4 * x + k] = (uint16_t)idx;
+                const int64_t o = obj_of(x, k);
+                if (o < p.n) row[o] = (uint16_t)idx;
               }
             }
           } else if constexpr (kPrescaled) {
@@ -573,9 +589,10 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid
   if constexpr (!WRITE_IDX) {
 #pragma unroll
     for (int k = 0; k < kObj; ++k) {
-      if (obj0 + k < p.n) {
+      const int64_t o = obj_of(k / 4, k % 4);
+      if (o < p.n) {
         // finalize: f64(acc) * scale + bias, two roundings (evaluate.py:298-299, oracle.py:53-54)
-        p.out[obj0 + k] = p.last ? __dadd_rn(__dmul_rn((double)acc[k], p.scale), p.bias) : (double)acc[k];
+        p.out[o] = p.last ? __dadd_rn(__dmul_rn((double)acc[k], p.scale), p.bias) : (double)acc[k];
       }
     }
   }
@@ -655,7 +672,8 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_split_kernel(const 
   const int ctid = tid - kApplyProducerThreads;
   const int word = ctid / TPW, part = ctid % TPW;
   const uint32_t my_q = smem_u32(qtile) + 4 * word;
-  const int64_t obj0 = tile_idx * p.tile + 4 * word + part * kOPT;
+  const int64_t tile_base = tile_idx * p.tile;
+  auto obj_of = [&](int k) { return word_object(tile_base, word, part * kOPT + k); };  // k < kOPT
   // per-lane constants: the index bits this lane owns and the bytes it gathers
   uint32_t shift[kDPT], mask[kDPT];
 #pragma unroll
@@ -669,7 +687,7 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_split_kernel(const 
   for (int k = 0; k < kOPT; ++k) sel[k] = kPrescaled ? (0x7650u | (uint32_t)(part * kOPT + k)) : (0x4440u | (uint32_t)(part * kOPT + k));
   acc_t acc[kOPT];
 #pragma unroll
-  for (int k = 0; k < kOPT; ++k) acc[k] = (p.first || obj0 + k >= p.n) ? (acc_t)0 : (acc_t)p.out[obj0 + k];
+  for (int k = 0; k < kOPT; ++k) acc[k] = (p.first || obj_of(k) >= p.n) ? (acc_t)0 : (acc_t)p.out[obj_of(k)];
   mbar_wait_warp(tile_bar, 0);
 
   // this lane's first descriptor in a tree: its part's first split, the half for its bit 6
@@ -717,7 +735,7 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_split_kernel(const 
   }
 #pragma unroll
   for (int k = 0; k < kOPT; ++k) {
-    if (obj0 + k < p.n) p.out[obj0 + k] = p.last ? __dadd_rn(__dmul_rn((double)acc[k], p.scale), p.bias) : (double)acc[k];
+    if (obj_of(k) < p.n) p.out[obj_of(k)] = p.last ? __dadd_rn(__dmul_rn((double)acc[k], p.scale), p.bias) : (double)acc[k];
   }
 }
 
@@ -752,13 +770,14 @@ __global__ void __launch_bounds__(kMultiThreads) apply_multi_kernel(const __grid
   const int word = threadIdx.x;
   const int64_t tile_idx = blockIdx.x;
   const uint8_t* qrow0 = p.q + tile_idx * (int64_t)p.n_features * p.tile + 4 * word;
-  const int64_t obj0 = tile_idx * p.tile + 4 * word;
+  const int64_t tile_base = tile_idx * p.tile;
+  auto obj_of = [&](int k) { return word_object(tile_base, word, k); };
   double acc[4][C];
 #pragma unroll
   for (int k = 0; k < 4; ++k)
 #pragma unroll
     for (int c = 0; c < C; ++c)
-      acc[k][c] = (p.first || obj0 + k >= p.n) ? 0.0 : p.out[(obj0 + k) * C + c];
+      acc[k][c] = (p.first || obj_of(k) >= p.n) ? 0.0 : p.out[obj_of(k) * C + c];
   for (int t = p.tree_begin; t < p.tree_end; ++t) {
     const uint2* ds = reinterpret_cast<const uint2*>(p.desc) + (size_t)t * DI;
     uint32_t lo = 0, hi = 0;
@@ -800,10 +819,10 @@ __global__ void __launch_bounds__(kMultiThreads) apply_multi_kernel(const __grid
   }
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    if (obj0 + k >= p.n) continue;
+    if (obj_of(k) >= p.n) continue;
 #pragma unroll
     for (int c = 0; c < C; ++c)
-      p.out[(obj0 + k) * C + c] = p.last ? __dadd_rn(__dmul_rn(acc[k][c], p.scale), p.bias) : acc[k][c];
+      p.out[obj_of(k) * C + c] = p.last ? __dadd_rn(__dmul_rn(acc[k][c], p.scale), p.bias) : acc[k][c];
   }
 }
 
