@@ -6,6 +6,7 @@
 namespace obt {
 
 using QuantFn = void (*)(QuantizeParams);
+using QuantTmaFn = void (*)(const CUtensorMap, const QuantizeParams);
 
 struct ApplyKernel {
   const void* fn = nullptr;
@@ -16,6 +17,7 @@ struct ApplyKernel {
 
 // K1, levels 0..8
 QuantFn pick_quant(int levels, int layout, bool tiled);
+QuantTmaFn pick_quant_tma(int levels);
 // K2, depths {1..8, 10, 12}
 ApplyKernel pick_apply(int di, int cmp, int leaf, bool write_idx, int dsrc);
 // K2s, depth-split (tpw 2: depths 2/4/6/8, tpw 4: depths 4/8)

@@ -24,4 +24,19 @@ QuantFn pick_quant(int levels, int layout, bool tiled) {
   }
 }
 
+QuantTmaFn pick_quant_tma(int levels) {
+  switch (levels) {
+    case 0: return quantize_tma_kernel<0>;
+    case 1: return quantize_tma_kernel<1>;
+    case 2: return quantize_tma_kernel<2>;
+    case 3: return quantize_tma_kernel<3>;
+    case 4: return quantize_tma_kernel<4>;
+    case 5: return quantize_tma_kernel<5>;
+    case 6: return quantize_tma_kernel<6>;
+    case 7: return quantize_tma_kernel<7>;
+    case 8: return quantize_tma_kernel<8>;
+    default: return nullptr;
+  }
+}
+
 }  // namespace obt

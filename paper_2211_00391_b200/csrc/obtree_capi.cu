@@ -4,6 +4,7 @@
 // reference, evaluate.py:138-166 and model.py:231-277), device residency, the
 // per-call launch plan (tile size, workspace) and kernel dispatch.  No CPU compute
 // path exists: if a kernel cannot run the call fails with an error code.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -26,6 +27,7 @@ using obt::ApplyKernel;
 using obt::QuantFn;
 using obt::pick_apply;
 using obt::pick_quant;
+using obt::pick_quant_tma;
 using obt::pick_split;
 
 namespace {
@@ -482,33 +484,110 @@ int apply_lanes(const obt_model* m, int tile, bool write_idx) {
   return choose_tpw(m, tile, write_idx, use_param_descriptors(m));
 }
 
+// Features per CTA (grid.y chunk): the fewest chunks whose Eytzinger arrays fit
+// `budget` bytes, split evenly (multiples of the 8-feature step); small batches split
+// finer until the grid has ~2 CTAs per SM, so a 10k-object batch is not quantized by 10
+// CTAs.
+int quantize_chunk(const obt_model* m, const BorderTable& bt, int64_t n_slots, size_t budget) {
+  const int F = m->n_features;
+  const size_t per_feature = bt.levels > 0 ? (size_t)bt.pitch * 4 : 0;
+  int chunks = per_feature ? (int)std::max<size_t>(1, (F * per_feature + budget - 1) / budget) : 1;
+  int fc = 0;
+  for (;; ++chunks) {
+    fc = ((F + chunks - 1) / chunks + 7) / 8 * 8;
+    if ((size_t)fc * per_feature <= budget || fc == 8) break;
+  }
+  const int64_t blocks = (n_slots + obt::kQuantBlock - 1) / obt::kQuantBlock;
+  while (fc > 8 && blocks * ((F + fc - 1) / fc) < 2 * m->sm_count) fc = std::max(8, (fc / 2 + 7) / 8 * 8);
+  return fc;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static const EncodeTiledFn fn = []() -> EncodeTiledFn {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+
+#ifndef OBT_TMA_L2
+#define OBT_TMA_L2 256
+#endif
+CUtensorMapL2promotion tma_l2_promotion() {
+  return OBT_TMA_L2 == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+         : OBT_TMA_L2 == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+         : OBT_TMA_L2 == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                             : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
+
+bool quantize_tma_enabled() {
+  const char* e = getenv("OBT_QUANT_TMA");  // A/B knob: 0 = always the LDG kernel
+  return !(e && !strcmp(e, "0"));
+}
+
 int launch_quantize(const obt_model* m, const float* x, int64_t n, int layout, uint8_t* out, bool tiled,
                     int tile, int64_t n_slots, bool swizzle, cudaStream_t stream) {
   const BorderTable& bt = tiled ? m->used : m->full;
-  QuantFn fn = pick_quant(bt.levels, layout, tiled);
-  if (!fn) return fail(OBT_E_UNSUPPORTED, "no quantize kernel for %d levels", bt.levels);
+  const int F = m->n_features;
   obt::QuantizeParams p{};
   p.x = x;
   p.n = n;
   p.n_slots = n_slots;
-  p.n_features = m->n_features;
+  p.n_features = F;
   p.eytz = bt.d;
   p.eytz_pitch = bt.pitch;
   p.out = out;
   p.tile = tile;
-  int fc = obt::quantize_chunk_features(bt.levels > 0 ? bt.pitch : 0, m->n_features);
-  // small batches: split the features finer (multiples of the 8-feature step) until the
-  // grid has ~2 CTAs per SM, so a 10k-object batch is not quantized by 10 CTAs
-  const int64_t blocks = (n_slots + obt::kQuantBlock - 1) / obt::kQuantBlock;
-  while (fc > 8 && blocks * ((m->n_features + fc - 1) / fc) < 2 * m->sm_count) fc = std::max(8, (fc / 2 + 7) / 8 * 8);
-  const size_t smem = bt.levels > 0 ? (size_t)std::min(fc, m->n_features) * bt.pitch * 4 : 16;
-  p.chunk_features = fc;
   p.two = 2;
   p.swizzle = swizzle ? 1 : 0;
+  const unsigned blocks = (unsigned)((n_slots + obt::kQuantBlock - 1) / obt::kQuantBlock);
+
+  // K1t: TMA-staged rows (object-major, tiled, 16-byte row pitch and alignment)
+  obt::QuantTmaFn tfn = pick_quant_tma(bt.levels);
+  if (tiled && layout == OBT_LAYOUT_OBJECT_MAJOR && F % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+      tfn && encode_tiled() && quantize_tma_enabled()) {
+    // two CTAs per SM: each gets half the SM's shared memory less the per-CTA reserve
+    const size_t half = (size_t)(m->smem_optin + 1024) / 2 - 1024;
+    const int fc = quantize_chunk(m, bt, n_slots, half - obt::kQTSmemFixed);
+    CUtensorMap map;
+    const cuuint64_t dims[2] = {(cuuint64_t)F, (cuuint64_t)n};
+    const cuuint64_t strides[1] = {(cuuint64_t)F * 4};
+    const cuuint32_t box[2] = {(cuuint32_t)obt::kQuantStep, (cuuint32_t)obt::kQTBoxRows};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_tiled()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(x), dims, strides,
+                                      box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                                      tma_l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r == CUDA_SUCCESS) {
+      p.chunk_features = fc;
+      const size_t smem = obt::kQTSmemFixed + (bt.levels > 0 ? (size_t)std::min(fc, F) * bt.pitch * 4 : 16);
+      CUDA_TRY(cudaFuncSetAttribute(tfn, cudaFuncAttributeMaxDynamicSharedMemorySize, m->smem_optin));
+      const dim3 grid(blocks, (unsigned)((F + fc - 1) / fc));
+      tfn<<<grid, obt::kQTThreads, smem, stream>>>(map, p);
+      ++g_launches;
+      CUDA_TRY(cudaGetLastError());
+      return OBT_OK;
+    }
+  }
+
+  QuantFn fn = pick_quant(bt.levels, layout, tiled);
+  if (!fn) return fail(OBT_E_UNSUPPORTED, "no quantize kernel for %d levels", bt.levels);
+  const int fc = quantize_chunk(m, bt, n_slots, obt::kQuantSmem);
+  const size_t smem = bt.levels > 0 ? (size_t)std::min(fc, F) * bt.pitch * 4 : 16;
+  p.chunk_features = fc;
   // the opt-in maximum, not this launch's size: the attribute is per function and
   // process-wide, so every caller must set the same value (concurrent launches race otherwise)
   CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, m->smem_optin));
-  dim3 grid((unsigned)((n_slots + obt::kQuantBlock - 1) / obt::kQuantBlock), (unsigned)((m->n_features + fc - 1) / fc));
+  const dim3 grid(blocks, (unsigned)((F + fc - 1) / fc));
   fn<<<grid, obt::kQuantThreads, smem, stream>>>(p);
   ++g_launches;
   CUDA_TRY(cudaGetLastError());

@@ -17,6 +17,7 @@
 //      reference fold, then out = acc * scale + bias with two roundings.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_fp16.h>
 #include <stdint.h>
@@ -70,6 +71,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
   while (!__all_sync(0xffffffffu, mbar_try(bar, parity))) {
   }
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 // global -> shared bulk copy; bytes % 16 == 0, both addresses 16-byte aligned.
@@ -134,13 +139,134 @@ __host__ __device__ constexpr int quantize_chunk_features(int eytz_pitch, int n_
 // runtime value 2 (a kernel parameter) so the update is an IMAD on the FMA pipe; plain
 // C++ (no asm) lets the compiler interleave the independent searches of a lane.
 // NaN compares false and walks left, giving bucket 0 (quantize.py:171).
+#ifndef OBT_EYTZ_MASK
+#define OBT_EYTZ_MASK 0
+#endif
 __device__ __forceinline__ uint32_t eytz_level(uint32_t o, float x, const float* e, uint32_t two) {
   const float b = *reinterpret_cast<const float*>(reinterpret_cast<const unsigned char*>(e) + o);
+#if OBT_EYTZ_MASK
+  // [x > b] as a 0 / all-ones mask (one FSET on the ALU pipe), then o' = 2o + 4 - 4 mask
+  // as two IMADs on the FMA pipe: one ALU op per level instead of FSETP + SEL
+  uint32_t m;
+  asm("set.gt.u32.f32 %0, %1, %2;" : "=r"(m) : "f"(x), "f"(b));
+  return m * 0xFFFFFFFCu + (o * two + 4u);
+#else
   return o * two + (x > b ? 8u : 4u);
+#endif
 }
 
 constexpr int kQuantStep = 8;  // features per step: one 32-byte sector per row
 
+// The searches of one step (8 features x the lane's 4 objects) and its 8 packed
+// bucket-word stores.  Lane objects are base + lane + 32k (the tile layout's word `lane`
+// of the 128-object block at `base`); ey holds the feature chunk's Eytzinger arrays.
+template <int L, bool TILED>
+__device__ __forceinline__ void quantize_step(const QuantizeParams& p, const float* ey, const float (&v)[kQuantStep][4],
+                                              int f0, int fq, int nf, int64_t base, int lane, bool full_objs) {
+  constexpr int kE = (1 << L) - 1;
+  constexpr int S = kQuantStep;
+  const uint32_t two = (uint32_t)p.two;
+  (void)two;  // unused when every level is resolved without a lookup
+  const int F = p.n_features;
+  const int64_t ob = base + lane;
+  uint32_t o[S][4];
+#pragma unroll
+  for (int j = 0; j < S; ++j)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) o[j][k] = 0;
+  // the top levels from registers: the feature's top nodes are loaded once (broadcast
+  // loads) and serve the lane's 4 objects, so each value makes L - kTop dependent
+  // shared-memory lookups instead of L.  Measured on B200 (cfg2, cfg4): kTop = 2 beats
+  // 3 (more selects on the ALU pipe), 1 and 0 (more lookups)
+#ifndef OBT_QUANT_TOP
+#define OBT_QUANT_TOP 2
+#endif
+  constexpr int kTop = (OBT_QUANT_TOP == 3 && L >= 4) ? 3 : (OBT_QUANT_TOP == 2 && L >= 3) ? 2
+                       : (OBT_QUANT_TOP == 1 && L >= 2) ? 1 : 0;
+  if constexpr (kTop == 1) {
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      const float n0 = ey[min(fq + j, nf - 1) * kE];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) o[j][k] = v[j][k] > n0 ? 8u : 4u;  // position 1 + c0 (x4)
+    }
+  }
+  if constexpr (kTop == 2) {
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      const float* e = ey + min(fq + j, nf - 1) * kE;
+      const float n0 = e[0], n1 = e[1], n2 = e[2];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float x = v[j][k];
+        const bool c0 = x > n0;
+        const bool c1 = x > (c0 ? n2 : n1);
+        // Eytzinger position after two levels: 3 + 2 c0 + c1 (byte offset x4)
+        o[j][k] = 12u + (c0 ? 8u : 0u) + (c1 ? 4u : 0u);
+      }
+    }
+  }
+  if constexpr (kTop == 3) {
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      const float* e = ey + min(fq + j, nf - 1) * kE;
+      float n[7];
+#pragma unroll
+      for (int i = 0; i < 7; ++i) n[i] = e[i];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float x = v[j][k];
+        const bool c0 = x > n[0];
+        const bool c1 = x > (c0 ? n[2] : n[1]);
+        const float b2 = c0 ? (c1 ? n[6] : n[5]) : (c1 ? n[4] : n[3]);
+        const bool c2 = x > b2;
+        // Eytzinger position after three levels: 7 + 4 c0 + 2 c1 + c2 (byte offset x4)
+        o[j][k] = 28u + (c0 ? 16u : 0u) + (c1 ? 8u : 0u) + (c2 ? 4u : 0u);
+      }
+    }
+  }
+#pragma unroll
+  for (int l = kTop; l < L; ++l)
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      const float* e = ey + min(fq + j, nf - 1) * kE;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) o[j][k] = eytz_level(o[j][k], v[j][k], e, two);
+    }
+#pragma unroll
+  for (int j = 0; j < S; ++j) {
+    if (fq + j >= nf) break;
+    uint32_t word = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      // bucket = leaf position - E; padding objects are zero (quantize.py:172)
+      const uint32_t q = (o[j][k] >> 2) - (uint32_t)kE;
+      word |= q << (8 * k);
+    }
+    if (!full_objs) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (ob + 32 * k >= p.n) word &= ~(0xFFu << (8 * k));
+    }
+    const int f = f0 + fq + j;
+    if (TILED) {
+      const int64_t t = base / p.tile, w = (base - t * p.tile + 4 * lane) ^ ((p.swizzle && (f & 1)) ? 64 : 0);
+      *reinterpret_cast<uint32_t*>(p.out + (t * F + f) * (int64_t)p.tile + w) = word;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (ob + 32 * k < p.n) p.out[(int64_t)f * p.n + ob + 32 * k] = (uint8_t)(word >> (8 * k));
+    }
+  }
+}
+
+// One CTA: 1024 objects (8 warps x 32 lanes x 4 objects) x one chunk of features
+// (grid.y).  The chunk's Eytzinger arrays are staged in shared memory once; each lane
+// then walks its 4 objects (rows one apart from its neighbours') x 8 features per step:
+// a 32-byte sector per row straight from HBM, 32 independent searches, 8 packed 32-bit
+// bucket stores (each warp writes 128 contiguous bytes of a feature row of the tile).
+// The fallback for inputs the TMA-staged kernel (K1t) does not take, and the plain
+// [F][n] output of obt_quantize_dev.
 template <int L, int LAYOUT, bool TILED>
 __global__ void __launch_bounds__(kQuantThreads, 2) quantize_kernel(QuantizeParams p) {
   extern __shared__ __align__(16) unsigned char qsm[];
@@ -212,74 +338,106 @@ __global__ void __launch_bounds__(kQuantThreads, 2) quantize_kernel(QuantizePara
   };
 
   // the 32 searches of one step and its 8 packed bucket-word stores
-  auto search_store = [&](const float (&v)[S][4], int fq) {
-    uint32_t o[S][4];
-#pragma unroll
-    for (int j = 0; j < S; ++j)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) o[j][k] = 0;
-    // levels 0-2 from registers: the feature's 7 top nodes are loaded once (three
-    // broadcast loads) and serve the lane's 4 objects, so each value makes L - 3
-    // dependent shared-memory lookups instead of L
-    constexpr int kTop = L >= 4 ? 3 : 0;
-    if constexpr (kTop == 3) {
-#pragma unroll
-      for (int j = 0; j < S; ++j) {
-        const float* e = ey + min(fq + j, nf - 1) * kE;
-        float n[7];
-#pragma unroll
-        for (int i = 0; i < 7; ++i) n[i] = e[i];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float x = v[j][k];
-          const bool c0 = x > n[0];
-          const bool c1 = x > (c0 ? n[2] : n[1]);
-          const float b2 = c0 ? (c1 ? n[6] : n[5]) : (c1 ? n[4] : n[3]);
-          const bool c2 = x > b2;
-          // Eytzinger position after three levels: 7 + 4 c0 + 2 c1 + c2 (byte offset x4)
-          o[j][k] = 28u + (c0 ? 16u : 0u) + (c1 ? 8u : 0u) + (c2 ? 4u : 0u);
-        }
-      }
-    }
-#pragma unroll
-    for (int l = kTop; l < L; ++l)
-#pragma unroll
-      for (int j = 0; j < S; ++j) {
-        const float* e = ey + min(fq + j, nf - 1) * kE;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) o[j][k] = eytz_level(o[j][k], v[j][k], e, two);
-      }
-#pragma unroll
-    for (int j = 0; j < S; ++j) {
-      if (fq + j >= nf) break;
-      uint32_t word = 0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        // bucket = leaf position - E; padding objects are zero (quantize.py:172)
-        const uint32_t q = (o[j][k] >> 2) - (uint32_t)kE;
-        word |= q << (8 * k);
-      }
-      if (!full_objs) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (ob + 32 * k >= p.n) word &= ~(0xFFu << (8 * k));
-      }
-      const int f = f0 + fq + j;
-      if (TILED) {
-        const int64_t t = base / p.tile, w = (base - t * p.tile + 4 * lane) ^ ((p.swizzle && (f & 1)) ? 64 : 0);
-        *reinterpret_cast<uint32_t*>(p.out + (t * F + f) * (int64_t)p.tile + w) = word;
-      } else {
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (ob + 32 * k < p.n) p.out[(int64_t)f * p.n + ob + 32 * k] = (uint8_t)(word >> (8 * k));
-      }
-    }
-  };
 
   for (int fq = 0; fq < nf; fq += S) {
     float v[S][4];
     load_step(v, fq);
-    search_store(v, fq);
+    quantize_step<L, TILED>(p, ey, v, f0, fq, nf, base, lane, full_objs);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1t: TMA-staged quantize (object-major input, tiled output; F % 4 == 0, 16-byte
+// aligned features).  A producer warp streams the CTA's 1024 feature rows, 8 features
+// (one 32-byte sector) per row per step, with four 2-D tensor copies per stage
+// (box 8 features x 256 rows, 32-byte swizzle) into a 2-stage ring; the 8 consumer
+// warps read their rows back with two conflict-free LDS.128 each (rows l + 32k of a
+// quarter-warp are 8 consecutive rows, and the swizzle spreads their 16-byte halves
+// over all 8 bank quads), release the stage, and run the same searches and stores as
+// K1.  The rows never occupy registers while in flight, and the TMA requests are whole
+// sectors, so the consumer warps wait on shared memory instead of HBM.
+constexpr int kQTConsumerWarps = kQuantBlock / 128;                  // 8
+constexpr int kQTThreads = 32 * (1 + kQTConsumerWarps);              // producer + consumers
+constexpr int kQTStages = 2;
+constexpr int kQTBoxRows = 256;
+constexpr int kQTStageBytes = kQuantBlock * kQuantStep * 4;          // 32 KB
+constexpr int kQTSmemFixed = 1024 + kQTStages * kQTStageBytes + 64;  // alignment + ring + barriers
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int L>
+__global__ void __launch_bounds__(kQTThreads, 2) quantize_tma_kernel(const __grid_constant__ CUtensorMap rows,
+                                                                     const QuantizeParams p) {
+  extern __shared__ __align__(16) unsigned char qt_raw[];
+  unsigned char* ring = qt_raw + ((1024u - (smem_u32(qt_raw) & 1023u)) & 1023u);  // swizzle atoms need alignment
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kQTStages * kQTStageBytes);
+  uint64_t* empty = full + kQTStages;
+  float* ey = reinterpret_cast<float*>(empty + kQTStages);
+  constexpr int kE = (1 << L) - 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int fc = p.chunk_features;
+  const int f0 = blockIdx.y * fc;
+  const int nf = min(fc, p.n_features - f0);
+  const int n_steps = (nf + kQuantStep - 1) / kQuantStep;
+  const int64_t row0 = (int64_t)blockIdx.x * kQuantBlock;
+  // consumer warps whose 128-object block lies inside the grid's slots
+  const int64_t blocks_left = (p.n_slots - row0 + 127) / 128;
+  const int active = blocks_left < kQTConsumerWarps ? (int)blocks_left : kQTConsumerWarps;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kQTStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 32 * active);  // every active consumer thread releases its reads
+    }
+    fence_mbar_init();
+  }
+  if (kE > 0) {
+    const float* src = p.eytz + (int64_t)f0 * kE;
+    for (int i = threadIdx.x; i < nf * kE; i += kQTThreads) ey[i] = __ldg(src + i);
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int st = 0; st < n_steps; ++st) {
+        const int s = st % kQTStages;
+        if (st >= kQTStages) mbar_wait(&empty[s], (uint32_t)(st / kQTStages - 1) & 1u);
+        mbar_expect_tx(&full[s], kQTStageBytes);  // out-of-range rows/features arrive zero-filled
+        unsigned char* dst = ring + (size_t)s * kQTStageBytes;
+#pragma unroll
+        for (int b = 0; b < kQuantBlock / kQTBoxRows; ++b)
+          tma_load_2d(dst + b * kQTBoxRows * kQuantStep * 4, &rows, f0 + st * kQuantStep,
+                      (int)(row0 + b * kQTBoxRows), &full[s]);
+      }
+    }
+    return;
+  }
+  const int cw = warp - 1;
+  if (cw >= active) return;
+  const int64_t base = row0 + cw * 128;
+  const bool full_objs = base + lane + 96 < p.n;
+  for (int st = 0; st < n_steps; ++st) {
+    const int s = st % kQTStages;
+    mbar_wait_warp(&full[s], (uint32_t)(st / kQTStages) & 1u);
+    const unsigned char* stage = ring + (size_t)s * kQTStageBytes;
+    float v[kQuantStep][4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      // row r = 128 cw + lane + 32k: 32 bytes at 32 r, 16-byte halves swapped when bit 2 of r is set
+      const int r = cw * 128 + lane + 32 * k;
+      const unsigned char* rp = stage + 32 * r;
+      const uint32_t sw = (uint32_t)((r >> 2) & 1) * 16u;
+      const float4 a = *reinterpret_cast<const float4*>(rp + sw);
+      const float4 b = *reinterpret_cast<const float4*>(rp + (16u ^ sw));
+      v[0][k] = a.x; v[1][k] = a.y; v[2][k] = a.z; v[3][k] = a.w;
+      v[4][k] = b.x; v[5][k] = b.y; v[6][k] = b.z; v[7][k] = b.w;
+    }
+    mbar_arrive(&empty[s]);  // values are in registers: the producer may refill the stage
+    quantize_step<L, true>(p, ey, v, f0, st * kQuantStep, nf, base, lane, full_objs);
   }
 }
 
@@ -358,9 +516,6 @@ __device__ __forceinline__ uint32_t byte_of(uint32_t w) {
   return __byte_perm(w, 0u, 0x4440u | K);
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 
 __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
   uint32_t v;
