@@ -521,7 +521,7 @@ EncodeTiledFn encode_tiled() {
 }
 
 #ifndef OBT_TMA_L2
-#define OBT_TMA_L2 256
+#define OBT_TMA_L2 128  // measured: 256 B reads 1.2 GB for 0.8 GB of features, 128 B 0.99 GB, same time
 #endif
 CUtensorMapL2promotion tma_l2_promotion() {
   return OBT_TMA_L2 == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
