@@ -809,12 +809,13 @@ int obt_model_create(const obt_model_desc* d, int device, obt_model** out) {
       const float f = (float)v;
       exact32 = std::isfinite(f) && (double)f == v && !(v == 0.0 && std::signbit(v) != std::signbit(f));
     }
-    m->leaf_storage = exact32 ? 1 : 0;
+    const char* force64 = getenv("OBT_LEAF_STORAGE");  // A/B knob: "64" keeps binary64 tables
+    m->leaf_storage = (exact32 && !(force64 && !strcmp(force64, "64"))) ? 1 : 0;
   }
   const size_t ls = leaf_size(m->leaf_storage);
   if (C > 1) {
-    // multi-output records [T][2^DI][CP]: one leaf's C values contiguous, rows of 16 bytes
-    const int CP = m->leaf_storage == 1 ? (C + 3) / 4 * 4 : (C + 1) / 2 * 2;
+    // multi-output records [T][2^DI][CP]: one leaf's C values contiguous, padded to 32-byte rows (fp32)
+    const int CP = obt::multi_record_values(m->leaf_storage, C);
     std::vector<uint8_t> rec((size_t)std::max(m->n_trees, 1) * per_tree * CP * ls, 0);
     for (int t = 0; t < m->n_trees; ++t)
       for (int c = 0; c < C; ++c)

@@ -918,10 +918,22 @@ struct MultiParams {
 
 constexpr int kMultiThreads = 128;  // 512 objects per CTA = one tile
 
+// Values per multi-output leaf record: fp32 records in 16-byte rows (48 bytes at C = 10;
+// 32-byte rows with 256-bit loads measured slower), fp64 records in 16-byte rows.
+#ifndef OBT_MULTI_ROW32
+#define OBT_MULTI_ROW32 0
+#endif
+__host__ __device__ constexpr int multi_record_values(int leaf, int c) {
+  return leaf == 1 ? (OBT_MULTI_ROW32 ? (c + 7) / 8 * 8 : (c + 3) / 4 * 4) : (c + 1) / 2 * 2;
+}
+#ifndef OBT_MULTI_PF
+#define OBT_MULTI_PF 0  // measured no gain at cfg5 (L2 prefetch 4-16 trees ahead)
+#endif
+
 template <int DI, int CMP, int LEAF, int C>
 __global__ void __launch_bounds__(kMultiThreads) apply_multi_kernel(const __grid_constant__ MultiParams p) {
   using leaf_t = typename LeafT<LEAF>::T;
-  constexpr int CP = LEAF == 1 ? (C + 3) / 4 * 4 : (C + 1) / 2 * 2;  // record stride (16-byte rows)
+  constexpr int CP = multi_record_values(LEAF, C);  // record stride: 32-byte rows (fp32), 16-byte (fp64)
   const int word = threadIdx.x;
   const int64_t tile_idx = blockIdx.x;
   const uint8_t* qrow0 = p.q + tile_idx * (int64_t)p.n_features * p.tile + 4 * word;
@@ -934,6 +946,17 @@ __global__ void __launch_bounds__(kMultiThreads) apply_multi_kernel(const __grid
     for (int c = 0; c < C; ++c)
       acc[k][c] = (p.first || obj_of(k) >= p.n) ? 0.0 : p.out[obj_of(k) * C + c];
   for (int t = p.tree_begin; t < p.tree_end; ++t) {
+    if (OBT_MULTI_PF > 0 && t + OBT_MULTI_PF < p.tree_end) {
+      // the bucket rows of a tree OBT_MULTI_PF ahead into L2: the tile's rows do not stay
+      // L2-resident between uses (F = 1000 bytes per object), so without this every
+      // tree's index waits on HBM
+      const uint2* dp = reinterpret_cast<const uint2*>(p.desc) + (size_t)(t + OBT_MULTI_PF) * DI;
+#pragma unroll
+      for (int d = 0; d < DI; ++d) {
+        const uint32_t off = CMP == 7 ? __ldg(&dp[d].x) : (__ldg(&dp[d].x) >> 8);
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(qrow0 + off));
+      }
+    }
     const uint2* ds = reinterpret_cast<const uint2*>(p.desc) + (size_t)t * DI;
     uint32_t lo = 0, hi = 0;
 #pragma unroll
@@ -950,26 +973,44 @@ __global__ void __launch_bounds__(kMultiThreads) apply_multi_kernel(const __grid
       else hi |= (b7 >> (15 - d)) & (0x01010101u << (d - 8));
     }
     const leaf_t* tab = reinterpret_cast<const leaf_t*>(p.leaves) + ((size_t)t << DI) * CP;
+    // all 4 objects' records are requested before any is consumed: the L2 round trips
+    // overlap (each record is CP values in 16-byte rows)
+    if constexpr (LEAF == 1 && OBT_MULTI_ROW32) {
+      // fp32 records: one 256-bit load per 32-byte row
+      constexpr int kRows = (C + 7) / 8;
+      float rec[4][kRows * 8];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t idx = ((lo >> (8 * k)) & 0xffu) | (DI > 8 ? ((hi >> (8 * k)) & 0xffu) << 8 : 0u);
-      const leaf_t* rec = tab + (size_t)idx * CP;
-      leaf_t v[CP];
-      if constexpr (LEAF == 1) {
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t idx = ((lo >> (8 * k)) & 0xffu) | (DI > 8 ? ((hi >> (8 * k)) & 0xffu) << 8 : 0u);
+        const float* r = reinterpret_cast<const float*>(tab) + (size_t)idx * CP;
 #pragma unroll
-        for (int c4 = 0; c4 < CP / 4; ++c4) {
-          const float4 q4 = __ldg(reinterpret_cast<const float4*>(rec) + c4);
-          v[4 * c4 + 0] = q4.x; v[4 * c4 + 1] = q4.y; v[4 * c4 + 2] = q4.z; v[4 * c4 + 3] = q4.w;
-        }
-      } else {
-#pragma unroll
-        for (int c2 = 0; c2 < CP / 2; ++c2) {
-          const double2 q2 = __ldg(reinterpret_cast<const double2*>(rec) + c2);
-          v[2 * c2 + 0] = q2.x; v[2 * c2 + 1] = q2.y;
+        for (int i = 0; i < kRows; ++i) {
+          float* d = rec[k] + 8 * i;
+          asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                       : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3]), "=f"(d[4]), "=f"(d[5]), "=f"(d[6]), "=f"(d[7])
+                       : "l"(r + 8 * i));
         }
       }
 #pragma unroll
-      for (int c = 0; c < C; ++c) acc[k][c] += (double)v[c];
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc[k][c] += (double)rec[k][c];
+    } else {
+      constexpr int kRows = CP * (int)sizeof(leaf_t) / 16;
+      uint4 rec[4][kRows];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t idx = ((lo >> (8 * k)) & 0xffu) | (DI > 8 ? ((hi >> (8 * k)) & 0xffu) << 8 : 0u);
+        const uint4* r = reinterpret_cast<const uint4*>(tab + (size_t)idx * CP);
+#pragma unroll
+        for (int i = 0; i < kRows; ++i) rec[k][i] = __ldg(r + i);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const leaf_t* v = reinterpret_cast<const leaf_t*>(rec[k]);
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc[k][c] += (double)v[c];
+      }
     }
   }
 #pragma unroll
