@@ -139,20 +139,18 @@ __host__ __device__ constexpr int quantize_chunk_features(int eytz_pitch, int n_
 // runtime value 2 (a kernel parameter) so the update is an IMAD on the FMA pipe; plain
 // C++ (no asm) lets the compiler interleave the independent searches of a lane.
 // NaN compares false and walks left, giving bucket 0 (quantize.py:171).
-#ifndef OBT_EYTZ_MASK
-#define OBT_EYTZ_MASK 0
-#endif
+// The condition is applied as a predicated add written in PTX: ptxas then emits FSETP +
+// a predicated IADD that it can place on the FMA pipe (IMAD.IADD), instead of FSETP +
+// SEL, both on the ALU pipe that bounds this kernel (measured on B200).
+__device__ __forceinline__ uint32_t add_if_greater(uint32_t r, float x, float b, uint32_t inc) {
+  asm("{\n .reg .pred p;\n setp.gt.f32 p, %1, %2;\n @p add.u32 %0, %0, %3;\n}" : "+r"(r) : "f"(x), "f"(b), "r"(inc));
+  return r;
+}
+
 __device__ __forceinline__ uint32_t eytz_level(uint32_t o, float x, const float* e, uint32_t two) {
   const float b = *reinterpret_cast<const float*>(reinterpret_cast<const unsigned char*>(e) + o);
-#if OBT_EYTZ_MASK
-  // [x > b] as a 0 / all-ones mask (one FSET on the ALU pipe), then o' = 2o + 4 - 4 mask
-  // as two IMADs on the FMA pipe: one ALU op per level instead of FSETP + SEL
-  uint32_t m;
-  asm("set.gt.u32.f32 %0, %1, %2;" : "=r"(m) : "f"(x), "f"(b));
-  return m * 0xFFFFFFFCu + (o * two + 4u);
-#else
-  return o * two + (x > b ? 8u : 4u);
-#endif
+  const uint32_t four = two + two;  // runtime 4: the adds stay IMAD-able
+  return add_if_greater(o * two + four, x, b, four);
 }
 
 constexpr int kQuantStep = 8;  // features per step: one 32-byte sector per row
@@ -200,9 +198,9 @@ __device__ __forceinline__ void quantize_step(const QuantizeParams& p, const flo
       for (int k = 0; k < 4; ++k) {
         const float x = v[j][k];
         const bool c0 = x > n0;
-        const bool c1 = x > (c0 ? n2 : n1);
         // Eytzinger position after two levels: 3 + 2 c0 + c1 (byte offset x4)
-        o[j][k] = 12u + (c0 ? 8u : 0u) + (c1 ? 4u : 0u);
+        const uint32_t o1 = add_if_greater(12u, x, n0, 8u);
+        o[j][k] = add_if_greater(o1, x, c0 ? n2 : n1, 4u);
       }
     }
   }
