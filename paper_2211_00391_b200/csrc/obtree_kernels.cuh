@@ -164,7 +164,8 @@ __device__ __forceinline__ void quantize_step(const QuantizeParams& p, const flo
   constexpr int kE = (1 << L) - 1;
   constexpr int S = kQuantStep;
   const uint32_t two = (uint32_t)p.two;
-  (void)two;  // unused when every level is resolved without a lookup
+  // 2^30, 2^6, 2^14, 2^22 from the run-time 2 (kept as IMAD multipliers, not shifts)
+  const uint32_t m6 = two << 5, m14 = two << 13, m22 = two << 21, m30 = two << 29;
   const int F = p.n_features;
   const int64_t ob = base + lane;
   uint32_t o[S][4];
@@ -234,13 +235,13 @@ __device__ __forceinline__ void quantize_step(const QuantizeParams& p, const flo
 #pragma unroll
   for (int j = 0; j < S; ++j) {
     if (fq + j >= nf) break;
-    uint32_t word = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      // bucket = leaf position - E; padding objects are zero (quantize.py:172)
-      const uint32_t q = (o[j][k] >> 2) - (uint32_t)kE;
-      word |= q << (8 * k);
-    }
+    // bucket k = o_k / 4 - E in byte k (padding objects are zero, quantize.py:172):
+    // word = (o0 >> 2) + 64 o1 + 2^14 o2 + 2^22 o3 - E * 0x01010101, as IMAD.HI + IMADs with
+    // run-time multipliers, so the packing runs on the FMA pipe rather than the ALU pipe
+    uint32_t word = __umulhi(o[j][0], m30) - (uint32_t)kE * 0x01010101u;
+    word = o[j][1] * m6 + word;
+    word = o[j][2] * m14 + word;
+    word = o[j][3] * m22 + word;
     if (!full_objs) {
 #pragma unroll
       for (int k = 0; k < 4; ++k)
