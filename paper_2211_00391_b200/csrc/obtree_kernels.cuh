@@ -288,7 +288,8 @@ __global__ void __launch_bounds__(kQuantThreads, 2) quantize_kernel(QuantizePara
   if (base >= p.n_slots) return;  // past the last tile (no barrier follows)
   const int64_t ob = base + lane;
   const bool full_objs = ob + 96 < p.n;
-  const bool vec_rows = LAYOUT == 0 ? ((F & 3) == 0 && (f0 & 3) == 0) : true;
+  const bool vec_rows =
+      LAYOUT == 0 ? ((F & 3) == 0 && (f0 & 3) == 0 && (reinterpret_cast<uintptr_t>(p.x) & 15) == 0) : true;
   static_assert(kQuantStep == 8, "a 256-bit row load covers exactly one step");
   const bool sector_rows = LAYOUT == 0 && (F & 7) == 0 && (reinterpret_cast<uintptr_t>(p.x) & 31) == 0;
   const uint32_t two = (uint32_t)p.two;

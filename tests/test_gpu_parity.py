@@ -413,3 +413,24 @@ def test_concurrent_predicts_from_threads():
     for t in threads:
         t.join()
     assert not errors, errors[:3]
+
+
+@pytest.mark.parametrize("F", [4, 8, 12, 200])
+@pytest.mark.parametrize("n", [1, 127, 1023, 1025, 4099])
+def test_tma_quantize_path_ragged_batches(F, n):
+    """K1t (TMA-staged rows: object-major, F % 4 == 0, 16-byte aligned) on ragged
+    batches -- partial CTAs and zero-filled rows past n -- and the LDG fallback on the
+    same data through a misaligned view (forces K1): both bit-exact."""
+    model = _model(F, 64, 50, 6, seed=F * 10 + n % 7)
+    x = _features(model, n, seed=F + n)
+    fm = oracle.flatten(model)
+    want = oracle.evaluate_scalar(fm, x)
+    ev = obt.Evaluator(model)
+    xd = torch.from_numpy(x).cuda()
+    assert np.array_equal(ev.predict_device(xd).cpu().numpy(), want)
+    pad = torch.empty(n * F + 1, dtype=torch.float32, device="cuda")
+    xm = pad[1:].view(n, F)  # 4-byte aligned only: not eligible for the tensor map
+    xm.copy_(xd)
+    assert np.array_equal(ev.predict_device(xm).cpu().numpy(), want)
+    q_ref = oracle.quantize(fm, x)
+    assert np.array_equal(stages.quantize(model, xd).cpu().numpy(), q_ref)
