@@ -90,9 +90,11 @@ int obt_model_info(const obt_model* model, int32_t* n_features, int32_t* n_trees
 int obt_workspace_size(const obt_model* model, int64_t n_objects, size_t* bytes);
 
 /* Evaluator.predict (evaluate.py:268-300) on device-resident features:
- * x_dev float32 [n][F] or [F][n]; out_dev float64 [n][C].  workspace may be NULL
- * (then it is taken from the stream-ordered pool).  n == 0 is a no-op
- * (evaluate.py:277-279).  Asynchronous on `stream`. */
+ * x_dev float32 [n][F] or [F][n] (4-byte aligned; 16-byte aligned object-major rows
+ * with F % 4 == 0 take the TMA-staged quantize); out_dev float64 [n][C].  workspace
+ * (256-byte aligned, obt_workspace_size bytes) may be NULL: then it comes from the
+ * library's stream-ordered pool.  n == 0 is a no-op (evaluate.py:277-279).
+ * Asynchronous on `stream`. */
 int obt_predict_dev(const obt_model* model, const float* x_dev, int64_t n_objects,
                     int32_t layout, double* out_dev, void* workspace, size_t workspace_bytes,
                     void* stream);

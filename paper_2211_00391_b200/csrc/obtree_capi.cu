@@ -924,6 +924,12 @@ static int predict_impl(obt_model* m, const float* x, int64_t n, int32_t layout,
   const size_t need = workspace_bytes(m, n, tile);
   uint8_t* q = static_cast<uint8_t*>(ws);
   bool owned = false;
+  // bucket tiles move by TMA bulk copies (16-byte aligned); predictions are doubles
+  if (ws && (reinterpret_cast<uintptr_t>(ws) & 255))
+    return fail(OBT_E_INVALID, "workspace must be 256-byte aligned");
+  if (out && (reinterpret_cast<uintptr_t>(out) & 7)) return fail(OBT_E_INVALID, "output must be 8-byte aligned");
+  if (idx_out && (reinterpret_cast<uintptr_t>(idx_out) & 1)) return fail(OBT_E_INVALID, "index output must be 2-byte aligned");
+  if (x && (reinterpret_cast<uintptr_t>(x) & 3)) return fail(OBT_E_INVALID, "features must be 4-byte aligned");
   if (!q || ws_bytes < need) {
     if (ws && ws_bytes < need) return fail(OBT_E_INVALID, "workspace of %zu bytes, need %zu", ws_bytes, need);
     CUDA_TRY(pool_alloc(reinterpret_cast<void**>(&q), need, m->device, stream));

@@ -434,3 +434,24 @@ def test_tma_quantize_path_ragged_batches(F, n):
     assert np.array_equal(ev.predict_device(xm).cpu().numpy(), want)
     q_ref = oracle.quantize(fm, x)
     assert np.array_equal(stages.quantize(model, xd).cpu().numpy(), q_ref)
+
+
+def test_misaligned_workspace_and_output_rejected():
+    """Caller buffers the kernels cannot use are refused with OBT_E_INVALID, not faulted on."""
+    from paper_2211_00391_b200 import _native
+
+    model = _model(8, 16, 10, 4, seed=3)
+    x = torch.from_numpy(_features(model, 300, seed=4)).cuda()
+    ev = obt.Evaluator(model)
+    ws = torch.empty(ev.workspace_bytes(300) + 512, dtype=torch.uint8, device="cuda")
+    with pytest.raises(_native.NativeError, match="256-byte aligned"):
+        ev.predict_device(x, workspace=ws[1:])
+    lib = _native.require_gpu()
+    out = torch.empty(301, dtype=torch.float64, device="cuda")
+    handle = ev._dev.handle if hasattr(ev, "_dev") else None
+    if handle is None:
+        pytest.skip("evaluator exposes no device handle")
+    rc = lib.obt_predict_dev(handle, x.data_ptr(), 300, 0, out.data_ptr() + 4, None, 0,
+                             _native.current_stream_handle())
+    assert rc == _native.OBT_E_INVALID and b"8-byte aligned" in lib.obt_last_error()
+    ev.predict_device(x, workspace=ws[:ev.workspace_bytes(300)])  # aligned: fine
