@@ -1056,7 +1056,26 @@ int obt_predict_host(const obt_model* mc, const float* x_host, int64_t n, int32_
   // 128 MB of features (a single chunk when the batch is small).
   int64_t rows = std::max<int64_t>(1024, ((int64_t)128 << 20) / ((int64_t)F * 4) / 1024 * 1024);
   rows = std::min(rows, n);
-  const int64_t n_chunks = (n + rows - 1) / rows;
+  // Chunk boundaries: full chunks, then a tapered tail (rows/2, /4, /8, /8) so the work
+  // left after the last copy -- that chunk's kernels and score copy -- is small.
+  std::vector<int64_t> bounds{0};
+  if (n <= rows) {
+    bounds.push_back(n);  // one chunk: nothing to overlap
+  } else {
+    const int64_t r = rows;
+    const int64_t tail[4] = {std::max<int64_t>(1024, r / 2), std::max<int64_t>(1024, r / 4),
+                             std::max<int64_t>(1024, r / 8), std::max<int64_t>(1024, r / 8)};
+    const int64_t tail_sum = tail[0] + tail[1] + tail[2] + tail[3];
+    int64_t pos = 0;
+    while (n - pos > tail_sum + r) { pos += r; bounds.push_back(pos); }
+    if (n - pos > tail_sum) { pos = n - tail_sum; bounds.push_back(pos); }
+    for (int i = 0; i < 4 && pos < n; ++i) {
+      pos = std::min(n, pos + tail[i]);
+      if (pos > bounds.back()) bounds.push_back(pos);
+    }
+    if (bounds.back() != n) bounds.push_back(n);
+  }
+  const int64_t n_chunks = (int64_t)bounds.size() - 1;
   const int nbuf = n_chunks > 1 ? 2 : 1;
   float* x_dev[2] = {nullptr, nullptr};
   double* out_dev[2] = {nullptr, nullptr};
@@ -1083,7 +1102,7 @@ int obt_predict_host(const obt_model* mc, const float* x_host, int64_t n, int32_
   int launches = 0;
   for (int64_t i = 0; i < n_chunks && rc == OBT_OK; ++i) {
     const int b = (int)(i % nbuf);
-    const int64_t o0 = i * rows, ni = std::min(rows, n - o0);
+    const int64_t o0 = bounds[i], ni = bounds[i + 1] - bounds[i];
     if (i >= nbuf) cuda_ok(cudaStreamWaitEvent(copy, done[b], 0), "stream wait");  // buffer b free again
     if (layout == OBT_LAYOUT_OBJECT_MAJOR) {
       cuda_ok(cudaMemcpyAsync(x_dev[b], x_host + o0 * F, (size_t)ni * F * 4, cudaMemcpyHostToDevice, copy), "H2D");

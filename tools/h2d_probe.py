@@ -17,3 +17,16 @@ for _ in range(5):
 torch.cuda.synchronize()
 dt = (time.perf_counter() - t) / 5
 print(f"D2H pinned 800 MB: {dt*1e3:.2f} ms = {0.8/dt:.1f} GB/s")
+# 128 MB chunks back to back (the obt_predict_host pipeline's copy pattern)
+chunk = 128 << 20
+n = x.numel() * 4
+t = time.perf_counter()
+for _ in range(5):
+    off = 0
+    while off < n:
+        ln = min(chunk, n - off)
+        d.view(torch.uint8)[off:off + ln].copy_(x.view(torch.uint8)[off:off + ln], non_blocking=True)
+        off += ln
+torch.cuda.synchronize()
+dt = (time.perf_counter() - t) / 5
+print(f"H2D pinned 800 MB in 128 MB chunks: {dt*1e3:.2f} ms = {0.8/dt:.1f} GB/s")
