@@ -535,8 +535,17 @@ bool quantize_tma_enabled() {
   return !(e && !strcmp(e, "0"));
 }
 
+// Tiled output may have a second region (objects >= split, tiles of tile2 into out2):
+// the tail-wave region of predict_impl, quantized by the same launch.
+struct SecondRegion {
+  int64_t split = -1;  // < 0: none
+  uint8_t* out = nullptr;
+  int tile = 0;
+  bool swizzle = false;
+};
+
 int launch_quantize(const obt_model* m, const float* x, int64_t n, int layout, uint8_t* out, bool tiled,
-                    int tile, int64_t n_slots, bool swizzle, cudaStream_t stream) {
+                    int tile, int64_t n_slots, bool swizzle, cudaStream_t stream, SecondRegion r2 = SecondRegion()) {
   const BorderTable& bt = tiled ? m->used : m->full;
   const int F = m->n_features;
   obt::QuantizeParams p{};
@@ -550,6 +559,11 @@ int launch_quantize(const obt_model* m, const float* x, int64_t n, int layout, u
   p.tile = tile;
   p.two = 2;
   p.swizzle = swizzle ? 1 : 0;
+  p.ld = n;
+  p.split = r2.split < 0 ? n_slots : r2.split;
+  p.out2 = r2.out;
+  p.tile2 = r2.tile > 0 ? r2.tile : tile;
+  p.swizzle2 = r2.swizzle ? 1 : 0;
   const unsigned blocks = (unsigned)((n_slots + obt::kQuantBlock - 1) / obt::kQuantBlock);
 
   // K1t: TMA-staged rows (object-major, tiled, 16-byte row pitch and alignment)
@@ -702,6 +716,43 @@ struct DeviceGuard {
 size_t workspace_bytes(const obt_model* m, int64_t n, int tile) {
   const int64_t n_tiles = (n + tile - 1) / tile;
   return (size_t)n_tiles * tile * m->n_features;
+}
+
+// One predict over up to two object ranges: whole waves of the main tile (one tile per
+// SM per wave), then the remainder -- what would be a partial last wave -- re-tiled so
+// every SM gets a share.  The smaller tail tiles run with depth-split lanes when they
+// leave few warps, so the tail finishes sooner than one more wave of main tiles
+// (cfg2: 977 tiles = 6.6 waves of 1024 objects).  OBT_TAIL_SPLIT=0 disables it.
+struct Regions {
+  int n_reg = 1;
+  int64_t begin[2] = {0, 0}, count[2] = {0, 0};
+  int tile[2] = {-1, -1};
+};
+
+Regions plan_regions(const obt_model* m, int64_t n, bool split_ok) {
+  Regions r;
+  r.count[0] = n;
+  r.tile[0] = plan_tile(m, n);
+  const char* e = getenv("OBT_TAIL_SPLIT");
+  if (!split_ok || r.tile[0] < 0 || m->n_outputs > 1 || (e && !strcmp(e, "0"))) return r;
+  const int64_t wave = (int64_t)m->sm_count * r.tile[0];
+  const int64_t full = n / wave * wave, rest = n - full;
+  if (full == 0 || rest == 0) return r;
+  int64_t tb = (rest + m->sm_count - 1) / m->sm_count;
+  tb = (tb + kTileQuantum - 1) / kTileQuantum * kTileQuantum;
+  if (tb >= r.tile[0]) return r;
+  r.n_reg = 2;
+  r.count[0] = full;
+  r.begin[1] = full;
+  r.count[1] = rest;
+  r.tile[1] = (int)tb;
+  return r;
+}
+
+size_t regions_workspace(const obt_model* m, const Regions& r) {
+  size_t b = 0;
+  for (int i = 0; i < r.n_reg; ++i) b += workspace_bytes(m, r.count[i], r.tile[i]);
+  return b;
 }
 
 int check_layout(int layout) {
@@ -879,9 +930,9 @@ int obt_model_info(const obt_model* m, int32_t* n_features, int32_t* n_trees, in
 int obt_workspace_size(const obt_model* m, int64_t n, size_t* bytes) {
   if (!m || !bytes) return fail(OBT_E_INVALID, "null argument");
   if (n < 0) return fail(OBT_E_INVALID, "negative object count");
-  const int tile = plan_tile(m, std::max<int64_t>(n, 1));
-  if (tile < 0) return fail(OBT_E_UNSUPPORTED, "%d features do not fit a 128-object tile", m->n_features);
-  *bytes = n == 0 ? 0 : workspace_bytes(m, n, tile);
+  const Regions one = plan_regions(m, std::max<int64_t>(n, 1), false), two = plan_regions(m, std::max<int64_t>(n, 1), true);
+  if (one.tile[0] < 0) return fail(OBT_E_UNSUPPORTED, "%d features do not fit a 128-object tile", m->n_features);
+  *bytes = n == 0 ? 0 : std::max(regions_workspace(m, one), regions_workspace(m, two));
   return OBT_OK;
 }
 
@@ -919,9 +970,9 @@ static cudaError_t pool_alloc(void** ptr, size_t bytes, int device, cudaStream_t
 static int predict_impl(obt_model* m, const float* x, int64_t n, int32_t layout, double* out, uint16_t* idx_out,
                         int tree_begin, int tree_end, void* ws, size_t ws_bytes, cudaStream_t stream,
                         cudaEvent_t ev_begin = nullptr, cudaEvent_t ev_mid = nullptr, cudaEvent_t ev_end = nullptr) {
-  const int tile = plan_tile(m, n);
-  if (tile < 0) return fail(OBT_E_UNSUPPORTED, "%d features do not fit a 128-object tile", m->n_features);
-  const size_t need = workspace_bytes(m, n, tile);
+  const Regions reg = plan_regions(m, n, idx_out == nullptr);
+  if (reg.tile[0] < 0) return fail(OBT_E_UNSUPPORTED, "%d features do not fit a 128-object tile", m->n_features);
+  const size_t need = regions_workspace(m, reg);
   uint8_t* q = static_cast<uint8_t*>(ws);
   bool owned = false;
   // bucket tiles move by TMA bulk copies (16-byte aligned); predictions are doubles
@@ -935,17 +986,30 @@ static int predict_impl(obt_model* m, const float* x, int64_t n, int32_t layout,
     CUDA_TRY(pool_alloc(reinterpret_cast<void**>(&q), need, m->device, stream));
     owned = true;
   }
-  const int64_t n_slots = ((n + tile - 1) / tile) * (int64_t)tile;
+  // one quantize launch writes both regions' bucket tiles (each laid out for its tile
+  // size and lanes per word), then one apply launch per region
+  uint8_t* qr[2] = {q, q + workspace_bytes(m, reg.count[0], reg.tile[0])};
+  int tpw[2] = {1, 1};
+  for (int i = 0; i < reg.n_reg; ++i) tpw[i] = apply_lanes(m, reg.tile[i], idx_out != nullptr);
   if (ev_begin) CUDA_TRY(cudaEventRecord(ev_begin, stream));
-  const int tpw = apply_lanes(m, tile, idx_out != nullptr);
-  int rc = launch_quantize(m, x, n, layout, q, true, tile, n_slots, tpw > 1, stream);
+  SecondRegion r2;
+  int64_t n_slots = ((reg.count[0] + reg.tile[0] - 1) / reg.tile[0]) * (int64_t)reg.tile[0];
+  if (reg.n_reg == 2) {
+    r2.split = reg.count[0];  // whole waves of whole tiles: a multiple of 128
+    r2.out = qr[1];
+    r2.tile = reg.tile[1];
+    r2.swizzle = tpw[1] > 1;
+    n_slots += ((reg.count[1] + reg.tile[1] - 1) / reg.tile[1]) * (int64_t)reg.tile[1];
+  }
+  int rc = launch_quantize(m, x, n, layout, q, true, reg.tile[0], n_slots, tpw[0] > 1, stream, r2);
   if (rc == OBT_OK && ev_mid) CUDA_TRY(cudaEventRecord(ev_mid, stream));
-  if (rc == OBT_OK) {
+  for (int i = 0; i < reg.n_reg && rc == OBT_OK; ++i) {
+    const int64_t b = reg.begin[i], c = reg.count[i];
     if (m->n_outputs > 1) {
       rc = idx_out ? fail(OBT_E_UNSUPPORTED, "leaf-index dumps are implemented for single-output models")
-                   : launch_multi(m, q, n, out, stream);
+                   : launch_multi(m, qr[i], c, out + b * m->n_outputs, stream);
     } else {
-      rc = launch_apply(m, q, n, tile, tpw, out, idx_out, tree_begin, tree_end, stream);
+      rc = launch_apply(m, qr[i], c, reg.tile[i], tpw[i], out ? out + b : nullptr, idx_out, tree_begin, tree_end, stream);
     }
   }
   if (rc == OBT_OK && ev_end) CUDA_TRY(cudaEventRecord(ev_end, stream));

@@ -121,6 +121,12 @@ struct QuantizeParams {
   int32_t chunk_features;  // features per CTA (grid.y chunks), a multiple of 8
   int32_t two;             // the constant 2, passed at run time (see eytz_level)
   int32_t swizzle;         // tiled: odd feature rows XOR object byte offsets with 64 (K2s layout)
+  int64_t ld;              // feature-major: row pitch in objects (>= n; a batch may be a column range)
+  // tiled output in two regions: objects >= split (a multiple of 128) go to out2 in tiles
+  // of tile2 with swizzle2 (the tail-wave region of predict_impl); split = n_slots if none
+  int64_t split;
+  uint8_t* out2;
+  int32_t tile2, swizzle2;
 };
 
 constexpr int kQuantObjects = 128;    // tile quantum: a quantize warp's 128 objects never straddle tiles
@@ -249,8 +255,12 @@ __device__ __forceinline__ void quantize_step(const QuantizeParams& p, const flo
     }
     const int f = f0 + fq + j;
     if (TILED) {
-      const int64_t t = base / p.tile, w = (base - t * p.tile + 4 * lane) ^ ((p.swizzle && (f & 1)) ? 64 : 0);
-      *reinterpret_cast<uint32_t*>(p.out + (t * F + f) * (int64_t)p.tile + w) = word;
+      const bool second = base >= p.split;  // warp-uniform: blocks never straddle the split
+      const int64_t rb = second ? base - p.split : base;
+      const int64_t tl = second ? p.tile2 : p.tile;
+      const bool sw = (second ? p.swizzle2 : p.swizzle) && (f & 1);
+      const int64_t t = rb / tl, w = (rb - t * tl + 4 * lane) ^ (sw ? 64 : 0);
+      *reinterpret_cast<uint32_t*>((second ? p.out2 : p.out) + (t * F + f) * tl + w) = word;
     } else {
 #pragma unroll
       for (int k = 0; k < 4; ++k)
@@ -323,7 +333,7 @@ __global__ void __launch_bounds__(kQuantThreads, 2) quantize_kernel(QuantizePara
 #pragma unroll
         for (int j = 0; j < S; ++j)
 #pragma unroll
-          for (int k = 0; k < 4; ++k) v[j][k] = __ldg(p.x + (int64_t)(f0 + fq + j) * p.n + ob + 32 * k);
+          for (int k = 0; k < 4; ++k) v[j][k] = __ldg(p.x + (int64_t)(f0 + fq + j) * p.ld + ob + 32 * k);
       }
     } else {
 #pragma unroll
@@ -331,7 +341,7 @@ __global__ void __launch_bounds__(kQuantThreads, 2) quantize_kernel(QuantizePara
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const bool in = ob + 32 * k < p.n && fq + j < nf;
-          const int64_t idx = LAYOUT == 0 ? (ob + 32 * k) * F + f0 + fq + j : (int64_t)(f0 + fq + j) * p.n + ob + 32 * k;
+          const int64_t idx = LAYOUT == 0 ? (ob + 32 * k) * F + f0 + fq + j : (int64_t)(f0 + fq + j) * p.ld + ob + 32 * k;
           v[j][k] = in ? __ldg(p.x + idx) : 0.0f;
         }
     }

@@ -455,3 +455,22 @@ def test_misaligned_workspace_and_output_rejected():
                              _native.current_stream_handle())
     assert rc == _native.OBT_E_INVALID and b"8-byte aligned" in lib.obt_last_error()
     ev.predict_device(x, workspace=ws[:ev.workspace_bytes(300)])  # aligned: fine
+
+
+@pytest.mark.parametrize("D", [6, 8])
+@pytest.mark.parametrize("layout", [obt.Layout.OBJECT_MAJOR, obt.Layout.FEATURE_MAJOR])
+def test_tail_wave_split_bit_exact(monkeypatch, D, layout):
+    """Batches past one full wave run the partial last wave as a second region of
+    smaller tiles (F = 500: 384-object tiles, 148 per wave): bit-exact against the oracle
+    and against the single-region path, in both input layouts."""
+    model = _model(500, 64, 30, D, seed=D)
+    n = 70001
+    x = _features(model, n, seed=D + 1, specials=False)
+    want = oracle.evaluate_scalar(oracle.flatten(model), x)
+    ev = obt.Evaluator(model)
+    xin = x if layout is obt.Layout.OBJECT_MAJOR else np.ascontiguousarray(x.T)
+    xd = torch.from_numpy(xin).cuda()
+    got = ev.predict_device(xd, layout=layout).cpu().numpy()
+    assert np.array_equal(got, want)
+    monkeypatch.setenv("OBT_TAIL_SPLIT", "0")
+    assert np.array_equal(ev.predict_device(xd, layout=layout).cpu().numpy(), want)
