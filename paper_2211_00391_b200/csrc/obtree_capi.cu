@@ -58,7 +58,7 @@ constexpr int kMaxDepth = 12;     // smem-staged leaf tables (2^12 fp32 = 16 KiB
 constexpr int kSentinel = 255;    // evaluate.py:32
 constexpr int kStages = 3;        // records in flight in the apply kernel's ring
 constexpr int kMaxOutputs = 16;   // multi-output kernel instantiations
-constexpr int kMultiTile = 4 * obt::kMultiThreads;  // objects per multi-output CTA
+constexpr int kMultiTile = obt::kMultiTileObjects;  // objects per multi-output CTA
 
 // Instantiated depths of the apply kernel; a model of depth D runs on the
 // smallest instantiation >= D with sentinel (never-true) padding splits.

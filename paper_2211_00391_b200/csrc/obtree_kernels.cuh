@@ -926,7 +926,16 @@ struct MultiParams {
   double scale, bias;
 };
 
-constexpr int kMultiThreads = 128;  // 512 objects per CTA = one tile
+#ifndef OBT_MULTI_OPL
+#define OBT_MULTI_OPL 4
+#endif
+// Objects folded per lane: a bucket word's 4 objects are shared by 4 / kMultiOPL lanes
+// (each evaluates the word's indices and folds its share), trading duplicate index
+// work for fewer fp64 accumulators per thread and more resident warps.
+constexpr int kMultiOPL = OBT_MULTI_OPL;
+constexpr int kMultiLanesPerWord = 4 / kMultiOPL;
+constexpr int kMultiTileObjects = 512;                    // one tile per CTA: 128 bucket words
+constexpr int kMultiThreads = kMultiTileObjects / 4 * kMultiLanesPerWord;
 
 // Values per multi-output leaf record: fp32 records in 16-byte rows (48 bytes at C = 10;
 // 32-byte rows with 256-bit loads measured slower), fp64 records in 16-byte rows.
@@ -944,14 +953,15 @@ template <int DI, int CMP, int LEAF, int C>
 __global__ void __launch_bounds__(kMultiThreads) apply_multi_kernel(const __grid_constant__ MultiParams p) {
   using leaf_t = typename LeafT<LEAF>::T;
   constexpr int CP = multi_record_values(LEAF, C);  // record stride: 32-byte rows (fp32), 16-byte (fp64)
-  const int word = threadIdx.x;
+  constexpr int OPL = kMultiOPL;
+  const int word = threadIdx.x / kMultiLanesPerWord, sub = threadIdx.x % kMultiLanesPerWord;
   const int64_t tile_idx = blockIdx.x;
   const uint8_t* qrow0 = p.q + tile_idx * (int64_t)p.n_features * p.tile + 4 * word;
   const int64_t tile_base = tile_idx * p.tile;
-  auto obj_of = [&](int k) { return word_object(tile_base, word, k); };
-  double acc[4][C];
+  auto obj_of = [&](int k) { return word_object(tile_base, word, sub * OPL + k); };  // k < OPL
+  double acc[OPL][C];
 #pragma unroll
-  for (int k = 0; k < 4; ++k)
+  for (int k = 0; k < OPL; ++k)
 #pragma unroll
     for (int c = 0; c < C; ++c)
       acc[k][c] = (p.first || obj_of(k) >= p.n) ? 0.0 : p.out[obj_of(k) * C + c];
@@ -988,10 +998,11 @@ __global__ void __launch_bounds__(kMultiThreads) apply_multi_kernel(const __grid
     if constexpr (LEAF == 1 && OBT_MULTI_ROW32) {
       // fp32 records: one 256-bit load per 32-byte row
       constexpr int kRows = (C + 7) / 8;
-      float rec[4][kRows * 8];
+      float rec[OPL][kRows * 8];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint32_t idx = ((lo >> (8 * k)) & 0xffu) | (DI > 8 ? ((hi >> (8 * k)) & 0xffu) << 8 : 0u);
+      for (int k = 0; k < OPL; ++k) {
+        const int kb = sub * OPL + k;  // byte of the word
+        const uint32_t idx = ((lo >> (8 * kb)) & 0xffu) | (DI > 8 ? ((hi >> (8 * kb)) & 0xffu) << 8 : 0u);
         const float* r = reinterpret_cast<const float*>(tab) + (size_t)idx * CP;
 #pragma unroll
         for (int i = 0; i < kRows; ++i) {
@@ -1002,21 +1013,22 @@ __global__ void __launch_bounds__(kMultiThreads) apply_multi_kernel(const __grid
         }
       }
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < OPL; ++k)
 #pragma unroll
         for (int c = 0; c < C; ++c) acc[k][c] += (double)rec[k][c];
     } else {
       constexpr int kRows = CP * (int)sizeof(leaf_t) / 16;
-      uint4 rec[4][kRows];
+      uint4 rec[OPL][kRows];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint32_t idx = ((lo >> (8 * k)) & 0xffu) | (DI > 8 ? ((hi >> (8 * k)) & 0xffu) << 8 : 0u);
+      for (int k = 0; k < OPL; ++k) {
+        const int kb = sub * OPL + k;  // byte of the word
+        const uint32_t idx = ((lo >> (8 * kb)) & 0xffu) | (DI > 8 ? ((hi >> (8 * kb)) & 0xffu) << 8 : 0u);
         const uint4* r = reinterpret_cast<const uint4*>(tab + (size_t)idx * CP);
 #pragma unroll
         for (int i = 0; i < kRows; ++i) rec[k][i] = __ldg(r + i);
       }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < OPL; ++k) {
         const leaf_t* v = reinterpret_cast<const leaf_t*>(rec[k]);
 #pragma unroll
         for (int c = 0; c < C; ++c) acc[k][c] += (double)v[c];
@@ -1024,7 +1036,7 @@ __global__ void __launch_bounds__(kMultiThreads) apply_multi_kernel(const __grid
     }
   }
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < OPL; ++k) {
     if (obj_of(k) >= p.n) continue;
 #pragma unroll
     for (int c = 0; c < C; ++c)
