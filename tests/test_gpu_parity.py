@@ -474,3 +474,57 @@ def test_tail_wave_split_bit_exact(monkeypatch, D, layout):
     assert np.array_equal(got, want)
     monkeypatch.setenv("OBT_TAIL_SPLIT", "0")
     assert np.array_equal(ev.predict_device(xd, layout=layout).cpu().numpy(), want)
+
+
+def test_config_invariance_within_precision_family():
+    """Every valid EvalConfig of a precision family gives the same bits (the reference's
+    layout/width/block/tail invariance, test_evaluate.py:172-213)."""
+    import itertools
+
+    from paper_2211_00391_b200.config import BLOCK_SIZES, TailPolicy, VectorWidth
+
+    model = _mixed_depth_model(19, 40, 70, seed=21)
+    x = _features(model, 777, seed=22)
+    fm = oracle.flatten(model)
+    want = {oracle.BINARY64: oracle.evaluate_scalar(fm, x, oracle.OBJECT_MAJOR, oracle.BINARY64),
+            oracle.BINARY16: oracle.evaluate_scalar(fm, x, oracle.OBJECT_MAJOR, oracle.BINARY16)}
+    checked = 0
+    for strategy, width, block, tail in itertools.product(obt.LeafStrategy, VectorWidth, BLOCK_SIZES, TailPolicy):
+        cfg = obt.EvalConfig(block_size=block, width=width, strategy=strategy, tail_policy=tail)
+        try:
+            cfg.validate()
+        except ValueError:
+            continue
+        prec = oracle.BINARY16 if strategy.precision.value == "binary16" else oracle.BINARY64
+        got = obt.Evaluator(model, cfg).predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
+        assert np.array_equal(got, want[prec]), cfg.describe()
+        checked += 1
+    assert checked >= 10
+
+
+def test_prediction_is_the_composition_of_the_stages():
+    """Fused = unit composition (test_evaluate.py:271-300): GPU leaf indices folded on the
+    host in tree order with the bank's leaves, then scale/bias, equal the GPU prediction."""
+    model = _mixed_depth_model(23, 50, 64, seed=31)
+    x = _features(model, 1500, seed=32)
+    idx = stages.as_uint16(stages.leaf_indices(model, torch.from_numpy(x).cuda())).astype(np.int64)
+    acc = np.zeros(x.shape[0])
+    for t, tree in enumerate(model.trees):
+        acc = acc + np.asarray(tree.leaf_values, dtype=np.float64)[idx[t]]
+    want = acc * model.scale + model.bias
+    got = obt.Evaluator(model).predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
+    assert np.array_equal(got, want)
+
+
+def test_fp16_family_within_reference_bound():
+    """FP16 leaves vs binary64 leaves on the GPU: |p16 - p64| <= |scale| T max|leaf| 2^-10
+    (test_acceptance.py:156, 240-247), and the binary16 family matches its oracle exactly."""
+    model = _model(40, 64, 300, 6, seed=41, sigma=0.05)
+    x = _features(model, 4000, seed=42)
+    fmx = obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR)
+    p64 = obt.Evaluator(model, obt.EvalConfig(strategy=obt.LeafStrategy.NAIVE)).predict(fmx)
+    p16 = obt.Evaluator(model, obt.EvalConfig(strategy=obt.LeafStrategy.NAIVE16)).predict(fmx)
+    max_leaf = max(float(np.abs(t.leaf_values).max()) for t in model.trees)
+    bound = abs(model.scale) * model.n_trees * max_leaf * 2.0 ** -10
+    assert float(np.abs(p16 - p64).max()) <= bound
+    assert np.array_equal(p16, oracle.evaluate_scalar(oracle.flatten(model), x, oracle.OBJECT_MAJOR, oracle.BINARY16))
