@@ -56,7 +56,10 @@ int fail(int code, const char* fmt, ...) {
 constexpr int kMaxBorders = 254;  // model.py:21
 constexpr int kMaxDepth = 12;     // smem-staged leaf tables (2^12 fp32 = 16 KiB per tree)
 constexpr int kSentinel = 255;    // evaluate.py:32
-constexpr int kStages = 3;        // records in flight in the apply kernel's ring
+#ifndef OBT_STAGES
+#define OBT_STAGES 2
+#endif
+constexpr int kStages = OBT_STAGES;  // records in flight in the apply kernel's ring
 constexpr int kMaxOutputs = 16;   // multi-output kernel instantiations
 constexpr int kMultiTile = obt::kMultiTileObjects;  // objects per multi-output CTA
 

@@ -475,7 +475,10 @@ __global__ void __launch_bounds__(kQTThreads, 2) quantize_tma_kernel(const __gri
 #ifndef OBT_GROUP_SHALLOW
 #define OBT_GROUP_SHALLOW 16
 #endif
-__host__ __device__ constexpr int tree_group(int di) { return di <= 6 ? OBT_GROUP_SHALLOW : di <= 8 ? 8 : 4; }
+#ifndef OBT_GROUP_D8
+#define OBT_GROUP_D8 16
+#endif
+__host__ __device__ constexpr int tree_group(int di) { return di <= 6 ? OBT_GROUP_SHALLOW : di <= 8 ? OBT_GROUP_D8 : 4; }
 #ifndef OBT_PACKED_DESC
 #define OBT_PACKED_DESC 0
 #endif
