@@ -473,10 +473,10 @@ __global__ void __launch_bounds__(kQTThreads, 2) quantize_tma_kernel(const __gri
 // trees (larger leaf tables) use groups of 8 / 4 so a chunk still fits the ring without
 // shrinking the bucket tile.
 #ifndef OBT_GROUP_SHALLOW
-#define OBT_GROUP_SHALLOW 16
+#define OBT_GROUP_SHALLOW 32
 #endif
 #ifndef OBT_GROUP_D8
-#define OBT_GROUP_D8 16
+#define OBT_GROUP_D8 32
 #endif
 __host__ __device__ constexpr int tree_group(int di) { return di <= 6 ? OBT_GROUP_SHALLOW : di <= 8 ? OBT_GROUP_D8 : 4; }
 #ifndef OBT_PACKED_DESC
@@ -583,7 +583,9 @@ constexpr int kApplyMaxThreads = OBT_APPLY_MAXT;  // 16 consumer warps + the pro
 template <int DI, int CMP, int LEAF, bool WRITE_IDX, int W, int DSRC>
 __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid_constant__ ApplyArgs<DSRC> args) {
   const ApplyParams& p = args.p;
-  constexpr int kTreeGroup = tree_group(DI);
+  // index dumps and 8-object threads keep more live values per tree: smaller unrolled
+  // groups (chunks hold multiples of tree_group(DI), so any divisor tiles them)
+  constexpr int kTreeGroup = (WRITE_IDX || W == 2) ? (tree_group(DI) < 8 ? tree_group(DI) : 8) : tree_group(DI);
   using LT = LeafT<LEAF>;
   using acc_t = typename LT::Acc;
   constexpr int kDW = desc_words(CMP);
