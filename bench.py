@@ -329,8 +329,29 @@ def run_ours(args, world, rank, local):
 
     stream = _native.current_stream_handle(device)
     K = args.steps
-    marks = [[_native.Event(), _native.Event(), _native.Event()] for _ in range(K)]
     t_start, t_end = _native.Event(), _native.Event()
+    # launch-bound steps (cfg1: ~30 us of kernels) replay a CUDA graph of one predict, so
+    # the number is the GPU's, not the host's launch rate
+    t_start.record(stream)
+    ev.predict_device(x, out=out, workspace=ws)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    one_ms = t_start.elapsed_ms(t_end)
+    use_graph = not tree_sharded and (args.graph == "on" or (args.graph == "auto" and one_ms < 0.2))
+    graph, graph_launches = None, 0
+    if use_graph:
+        gs = torch.cuda.Stream(device)
+        gs.wait_stream(torch.cuda.current_stream(device))
+        with torch.cuda.stream(gs):
+            ev.predict_device(x, out=out, workspace=ws)
+        gs.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=gs):
+            ev.predict_device(x, out=out, workspace=ws)
+        graph_launches = ev.last_launch_count()
+        graph.replay()
+        torch.cuda.synchronize()
+    marks = [[_native.Event(), _native.Event(), _native.Event()] for _ in range(K if graph is None else min(K, 20))]
     clocks = ClockSampler(device)
     clocks.start()
     time.sleep(0.15)
@@ -340,6 +361,10 @@ def run_ours(args, world, rank, local):
     t_start.record(stream)
     launches = 0
     for k in range(K):
+        if graph is not None:
+            graph.replay()
+            launches += graph_launches
+            continue
         ev.predict_device_marked(x, marks[k], out=out, workspace=ws)
         launches += ev.last_launch_count()
         if tree_sharded:
@@ -350,8 +375,13 @@ def run_ours(args, world, rank, local):
     barrier(world)
     clk = clocks.stop(w0, w1)
     elapsed_ms = max_over_ranks(t_start.elapsed_ms(t_end), world)
-    q_ms = sum(m[0].elapsed_ms(m[1]) for m in marks) / K
-    a_ms = sum(m[1].elapsed_ms(m[2]) for m in marks) / K
+    if graph is not None:
+        # per-kernel split from marked stream launches after the timed region
+        for m in marks:
+            ev.predict_device_marked(x, m, out=out, workspace=ws)
+        torch.cuda.synchronize()
+    q_ms = sum(m[0].elapsed_ms(m[1]) for m in marks) / len(marks)
+    a_ms = sum(m[1].elapsed_ms(m[2]) for m in marks) / len(marks)
     step_s = elapsed_ms / K / 1e3
     # object sharding: every rank folds all trees for its own N objects; tree sharding
     # (config 5): every rank folds its share of the trees for the same N objects
@@ -409,7 +439,8 @@ def run_ours(args, world, rank, local):
                    "leaves": "fp16 (binary32 fold)" if spec.half_leaves else "fp32 values (binary64 fold)",
                    "leaf_storage_on_device": ev.leaf_storage,
                    "l2": "inputs larger than L2 (features 4NF bytes, buckets NF bytes > 126 MB)",
-                   "parallelism": f"objects sharded over {world} GPU(s), no data-path collective"},
+                   "parallelism": f"objects sharded over {world} GPU(s), no data-path collective",
+                   "launch": "CUDA graph replay of one predict" if graph is not None else "stream launches"},
         "e2e": e2e,
         "gpu_launches": launches,
         "roofline": {
@@ -455,6 +486,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--ref-sample", type=int, default=65536)
+    ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
+                    help="replay a CUDA graph of one predict (auto: when a step is under 0.2 ms)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

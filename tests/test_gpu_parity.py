@@ -528,3 +528,30 @@ def test_fp16_family_within_reference_bound():
     bound = abs(model.scale) * model.n_trees * max_leaf * 2.0 ** -10
     assert float(np.abs(p16 - p64).max()) <= bound
     assert np.array_equal(p16, oracle.evaluate_scalar(oracle.flatten(model), x, oracle.OBJECT_MAJOR, oracle.BINARY16))
+
+
+def test_predict_captures_into_cuda_graph():
+    """predict_device is capturable (stream-ordered allocations, by-value tensor map,
+    plans built at warm-up): a CUDA graph replay is bit-exact and tracks new inputs."""
+    model = _model(24, 40, 120, 6, seed=61)
+    x1 = _features(model, 5000, seed=62)
+    x2 = _features(model, 5000, seed=63)
+    fm = oracle.flatten(model)
+    ev = obt.Evaluator(model)
+    xd = torch.from_numpy(x1).cuda()
+    out = torch.empty(5000, dtype=torch.float64, device="cuda")
+    ws = torch.empty(ev.workspace_bytes(5000), dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ev.predict_device(xd, out=out, workspace=ws)  # warm-up: tile plans, attributes
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        ev.predict_device(xd, out=out, workspace=ws)
+    g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), oracle.evaluate_scalar(fm, x1))
+    xd.copy_(torch.from_numpy(x2))
+    g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), oracle.evaluate_scalar(fm, x2))
