@@ -1143,6 +1143,29 @@ int obt_predict_host(const obt_model* mc, const float* x_host, int64_t n, int32_
     if (bounds.back() != n) bounds.push_back(n);
   }
   const int64_t n_chunks = (int64_t)bounds.size() - 1;
+  if (n_chunks == 1) {
+    // one chunk: nothing to overlap -- copy in, predict and copy out on `stream`
+    float* xd = nullptr;
+    double* od = nullptr;
+    rc = OBT_OK;
+    auto ok = [&](cudaError_t e, const char* what) {
+      if (e != cudaSuccess && rc == OBT_OK) rc = fail(OBT_E_CUDA, "%s failed: %s", what, cudaGetErrorString(e));
+      return rc == OBT_OK;
+    };
+    if (ok(pool_alloc(reinterpret_cast<void**>(&xd), (size_t)n * F * 4, m->device, stream), "feature buffer") &&
+        ok(pool_alloc(reinterpret_cast<void**>(&od), (size_t)n * C * 8, m->device, stream), "score buffer") &&
+        ok(cudaMemcpyAsync(xd, x_host, (size_t)n * F * 4, cudaMemcpyHostToDevice, stream), "H2D")) {
+      rc = predict_impl(m, xd, n, layout, od, nullptr, 0, 0, nullptr, 0, stream);
+      if (rc == OBT_OK) ok(cudaMemcpyAsync(out_host, od, (size_t)n * C * 8, cudaMemcpyDeviceToHost, stream), "D2H");
+    }
+    const int launches = g_launches;
+    if (xd) cudaFreeAsync(xd, stream);
+    if (od) cudaFreeAsync(od, stream);
+    const cudaError_t e = cudaStreamSynchronize(stream);
+    if (rc == OBT_OK && e != cudaSuccess) rc = fail(OBT_E_CUDA, "stream synchronize failed: %s", cudaGetErrorString(e));
+    g_launches = launches;
+    return rc;
+  }
   const int nbuf = n_chunks > 1 ? 2 : 1;
   float* x_dev[2] = {nullptr, nullptr};
   double* out_dev[2] = {nullptr, nullptr};
