@@ -80,7 +80,7 @@ struct BorderTable {
 
 struct TilePlan {
   uint8_t* d_chunks = nullptr;          // [n_chunks][chunk_bytes] descriptor + leaf records
-  std::vector<uint32_t> param_desc;     // [padded_trees][words per tree] for the parameter bank
+  std::vector<uint32_t> param_desc;     // [padded_trees][DI][2] {off, k replicated} for the parameter bank
 };
 
 }  // namespace
@@ -421,11 +421,8 @@ int get_tile_plan(obt_model* m, int tile, int variant, const TilePlan** out) {
 // Tiles are whole multiples of the quantize kernel's 256-object CTA, so a CTA never
 // straddles two tiles; the apply kernel runs tile / 4 consumer threads + 1 producer warp.
 constexpr int kTileQuantum = obt::kQuantObjects;
-// The parameter-bank descriptor path (no shared-memory traffic for descriptors, one
-// bucket-tile re-read per extra launch) measured ~30% slower per tree than the
-// shared-memory path on B200 (register-indexed LDC chains + unpack ALU ops; see
-// profiles/r01), so it is opt-in (OBT_DESC_SOURCE=param) until that changes.
-constexpr int kMaxParamLaunches = 0;
+// The parameter-bank descriptor path re-reads the bucket tile once per extra launch.
+constexpr int kMaxParamLaunches = 4;
 
 // Largest tile (multiple of 256 objects) whose bucket tile fits next to the stage ring;
 // then shrink for small batches so the grid still covers the SMs.
@@ -444,16 +441,20 @@ int plan_tile(const obt_model* m, int64_t n) {
   return (int)std::min(tmax, want);
 }
 
-// Chunks one parameter-bank launch can cover.
+// Chunks one parameter-bank launch can cover (two words per split).
 int param_chunks_per_launch(const obt_model* m) {
   const int words_per_chunk = 2 * m->depth_inst * m->chunk_trees;
   return obt::kParamDescWords / words_per_chunk;
 }
 
-int use_param_descriptors(const obt_model* m) {
+// Parameter-bank descriptors (no descriptor wavefronts: uniform constant loads) for a
+// region whose words have one lane each; the 7-bit compare only.  Measured on B200
+// (cfg2): 13% faster per tree in one launch, still 4% faster split over 4 launches, so
+// they are the default up to kMaxParamLaunches launches.
+int use_param_descriptors(const obt_model* m, int tpw) {
   const char* e = getenv("OBT_DESC_SOURCE");  // tuning override: "smem" or "param"
   if (e && !strcmp(e, "smem")) return 0;
-  if (m->compare_mode != 7) return 0;
+  if (m->compare_mode != 7 || tpw != 1) return 0;
   const int per = param_chunks_per_launch(m);
   if (per < 1) return 0;
   if (e && !strcmp(e, "param")) return 1;
@@ -465,8 +466,8 @@ int use_param_descriptors(const obt_model* m) {
 // Lanes per bucket word (measured on B200): depth-split lanes add descriptor and shuffle
 // traffic to the shared-memory pipe, so they pay only when the tile -- F bytes per
 // object -- leaves few warps (F = 500: 2 lanes); subject to TPW | depth.  OBT_TPW overrides.
-int choose_tpw(const obt_model* m, int tile, bool write_idx, int dsrc) {
-  if (write_idx || dsrc || m->depth_inst > 8) return 1;
+int choose_tpw(const obt_model* m, int tile, bool write_idx) {
+  if (write_idx || m->depth_inst > 8) return 1;
   const int words = tile / 4;
   const int cap = obt::kApplyMaxThreads - obt::kApplyProducerThreads;
   const char* e = getenv("OBT_TPW");
@@ -484,7 +485,9 @@ int choose_tpw(const obt_model* m, int tile, bool write_idx, int dsrc) {
 // buckets out for it).
 int apply_lanes(const obt_model* m, int tile, bool write_idx) {
   if (m->n_outputs > 1) return 1;
-  return choose_tpw(m, tile, write_idx, use_param_descriptors(m));
+  const char* e = getenv("OBT_DESC_SOURCE");
+  if (e && !strcmp(e, "param")) return 1;  // the parameter-bank kernels have one lane per word
+  return choose_tpw(m, tile, write_idx);
 }
 
 // Features per CTA (grid.y chunk): the fewest chunks whose Eytzinger arrays fit
@@ -619,7 +622,7 @@ int launch_quantize(const obt_model* m, const float* x, int64_t n, int layout, u
 int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, int tpw, double* out, uint16_t* idx_out,
                  int tree_begin, int tree_end, cudaStream_t stream) {
   const bool write_idx = idx_out != nullptr;
-  const int dsrc = use_param_descriptors(m);
+  const int dsrc = use_param_descriptors(m, tpw);
   const TilePlan* tp = nullptr;
   int rc = get_tile_plan(m, tile, tpw > 1 ? 1 : 0, &tp);
   if (rc != OBT_OK) return rc;

@@ -668,9 +668,9 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid
           dw[4 * v + 0] = q4.x; dw[4 * v + 1] = q4.y; dw[4 * v + 2] = q4.z; dw[4 * v + 3] = q4.w;
         }
       }
-      // parameter-bank descriptors of this group: {off, k replicated} word pairs; the
-      // index is a function of uniform loop counters only, so they load as LDCU.64 and
-      // feed LDS [R + UR] and IADD R, UR directly
+      // parameter-bank descriptors of this group: {off, k replicated} word pairs (LDC.64
+      // broadcasts from the constant bank, no shared-memory wavefronts; a packed 4-byte
+      // form measured slower: its unpack runs on the vector ALU)
       const int gbase = (c * (p.chunk_trees / kTreeGroup) + g) * (kTreeGroup * DI * 2);
 #pragma unroll
       for (int tt = 0; tt < kTreeGroup; ++tt) {
