@@ -40,6 +40,15 @@ FALLBACK_HBM_GBS = 6650.0
 FALLBACK_SM_MHZ = 1965.0
 
 
+def quantize_search(ev) -> str:
+    """The predict path's quantize search: cells(k) = cell-table kernel with k compares
+    per value, eytzinger(L) = L-level search."""
+    if not hasattr(ev, "quantize_kernel"):
+        return "n/a"
+    kind, param = ev.quantize_kernel()
+    return f"{kind}({param})"
+
+
 def peaks() -> dict:
     path = ROOT / "MEASURED_PEAKS.json"
     if path.exists():
@@ -438,6 +447,7 @@ def run_ours(args, world, rank, local):
                    "borders": spec.borders, "trees": spec.n_trees, "depth": spec.depth,
                    "leaves": "fp16 (binary32 fold)" if spec.half_leaves else "fp32 values (binary64 fold)",
                    "leaf_storage_on_device": ev.leaf_storage,
+                   "quantize_search": quantize_search(ev),
                    "l2": "inputs larger than L2 (features 4NF bytes, buckets NF bytes > 126 MB)",
                    "parallelism": f"objects sharded over {world} GPU(s), no data-path collective",
                    "launch": "CUDA graph replay of one predict" if graph is not None else "stream launches"},

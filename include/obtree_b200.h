@@ -86,6 +86,13 @@ int obt_model_info(const obt_model* model, int32_t* n_features, int32_t* n_trees
                    int32_t* max_depth, int32_t* n_outputs, int32_t* precision,
                    int32_t* leaf_storage, int32_t* compare_mode);
 
+/* Which quantize search the predict path runs for TMA-eligible inputs (object-major,
+ * F % 4 == 0, 16-byte aligned): kind 1 = cell tables (K1L) with `param` compares per
+ * value, kind 0 = Eytzinger search (K1t) with `param` levels.  Diagnostics for tests
+ * and tuning; no reference counterpart (the reference always counts every border,
+ * quantize.py:171). */
+int obt_model_quantize_kernel(const obt_model* model, int32_t* kind, int32_t* param);
+
 /* Bytes of scratch obt_predict_dev needs for n objects (the blocked bucket matrix). */
 int obt_workspace_size(const obt_model* model, int64_t n_objects, size_t* bytes);
 

@@ -33,6 +33,7 @@ EXPORTED_SYMBOLS = (
     "obt_model_create",
     "obt_model_destroy",
     "obt_model_info",
+    "obt_model_quantize_kernel",
     "obt_workspace_size",
     "obt_predict_dev",
     "obt_predict_host",
@@ -105,6 +106,7 @@ def load_library() -> ctypes.CDLL:
         "obt_model_create": (ctypes.c_int, [ctypes.POINTER(ModelDesc), ctypes.c_int, ctypes.POINTER(vp)]),
         "obt_model_destroy": (ctypes.c_int, [vp]),
         "obt_model_info": (ctypes.c_int, [vp, p_i32, p_i32, p_i32, p_i32, p_i32, p_i32, p_i32]),
+        "obt_model_quantize_kernel": (ctypes.c_int, [vp, p_i32, p_i32]),
         "obt_workspace_size": (ctypes.c_int, [vp, i64, ctypes.POINTER(sz)]),
         "obt_predict_dev": (ctypes.c_int, [vp, vp, i64, i32, vp, vp, sz, vp]),
         "obt_predict_host": (ctypes.c_int, [vp, vp, i64, i32, vp, vp]),

@@ -18,6 +18,8 @@ struct ApplyKernel {
 // K1, levels 0..8
 QuantFn pick_quant(int levels, int layout, bool tiled);
 QuantTmaFn pick_quant_tma(int levels);
+// K1L, cell-table quantize with kmax (1..4) compares per value
+QuantTmaFn pick_quant_lut(int kmax);
 // K2, depths {1..8, 10, 12}
 ApplyKernel pick_apply(int di, int cmp, int leaf, bool write_idx, int dsrc);
 // K2s, depth-split (tpw 2: depths 2/4/6/8, tpw 4: depths 4/8)
@@ -26,5 +28,8 @@ ApplyKernel pick_split(int di, int cmp, int leaf, int tpw);
 // capacity it was instantiated for through *di_out / *c_out
 const void* pick_multi(int di, int cmp, int leaf, int c, int* di_out);
 int multi_depth(int d);
+// K4s sliced multi-output (same depths / outputs); record slot bytes for leaf storage
+const void* pick_multi_slice(int di, int cmp, int leaf, int c, int* di_out);
+int multi_slice_slot(int leaf, int c);
 
 }  // namespace obt

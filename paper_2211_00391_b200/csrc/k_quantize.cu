@@ -1,4 +1,4 @@
-// k_quantize.cu -- instantiations of K1 (quantize_kernel) for 0..8 search levels.
+// k_quantize.cu -- instantiations of K1 / K1t (0..8 search levels) and K1L (1..4 cell compares).
 #include "dispatch.h"
 
 namespace obt {
@@ -35,6 +35,16 @@ QuantTmaFn pick_quant_tma(int levels) {
     case 6: return quantize_tma_kernel<6>;
     case 7: return quantize_tma_kernel<7>;
     case 8: return quantize_tma_kernel<8>;
+    default: return nullptr;
+  }
+}
+
+QuantTmaFn pick_quant_lut(int kmax) {
+  switch (kmax) {
+    case 1: return quantize_lut_kernel<1>;
+    case 2: return quantize_lut_kernel<2>;
+    case 3: return quantize_lut_kernel<3>;
+    case 4: return quantize_lut_kernel<4>;
     default: return nullptr;
   }
 }

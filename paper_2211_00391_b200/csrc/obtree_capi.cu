@@ -28,6 +28,7 @@ using obt::QuantFn;
 using obt::pick_apply;
 using obt::pick_quant;
 using obt::pick_quant_tma;
+using obt::pick_quant_lut;
 using obt::pick_split;
 
 namespace {
@@ -78,6 +79,16 @@ struct BorderTable {
   int pitch = 1;
 };
 
+// K1L cell tables of a border set (see quantize_lut_kernel): kmax = 0 when the set
+// needs more than kLutMaxCompares compares in some cell (the Eytzinger K1t runs then).
+struct LutTable {
+  uint8_t* d_lut = nullptr;        // [F][256]
+  unsigned char* d_rec = nullptr;  // [F][rec_stride]
+  int rec_stride = 0;
+  int kmax = 0;
+};
+constexpr int kLutMaxCompares = 4;
+
 struct TilePlan {
   uint8_t* d_chunks = nullptr;          // [n_chunks][chunk_bytes] descriptor + leaf records
   std::vector<uint32_t> param_desc;     // [padded_trees][DI][2] {off, k replicated} for the parameter bank
@@ -94,7 +105,10 @@ struct obt_model {
   int compare_mode = 7;      // 7: all buckets < 128; 8: full byte compare
   BorderTable full;          // every border: obt_quantize_dev (reference buckets)
   BorderTable used;          // borders referenced by splits: the predict path
-  void* d_multi_leaves = nullptr;   // multi-output records [T][2^DI][CP]
+  LutTable used_lut;         // cell tables of `used` (K1L), kmax 0 if not applicable
+  void* d_multi_leaves = nullptr;   // multi-output records [T][2^DI][CP] (K4) or [T][2^DI] slots (K4s)
+  int multi_slice = 0;              // 1: sliced kernel K4s with multi_slot-byte record slots
+  int multi_slot = 0;
   uint32_t* d_multi_desc = nullptr; // multi-output descriptors [T][DI][2] for kMultiTile
   double scale = 1.0, bias = 0.0;
   // host copies used to (re)build descriptor records for a tile size
@@ -116,6 +130,8 @@ struct obt_model {
     if (d_multi_leaves) cudaFree(d_multi_leaves);
     if (d_multi_desc) cudaFree(d_multi_desc);
     if (used.d) cudaFree(used.d);
+    if (used_lut.d_lut) cudaFree(used_lut.d_lut);
+    if (used_lut.d_rec) cudaFree(used_lut.d_rec);
   }
 };
 
@@ -181,6 +197,87 @@ int build_border_table(const float* borders, const int32_t* counts, int F, int s
   }
   CUDA_TRY(cudaMalloc(&out.d, eytz.size() * sizeof(float)));
   CUDA_TRY(cudaMemcpy(out.d, eytz.data(), eytz.size() * sizeof(float), cudaMemcpyHostToDevice));
+  return OBT_OK;
+}
+
+// Cell tables for K1L.  Per feature (borders b_0 < ... < b_{U-1}): lo = b_0, hi = b_{U-1},
+// s ~ 254 / (hi - lo), o = 1.5 * 2^23 - lo * s (+ nudges), checked with the device's own
+// fp32 operations (fmaxf / fminf / fmaf, correctly rounded on both sides) so that every
+// clamped x maps into [1.5 * 2^23, 1.5 * 2^23 + 255]; then cell c_k of each border,
+// lut[c] = #{k : c_k < c}, and K = the most borders sharing a cell.  Returns kmax = 0
+// (not applicable) if a feature needs more than kLutMaxCompares compares or its range
+// does not fit the map.
+int build_lut_table(const float* borders, const int32_t* counts, int F, int stride, LutTable& out) {
+  const float M = 12582912.0f;  // 1.5 * 2^23: floats in [2^23, 2^24) step by 1
+  uint32_t mbits;
+  std::memcpy(&mbits, &M, 4);
+  int umax = 0;
+  for (int f = 0; f < F; ++f) umax = std::max(umax, (int)counts[f]);
+  const int P = (umax + 1 + 3) / 4 * 4;  // borders + one +inf pad (index U is read)
+  out.rec_stride = obt::kLutRecHeader + 4 * P;
+  out.kmax = 0;
+  std::vector<uint8_t> lut((size_t)F * obt::kLutCells, 0);
+  std::vector<unsigned char> rec((size_t)F * out.rec_stride, 0);
+  auto cell_of = [&](float x, float lo, float hi, float sc, float of) -> long {
+    const float y = fmaf(fminf(fmaxf(x, lo), hi), sc, of);
+    uint32_t yb;
+    std::memcpy(&yb, &y, 4);
+    if (!(y >= 8388608.0f && y < 16777216.0f)) return -1;
+    return (long)yb - (long)mbits;
+  };
+  int kmax = 1;
+  for (int f = 0; f < F; ++f) {
+    const int U = counts[f];
+    const float* b = borders + (size_t)f * stride;
+    float lo = 0.0f, hi = 0.0f, sc = 0.0f, of = M;
+    if (U >= 2) {
+      lo = b[0];
+      hi = b[U - 1];
+      const double span = (double)hi - (double)lo;
+      sc = (float)(254.0 / span);
+      if (!(span > 0) || !std::isfinite(sc) || !(sc > 0)) return OBT_OK;
+      const double o0 = (double)M - (double)lo * (double)sc;
+      if (!(o0 > 8388608.0 + 512 && o0 < 16777216.0 - 512)) return OBT_OK;
+      of = (float)std::floor(o0);
+      bool ok = false;
+      for (int it = 0; it < 8; ++it) {
+        const long clo = cell_of(lo, lo, hi, sc, of), chi = cell_of(hi, lo, hi, sc, of);
+        if (clo < 0) { of += 1.0f; continue; }
+        if (chi > 255) { of -= 1.0f; continue; }
+        ok = clo >= 0 && chi <= 255;
+        break;
+      }
+      if (!ok) return OBT_OK;
+    } else if (U == 1) {
+      lo = hi = b[0];
+    }
+    // cells of the borders, lower-bound table, compares needed
+    std::vector<int> per_cell(obt::kLutCells, 0);
+    std::vector<long> cells(U);
+    for (int k = 0; k < U; ++k) {
+      const long c = cell_of(b[k], lo, hi, sc, of);
+      if (c < 0 || c > 255 || (k > 0 && c < cells[k - 1])) return OBT_OK;  // must be monotone
+      cells[k] = c;
+      ++per_cell[c];
+    }
+    int kf = 0;
+    for (int c = 0, below = 0; c < obt::kLutCells; ++c) {
+      lut[(size_t)f * obt::kLutCells + c] = (uint8_t)below;
+      below += per_cell[c];
+      kf = std::max(kf, per_cell[c]);
+    }
+    if (kf > kLutMaxCompares) return OBT_OK;
+    kmax = std::max(kmax, kf);
+    float* r = reinterpret_cast<float*>(rec.data() + (size_t)f * out.rec_stride);
+    r[0] = lo; r[1] = hi; r[2] = sc; r[3] = of;
+    float* bd = r + obt::kLutRecHeader / 4;
+    for (int k = 0; k < P; ++k) bd[k] = k < U ? b[k] : INFINITY;
+  }
+  CUDA_TRY(cudaMalloc(&out.d_lut, lut.size()));
+  CUDA_TRY(cudaMemcpy(out.d_lut, lut.data(), lut.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMalloc(&out.d_rec, rec.size()));
+  CUDA_TRY(cudaMemcpy(out.d_rec, rec.data(), rec.size(), cudaMemcpyHostToDevice));
+  out.kmax = kmax;
   return OBT_OK;
 }
 
@@ -494,18 +591,29 @@ int apply_lanes(const obt_model* m, int tile, bool write_idx) {
 // `budget` bytes, split evenly (multiples of the 8-feature step); small batches split
 // finer until the grid has ~2 CTAs per SM, so a 10k-object batch is not quantized by 10
 // CTAs.
-int quantize_chunk(const obt_model* m, const BorderTable& bt, int64_t n_slots, size_t budget) {
+int quantize_chunk_bytes(const obt_model* m, size_t per_feature, int64_t n_slots, size_t budget) {
   const int F = m->n_features;
-  const size_t per_feature = bt.levels > 0 ? (size_t)bt.pitch * 4 : 0;
   int chunks = per_feature ? (int)std::max<size_t>(1, (F * per_feature + budget - 1) / budget) : 1;
   int fc = 0;
   for (;; ++chunks) {
     fc = ((F + chunks - 1) / chunks + 7) / 8 * 8;
     if ((size_t)fc * per_feature <= budget || fc == 8) break;
   }
+  // Chunks that start on 32-feature (128-byte) boundaries of the object-major rows: the
+  // TMA reads of neighbouring chunks then never share an L2 line (balanced chunks of
+  // 100 features read 0.99 GB for cfg2's 0.8 GB of features)
+  const char* al = getenv("OBT_QUANT_ALIGN");  // A/B knob: 0 = balanced chunks
+  if (chunks > 1 && per_feature && !(al && !strcmp(al, "0"))) {
+    const int fit = (int)(budget / per_feature) / 32 * 32;
+    if (fit >= 32) fc = std::min(fit, (F + 7) / 8 * 8);
+  }
   const int64_t blocks = (n_slots + obt::kQuantBlock - 1) / obt::kQuantBlock;
   while (fc > 8 && blocks * ((F + fc - 1) / fc) < 2 * m->sm_count) fc = std::max(8, (fc / 2 + 7) / 8 * 8);
   return fc;
+}
+
+int quantize_chunk(const obt_model* m, const BorderTable& bt, int64_t n_slots, size_t budget) {
+  return quantize_chunk_bytes(m, bt.levels > 0 ? (size_t)bt.pitch * 4 : 0, n_slots, budget);
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
@@ -534,6 +642,19 @@ CUtensorMapL2promotion tma_l2_promotion() {
          : OBT_TMA_L2 == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
          : OBT_TMA_L2 == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
                              : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
+
+// K1L over K1t when its dependent shared loads per value (one cell byte + kmax border
+// compares) are fewer than the Eytzinger search's (levels - 2, the top two from
+// registers).  Measured on B200: cfg2 (kmax 1 vs 6 levels) 0.219 vs 0.247 ms; cfg4
+// (kmax 4 vs 7 levels) 6.12 vs 4.92 ms; cfg5 (kmax 3 vs 6 levels) 17.3 vs 16.6 ms.
+// OBT_QUANT_LUT=1 forces K1L wherever its tables exist, 0 disables it.
+bool lut_preferred(const obt_model* m) {
+  if (m->used_lut.kmax <= 0) return false;
+  const char* e = getenv("OBT_QUANT_LUT");
+  if (e && !strcmp(e, "0")) return false;
+  if (e && !strcmp(e, "1")) return true;
+  return 1 + m->used_lut.kmax < m->used.levels - 2;
 }
 
 bool quantize_tma_enabled() {
@@ -572,13 +693,19 @@ int launch_quantize(const obt_model* m, const float* x, int64_t n, int layout, u
   p.swizzle2 = r2.swizzle ? 1 : 0;
   const unsigned blocks = (unsigned)((n_slots + obt::kQuantBlock - 1) / obt::kQuantBlock);
 
-  // K1t: TMA-staged rows (object-major, tiled, 16-byte row pitch and alignment)
-  obt::QuantTmaFn tfn = pick_quant_tma(bt.levels);
+  // K1t / K1L: TMA-staged rows (object-major, tiled, 16-byte row pitch and alignment);
+  // K1L (cell tables) wherever the used-border set admits them
+  const LutTable& lt = m->used_lut;
+  const bool use_lut = tiled && lut_preferred(m);
+  obt::QuantTmaFn tfn = use_lut ? pick_quant_lut(lt.kmax) : pick_quant_tma(bt.levels);
   if (tiled && layout == OBT_LAYOUT_OBJECT_MAJOR && F % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
       tfn && encode_tiled() && quantize_tma_enabled()) {
     // two CTAs per SM: each gets half the SM's shared memory less the per-CTA reserve
     const size_t half = (size_t)(m->smem_optin + 1024) / 2 - 1024;
-    const int fc = quantize_chunk(m, bt, n_slots, half - obt::kQTSmemFixed);
+    const size_t lut_fixed = use_lut ? 256 + 32 : 0;  // 256-byte alignment of the tables
+    const int fc = use_lut ? quantize_chunk_bytes(m, (size_t)obt::kLutCells + lt.rec_stride, n_slots,
+                                                  half - obt::kQTSmemFixed - lut_fixed)
+                           : quantize_chunk(m, bt, n_slots, half - obt::kQTSmemFixed);
     CUtensorMap map;
     const cuuint64_t dims[2] = {(cuuint64_t)F, (cuuint64_t)n};
     const cuuint64_t strides[1] = {(cuuint64_t)F * 4};
@@ -589,7 +716,11 @@ int launch_quantize(const obt_model* m, const float* x, int64_t n, int layout, u
                                       tma_l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r == CUDA_SUCCESS) {
       p.chunk_features = fc;
-      const size_t smem = obt::kQTSmemFixed + (bt.levels > 0 ? (size_t)std::min(fc, F) * bt.pitch * 4 : 16);
+      p.lut = lt.d_lut;
+      p.lrec = lt.d_rec;
+      p.lrec_stride = lt.rec_stride;
+      const size_t smem = use_lut ? obt::kQTSmemFixed + lut_fixed + (size_t)std::min(fc, F) * (obt::kLutCells + lt.rec_stride)
+                                  : obt::kQTSmemFixed + (bt.levels > 0 ? (size_t)std::min(fc, F) * bt.pitch * 4 : 16);
       CUDA_TRY(cudaFuncSetAttribute(tfn, cudaFuncAttributeMaxDynamicSharedMemorySize, m->smem_optin));
       const dim3 grid(blocks, (unsigned)((F + fc - 1) / fc));
       tfn<<<grid, obt::kQTThreads, smem, stream>>>(map, p);
@@ -681,7 +812,8 @@ int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, int tpw, d
 
 int launch_multi(obt_model* m, const uint8_t* q, int64_t n, double* out, cudaStream_t stream) {
   int di = 0;
-  const void* fn = obt::pick_multi(m->depth_inst, m->compare_mode, m->leaf_storage, m->n_outputs, &di);
+  const void* fn = m->multi_slice ? obt::pick_multi_slice(m->depth_inst, m->compare_mode, m->leaf_storage, m->n_outputs, &di)
+                                  : obt::pick_multi(m->depth_inst, m->compare_mode, m->leaf_storage, m->n_outputs, &di);
   if (!fn || di != m->depth_inst) return fail(OBT_E_UNSUPPORTED, "no multi-output kernel for depth %d, %d outputs",
                                              m->depth_inst, m->n_outputs);
   obt::MultiParams p{};
@@ -700,7 +832,7 @@ int launch_multi(obt_model* m, const uint8_t* q, int64_t n, double* out, cudaStr
   p.scale = m->scale;
   p.bias = m->bias;
   void* kargs[] = {&p};
-  const dim3 grid((unsigned)((n + kMultiTile - 1) / kMultiTile)), block(obt::kMultiThreads);
+  const dim3 grid((unsigned)((n + kMultiTile - 1) / kMultiTile)), block(m->multi_slice ? kMultiTile / 4 : obt::kMultiThreads);
   CUDA_TRY(cudaLaunchKernel(fn, grid, block, kargs, 0, stream));
   ++g_launches;
   return OBT_OK;
@@ -838,6 +970,8 @@ int obt_model_create(const obt_model_desc* d, int device, obt_model** out) {
   if (rc2 != OBT_OK) return rc2;
   rc2 = build_border_table(used_borders.data(), used_counts.data(), d->n_features, d->border_stride, m->used);
   if (rc2 != OBT_OK) return rc2;
+  rc2 = build_lut_table(used_borders.data(), used_counts.data(), d->n_features, d->border_stride, m->used_lut);
+  if (rc2 != OBT_OK) return rc2;
   int umax = 0;
   for (int f = 0; f < d->n_features; ++f) umax = std::max(umax, (int)used_counts[f]);
   m->compare_mode = umax <= 127 ? 7 : 8;
@@ -871,14 +1005,20 @@ int obt_model_create(const obt_model_desc* d, int device, obt_model** out) {
   }
   const size_t ls = leaf_size(m->leaf_storage);
   if (C > 1) {
-    // multi-output records [T][2^DI][CP]: one leaf's C values contiguous, padded to 32-byte rows (fp32)
-    const int CP = obt::multi_record_values(m->leaf_storage, C);
-    std::vector<uint8_t> rec((size_t)std::max(m->n_trees, 1) * per_tree * CP * ls, 0);
+    // multi-output records, one leaf's C values contiguous: K4s slots of multi_slot bytes
+    // (a power of two, so a record never straddles a 128-byte line), or K4 [CP] rows
+    // K4s measured slower than K4 at config 5 (668 vs 575 ms: 168 registers, 12 warps per
+    // SM); kept as the OBT_MULTI_SLICE=1 knob
+    const char* ms = getenv("OBT_MULTI_SLICE");
+    m->multi_slice = (ms && !strcmp(ms, "1")) ? 1 : 0;
+    m->multi_slot = m->multi_slice ? obt::multi_slice_slot(m->leaf_storage, C)
+                                   : obt::multi_record_values(m->leaf_storage, C) * (int)ls;
+    std::vector<uint8_t> rec((size_t)std::max(m->n_trees, 1) * per_tree * m->multi_slot, 0);
     for (int t = 0; t < m->n_trees; ++t)
       for (int c = 0; c < C; ++c)
         for (size_t j = 0; j < per_tree_in; ++j) {
           const double v = d->leaves[(((size_t)t * C + c) << D) + j];
-          uint8_t* dst = rec.data() + (((size_t)t * per_tree + j) * CP + c) * ls;
+          uint8_t* dst = rec.data() + ((size_t)t * per_tree + j) * m->multi_slot + (size_t)c * ls;
           if (m->leaf_storage == 0) std::memcpy(dst, &v, 8);
           else { const float f = (float)v; std::memcpy(dst, &f, 4); }
         }
@@ -930,6 +1070,14 @@ int obt_model_info(const obt_model* m, int32_t* n_features, int32_t* n_trees, in
   if (precision) *precision = m->precision;
   if (leaf_storage) *leaf_storage = m->leaf_storage;
   if (compare_mode) *compare_mode = m->compare_mode;
+  return OBT_OK;
+}
+
+int obt_model_quantize_kernel(const obt_model* m, int32_t* kind, int32_t* param) {
+  if (!m) return fail(OBT_E_INVALID, "null model");
+  const bool lut = lut_preferred(m);
+  if (kind) *kind = lut ? 1 : 0;
+  if (param) *param = lut ? m->used_lut.kmax : m->used.levels;
   return OBT_OK;
 }
 

@@ -60,10 +60,32 @@ __device__ __forceinline__ uint32_t mbar_try(uint64_t* bar, uint32_t parity) {
   return ok;
 }
 
-// Single-thread wait (the producer): back off with nanosleep so a waiting producer
-// does not steal issue slots from the consumer warps of its SM sub-partition.
+// try_wait with a suspend-time hint: the thread sleeps in hardware until the phase
+// completes (or the hint, in ns, elapses), instead of re-issuing the probe.
+__device__ __forceinline__ uint32_t mbar_try_suspend(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
+      : "memory");
+  return ok;
+}
+
+#ifndef OBT_PRODUCER_SUSPEND_NS
+#define OBT_PRODUCER_SUSPEND_NS 1000000
+#endif
+// Single-thread wait (the producer).  A probe + nanosleep(64) loop measured 13 M
+// re-issued probes per cfg2 apply launch (17% of the launch's warp instructions, issue
+// slots taken from the consumer warps of the producer's SM sub-partition); with a
+// suspend hint the producer sleeps until the consumers release the stage.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  while (!mbar_try(bar, parity)) __nanosleep(64);
+  while (!mbar_try_suspend(bar, parity, OBT_PRODUCER_SUSPEND_NS)) {
+  }
 }
 
 // Whole-warp wait whose retry branch is warp-uniform (vote), so code after it stays in
@@ -127,6 +149,11 @@ struct QuantizeParams {
   int64_t split;
   uint8_t* out2;
   int32_t tile2, swizzle2;
+  // K1L cell tables (used borders): luts [F][256] cell -> lower-bound bucket, recs [F]
+  // of {lo, hi, s, o, borders[P] (+inf padded)} with stride lrec_stride bytes
+  const uint8_t* lut;
+  const unsigned char* lrec;
+  int32_t lrec_stride;
 };
 
 constexpr int kQuantObjects = 128;    // tile quantum: a quantize warp's 128 objects never straddle tiles
@@ -157,6 +184,31 @@ __device__ __forceinline__ uint32_t eytz_level(uint32_t o, float x, const float*
   const float b = *reinterpret_cast<const float*>(reinterpret_cast<const unsigned char*>(e) + o);
   const uint32_t four = two + two;  // runtime 4: the adds stay IMAD-able
   return add_if_greater(o * two + four, x, b, four);
+}
+
+// Store the packed buckets of one feature for a lane's 4 objects (base + lane + 32k):
+// tiled -> word `lane` of the 128-object block's row, plain -> 4 bytes of row f.
+template <bool TILED>
+__device__ __forceinline__ void store_bucket_word(const QuantizeParams& p, uint32_t word, int f, int64_t base, int lane,
+                                                  bool full_objs) {
+  const int64_t ob = base + lane;
+  if (!full_objs) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (ob + 32 * k >= p.n) word &= ~(0xFFu << (8 * k));  // padding objects are zero (quantize.py:172)
+  }
+  if (TILED) {
+    const bool second = base >= p.split;  // warp-uniform: blocks never straddle the split
+    const int64_t rb = second ? base - p.split : base;
+    const int64_t tl = second ? p.tile2 : p.tile;
+    const bool sw = (second ? p.swizzle2 : p.swizzle) && (f & 1);
+    const int64_t t = rb / tl, w = (rb - t * tl + 4 * lane) ^ (sw ? 64 : 0);
+    *reinterpret_cast<uint32_t*>((second ? p.out2 : p.out) + (t * p.n_features + f) * tl + w) = word;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (ob + 32 * k < p.n) p.out[(int64_t)f * p.n + ob + 32 * k] = (uint8_t)(word >> (8 * k));
+  }
 }
 
 constexpr int kQuantStep = 8;  // features per step: one 32-byte sector per row
@@ -248,24 +300,7 @@ __device__ __forceinline__ void quantize_step(const QuantizeParams& p, const flo
     word = o[j][1] * m6 + word;
     word = o[j][2] * m14 + word;
     word = o[j][3] * m22 + word;
-    if (!full_objs) {
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (ob + 32 * k >= p.n) word &= ~(0xFFu << (8 * k));
-    }
-    const int f = f0 + fq + j;
-    if (TILED) {
-      const bool second = base >= p.split;  // warp-uniform: blocks never straddle the split
-      const int64_t rb = second ? base - p.split : base;
-      const int64_t tl = second ? p.tile2 : p.tile;
-      const bool sw = (second ? p.swizzle2 : p.swizzle) && (f & 1);
-      const int64_t t = rb / tl, w = (rb - t * tl + 4 * lane) ^ (sw ? 64 : 0);
-      *reinterpret_cast<uint32_t*>((second ? p.out2 : p.out) + (t * F + f) * tl + w) = word;
-    } else {
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (ob + 32 * k < p.n) p.out[(int64_t)f * p.n + ob + 32 * k] = (uint8_t)(word >> (8 * k));
-    }
+    store_bucket_word<TILED>(p, word, f0 + fq + j, base, lane, full_objs);
   }
 }
 
@@ -452,6 +487,134 @@ __global__ void __launch_bounds__(kQTThreads, 2) quantize_tma_kernel(const __gri
 }
 
 // ---------------------------------------------------------------------------
+// K1L: cell-table quantize (TMA-staged rows as K1t, used borders only).  Per feature f
+// the host chooses an affine map y = fma(clamp(x, lo_f, hi_f), s_f, o_f) whose results
+// lie in [1.5 * 2^23, 1.5 * 2^23 + 255]: the low byte of y's bits is a cell c, monotone in
+// x (clamp and a correctly rounded fma with s_f >= 0 are monotone; NaN clamps to lo_f).
+// With c_k the cell of border k, lut_f[c] = #{k : c_k < c} and every border k with
+// c_k < c is below any x of cell c, every border with c_k > c is >= it; so the bucket
+// #{k : x > b_k} is lut_f[c] plus the count over the at most KMAX borders of cell c,
+// which KMAX compares against the sorted, +inf-padded borders finish (a compare past
+// the cell's borders is false).  The host evaluates the same fp32 ops (fmaf is correctly
+// rounded in both places), so buckets are bit-exact.  Per value: 2 FMNMX, FFMA, PRMT,
+// one byte load, KMAX x (address, load, compare-add) -- about a third of the Eytzinger
+// search's instructions, with fewer dependent shared loads.
+constexpr int kLutCells = 256;
+constexpr int kLutRecHeader = 16;  // lo, hi, s, o
+
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+
+template <int KMAX>
+__global__ void __launch_bounds__(kQTThreads, 2) quantize_lut_kernel(const __grid_constant__ CUtensorMap rows,
+                                                                     const QuantizeParams p) {
+  extern __shared__ __align__(16) unsigned char qt_raw[];
+  unsigned char* ring = qt_raw + ((1024u - (smem_u32(qt_raw) & 1023u)) & 1023u);  // swizzle atoms need alignment
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kQTStages * kQTStageBytes);
+  uint64_t* empty = full + kQTStages;
+  unsigned char* luts = reinterpret_cast<unsigned char*>(empty + kQTStages) + 32;  // 256-aligned below
+  luts += (256u - (smem_u32(luts) & 255u)) & 255u;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int fc = p.chunk_features;
+  const int f0 = blockIdx.y * fc;
+  const int nf = min(fc, p.n_features - f0);
+  unsigned char* recs = luts + (size_t)fc * kLutCells;
+  const int rs = p.lrec_stride;
+  const int n_steps = (nf + kQuantStep - 1) / kQuantStep;
+  const int64_t row0 = (int64_t)blockIdx.x * kQuantBlock;
+  const int64_t blocks_left = (p.n_slots - row0 + 127) / 128;
+  const int active = blocks_left < kQTConsumerWarps ? (int)blocks_left : kQTConsumerWarps;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kQTStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 32 * active);
+    }
+    fence_mbar_init();
+  }
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(p.lut + (size_t)f0 * kLutCells);
+    uint4* dst = reinterpret_cast<uint4*>(luts);
+    for (int i = threadIdx.x; i < nf * kLutCells / 16; i += kQTThreads) dst[i] = __ldg(src + i);
+    const uint4* rsrc = reinterpret_cast<const uint4*>(p.lrec + (size_t)f0 * rs);
+    uint4* rdst = reinterpret_cast<uint4*>(recs);
+    for (int i = threadIdx.x; i < nf * rs / 16; i += kQTThreads) rdst[i] = __ldg(rsrc + i);
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int st = 0; st < n_steps; ++st) {
+        const int s = st % kQTStages;
+        if (st >= kQTStages) mbar_wait(&empty[s], (uint32_t)(st / kQTStages - 1) & 1u);
+        mbar_expect_tx(&full[s], kQTStageBytes);
+        unsigned char* dst = ring + (size_t)s * kQTStageBytes;
+#pragma unroll
+        for (int b = 0; b < kQuantBlock / kQTBoxRows; ++b)
+          tma_load_2d(dst + b * kQTBoxRows * kQuantStep * 4, &rows, f0 + st * kQuantStep,
+                      (int)(row0 + b * kQTBoxRows), &full[s]);
+      }
+    }
+    return;
+  }
+  const int cw = warp - 1;
+  if (cw >= active) return;
+  const int64_t base = row0 + cw * 128;
+  const bool full_objs = base + lane + 96 < p.n;
+  const uint32_t luts_s = smem_u32(luts), recs_s = smem_u32(recs);
+  for (int st = 0; st < n_steps; ++st) {
+    const int s = st % kQTStages;
+    mbar_wait_warp(&full[s], (uint32_t)(st / kQTStages) & 1u);
+    const unsigned char* stage = ring + (size_t)s * kQTStageBytes;
+    float v[kQuantStep][4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int r = cw * 128 + lane + 32 * k;
+      const unsigned char* rp = stage + 32 * r;
+      const uint32_t sw = (uint32_t)((r >> 2) & 1) * 16u;
+      const float4 a = *reinterpret_cast<const float4*>(rp + sw);
+      const float4 b = *reinterpret_cast<const float4*>(rp + (16u ^ sw));
+      v[0][k] = a.x; v[1][k] = a.y; v[2][k] = a.z; v[3][k] = a.w;
+      v[4][k] = b.x; v[5][k] = b.y; v[6][k] = b.z; v[7][k] = b.w;
+    }
+    mbar_arrive(&empty[s]);
+    const int fq = st * kQuantStep;
+    uint32_t bk[kQuantStep][4];
+#pragma unroll
+    for (int j = 0; j < kQuantStep; ++j) {
+      const int fl = min(fq + j, nf - 1);
+      const float4 h = *reinterpret_cast<const float4*>(recs + (size_t)fl * rs);  // lo, hi, s, o (broadcast)
+      const uint32_t lut_base = luts_s + (uint32_t)fl * kLutCells;
+      const uint32_t bord = recs_s + (uint32_t)fl * rs + kLutRecHeader;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float x = v[j][k];
+        const float y = __fmaf_rn(fminf(fmaxf(x, h.x), h.y), h.z, h.w);
+        uint32_t b = lds_u8(__byte_perm(__float_as_uint(y), lut_base, 0x7650u));
+#pragma unroll
+        for (int i = 0; i < KMAX; ++i) b = add_if_greater(b, x, lds_f32(bord + 4u * b), 1u);
+        bk[j][k] = b;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kQuantStep; ++j) {
+      if (fq + j >= nf) break;
+      uint32_t word = bk[j][3] * 256u + bk[j][2];
+      word = word * 256u + bk[j][1];
+      word = word * 256u + bk[j][0];
+      store_bucket_word<true>(p, word, f0 + fq + j, base, lane, full_objs);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K2: tree apply.
 //
 // A split descriptor is one 32-bit word (off << 8) | k (plus, in 8-bit mode, a second
@@ -479,6 +642,18 @@ __global__ void __launch_bounds__(kQTThreads, 2) quantize_tma_kernel(const __gri
 #define OBT_GROUP_D8 32
 #endif
 __host__ __device__ constexpr int tree_group(int di) { return di <= 6 ? OBT_GROUP_SHALLOW : di <= 8 ? OBT_GROUP_D8 : 4; }
+#ifndef OBT_DESC_PAIR_LOADS
+#define OBT_DESC_PAIR_LOADS 1  // parameter-bank descriptors: two splits per 128-bit uniform load
+#endif
+#ifndef OBT_PF_TREES
+#define OBT_PF_TREES 2         // apply pipeline: bucket words requested this many trees ahead
+#endif
+#ifndef OBT_FOLD_LAG
+#define OBT_FOLD_LAG 1         // apply pipeline: leaves folded this many trees after their request
+#endif
+#ifndef OBT_SINGLE_CHAIN
+#define OBT_SINGLE_CHAIN 1     // index bits merged in one LOP3 chain (not even/odd chains)
+#endif
 #ifndef OBT_PACKED_DESC
 #define OBT_PACKED_DESC 0
 #endif
@@ -530,41 +705,59 @@ __device__ __forceinline__ uint32_t byte_of(uint32_t w) {
 }
 
 
+// Shared loads by 32-bit address.  VOL selects PTX-volatile loads, which ptxas keeps in
+// program order: K2's software pipeline then decides how far ahead each load is issued
+// (left to itself ptxas hoisted K2's bucket loads ~6 trees ahead and spilled).  The
+// other kernels keep plain loads (volatile ones made K2s spill).
+#ifndef OBT_LDS_VOLATILE
+#define OBT_LDS_VOLATILE 1
+#endif
+#define OBT_LDS_SEL(VOL) ((VOL) && OBT_LDS_VOLATILE)
+
+template <bool VOL = false>
 __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
   uint32_t v;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  if constexpr (OBT_LDS_SEL(VOL)) asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  else asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
 }
 
 // W consecutive bucket words (4W objects) of one feature row.
-template <int W>
+template <int W, bool VOL = false>
 __device__ __forceinline__ void lds_words(uint32_t addr, uint32_t (&w)[W]) {
   if constexpr (W == 1) {
-    w[0] = lds_u32(addr);
+    w[0] = lds_u32<VOL>(addr);
   } else if constexpr (W == 2) {
-    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w[0]), "=r"(w[1]) : "r"(addr));
+    if constexpr (OBT_LDS_SEL(VOL)) asm volatile("ld.volatile.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w[0]), "=r"(w[1]) : "r"(addr));
+    else asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w[0]), "=r"(w[1]) : "r"(addr));
   } else {
     static_assert(W == 4, "1, 2 or 4 bucket words per thread");
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "r"(addr));
+    if constexpr (OBT_LDS_SEL(VOL))
+      asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "r"(addr));
+    else
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "r"(addr));
   }
 }
 
-// Leaf loads by 32-bit shared address.
-template <int LEAF> __device__ __forceinline__ typename LeafT<LEAF>::T lds_leaf(uint32_t addr);
-template <> __device__ __forceinline__ double lds_leaf<0>(uint32_t addr) {
-  double v;
-  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
-  return v;
-}
-template <> __device__ __forceinline__ float lds_leaf<1>(uint32_t addr) {
-  float v;
-  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
-  return v;
-}
-template <> __device__ __forceinline__ __half lds_leaf<2>(uint32_t addr) {
-  unsigned short v;
-  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
-  return __ushort_as_half(v);
+// Leaf loads.
+template <int LEAF, bool VOL = false>
+__device__ __forceinline__ typename LeafT<LEAF>::T lds_leaf(uint32_t addr) {
+  if constexpr (LEAF == 0) {
+    double v;
+    if constexpr (OBT_LDS_SEL(VOL)) asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+    else asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+    return v;
+  } else if constexpr (LEAF == 1) {
+    float v;
+    if constexpr (OBT_LDS_SEL(VOL)) asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    else asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+  } else {
+    unsigned short v;
+    if constexpr (OBT_LDS_SEL(VOL)) asm volatile("ld.volatile.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+    else asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+    return __ushort_as_half(v);
+  }
 }
 
 // Leaf-table stride in a stage: prescaled tables sit on 256-byte boundaries so the
@@ -672,83 +865,132 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid
       // broadcasts from the constant bank, no shared-memory wavefronts; a packed 4-byte
       // form measured slower: its unpack runs on the vector ALU)
       const int gbase = (c * (p.chunk_trees / kTreeGroup) + g) * (kTreeGroup * DI * 2);
+      // Software pipeline over the group's trees (all indices compile-time after
+      // unrolling): iteration i requests the bucket words of tree i (stage A), builds the
+      // index of tree i - kPF and requests its leaves (stage B), and folds the leaves of
+      // tree i - kPF - 1 (stage C).  Each load's consumer thus sits about one tree of
+      // instructions after it in issue order, and folds stay in tree order.
+      constexpr int kPF = OBT_PF_TREES;
+      uint32_t wbuf[kPF + 1][DI][W];  // bucket words of the trees in flight
+      uint32_t kbuf[kPF + 1][DI];     // DSRC 1: k replicated per depth
+      constexpr int kLag = OBT_FOLD_LAG;
+      typename LT::T gbuf[kLag + 1][4 * W];  // gathered leaves awaiting their fold
+      (void)kbuf; (void)gbuf;
 #pragma unroll
-      for (int tt = 0; tt < kTreeGroup; ++tt) {
-        const int t = g * kTreeGroup + tt;
-        uint32_t lo_even[W], lo_odd[W], hi[W];
+      for (int it = 0; it < kTreeGroup + kPF + kLag; ++it) {
+        if (it < kTreeGroup) {  // stage A: bucket words of tree `it`
+          const int tt = it, sl = it % (kPF + 1);
+          uint32_t pend_off = 0, pend_k = 0;  // second split of a 128-bit descriptor pair
+          (void)pend_off; (void)pend_k;
 #pragma unroll
-        for (int x = 0; x < W; ++x) { lo_even[x] = 0; lo_odd[x] = 0; hi[x] = 0; }
-#pragma unroll
-        for (int d = 0; d < DI; ++d) {
-          uint32_t w[W];
-          uint32_t b7s[W];  // [q > ordinal] in bit 7 of each byte, garbage below
-          if constexpr (DSRC == 1) {
-            static_assert(CMP == 7 && W == 1, "parameter-bank descriptors: 7-bit compare, 4 objects per thread");
-            const uint32_t off = args.desc[gbase + 2 * (tt * DI + d)];
-            const uint32_t krep = args.desc[gbase + 2 * (tt * DI + d) + 1];
-            w[0] = lds_u32(my_q + off);
-            b7s[0] = w[0] + krep;
-          } else {
-            // shared-memory descriptors: 7-bit {off, k replicated}; 8-bit {(off << 8) | k, s}
-            const uint32_t d0 = dw[(tt * DI + d) * kDW], d1 = dw[(tt * DI + d) * kDW + (kDW - 1)];
-            if constexpr (CMP == 7 && kDW == 1) {
-              lds_words<W>(my_q + (d0 >> 8), w);
-              const uint32_t krep = __byte_perm(d0, 0u, 0x0000u);
-#pragma unroll
-              for (int x = 0; x < W; ++x) b7s[x] = w[x] + krep;
-            } else if constexpr (CMP == 7) {
-              lds_words<W>(my_q + d0, w);
-#pragma unroll
-              for (int x = 0; x < W; ++x) b7s[x] = w[x] + d1;
+          for (int d = 0; d < DI; ++d) {
+            if constexpr (DSRC == 1) {
+              static_assert(CMP == 7 && W == 1, "parameter-bank descriptors: 7-bit compare, 4 objects per thread");
+              // two splits per 128-bit load where the pair is 16-byte aligned (gbase is a
+              // multiple of 4 words, so the parity of tt * DI + d decides at compile time);
+              // ptxas splits it into two uniform LDCU.64 either way
+              const int sidx = tt * DI + d;
+              uint32_t off, krep;
+              if (OBT_DESC_PAIR_LOADS && (sidx & 1) == 0 && d + 1 < DI) {
+                const uint4 pr = *reinterpret_cast<const uint4*>(&args.desc[gbase + 2 * sidx]);
+                off = pr.x; krep = pr.y; pend_off = pr.z; pend_k = pr.w;
+              } else if (OBT_DESC_PAIR_LOADS && d > 0 && ((sidx - 1) & 1) == 0) {
+                off = pend_off; krep = pend_k;
+              } else {
+                off = args.desc[gbase + 2 * sidx];
+                krep = args.desc[gbase + 2 * sidx + 1];
+              }
+              wbuf[sl][d][0] = lds_u32<true>(my_q + off);
+              kbuf[sl][d] = krep;
             } else {
-              lds_words<W>(my_q + (d0 >> 8), w);
-              const uint32_t k = __byte_perm(d0, 0u, 0x0000u) & 0x7f7f7f7fu;
+              const uint32_t d0 = dw[(tt * DI + d) * kDW];
+              lds_words<W, true>(my_q + ((CMP == 7 && kDW == 2) ? d0 : (d0 >> 8)), wbuf[sl][d]);
+            }
+          }
+        }
+        if (it >= kPF && it - kPF < kTreeGroup) {  // stage B: index + leaf requests of tree ti
+          const int ti = it - kPF, sl = ti % (kPF + 1);
+          const int t = g * kTreeGroup + ti;
+          uint32_t lo_even[W], lo_odd[W], hi[W];
 #pragma unroll
-              for (int x = 0; x < W; ++x) b7s[x] = maj3((w[x] & 0x7f7f7f7fu) + k, w[x], d1);
+          for (int x = 0; x < W; ++x) { lo_even[x] = 0; lo_odd[x] = 0; hi[x] = 0; }
+#pragma unroll
+          for (int d = 0; d < DI; ++d) {
+            uint32_t b7s[W];  // [q > ordinal] in bit 7 of each byte, garbage below
+            if constexpr (DSRC == 1) {
+              b7s[0] = wbuf[sl][d][0] + kbuf[sl][d];
+            } else {
+              // shared-memory descriptors: 7-bit {off, k replicated}; 8-bit {(off << 8) | k, s}
+              const uint32_t d0 = dw[(ti * DI + d) * kDW], d1 = dw[(ti * DI + d) * kDW + (kDW - 1)];
+              if constexpr (CMP == 7 && kDW == 1) {
+                const uint32_t krep = __byte_perm(d0, 0u, 0x0000u);
+#pragma unroll
+                for (int x = 0; x < W; ++x) b7s[x] = wbuf[sl][d][x] + krep;
+              } else if constexpr (CMP == 7) {
+#pragma unroll
+                for (int x = 0; x < W; ++x) b7s[x] = wbuf[sl][d][x] + d1;
+              } else {
+                const uint32_t k = __byte_perm(d0, 0u, 0x0000u) & 0x7f7f7f7fu;
+#pragma unroll
+                for (int x = 0; x < W; ++x) {
+                  const uint32_t wv = wbuf[sl][d][x];
+                  b7s[x] = maj3((wv & 0x7f7f7f7fu) + k, wv, d1);
+                }
+              }
+            }
+#pragma unroll
+            for (int x = 0; x < W; ++x) {
+              const uint32_t b7 = b7s[x];
+              const int pos = d + kBitBase;  // target bit of condition d inside each byte
+              if (pos < 8) {
+                const uint32_t term = (pos == 7 ? b7 : (b7 >> (7 - pos))) & (0x01010101u << pos);
+                // one OR chain: each depth is one LOP3 (mask | acc) after its shift
+                if ((d & 1) && !OBT_SINGLE_CHAIN) lo_odd[x] |= term; else lo_even[x] |= term;
+              } else {
+                hi[x] |= (pos == 15 ? b7 : (b7 >> (15 - pos))) & (0x01010101u << (pos - 8));
+              }
             }
           }
 #pragma unroll
           for (int x = 0; x < W; ++x) {
-            const uint32_t b7 = b7s[x];
-          const int pos = d + kBitBase;  // target bit of condition d inside each byte
-            if (pos < 8) {
-              const uint32_t term = (pos == 7 ? b7 : (b7 >> (7 - pos))) & (0x01010101u << pos);
-              if (d & 1) lo_odd[x] |= term; else lo_even[x] |= term;
+            const uint32_t lo = lo_even[x] | lo_odd[x];
+            if constexpr (WRITE_IDX) {
+              const int tg = t_base + t;
+              if (tg >= p.tree_begin && tg < p.tree_end) {
+                uint16_t* row = p.idx_out + (int64_t)(tg - p.tree_begin) * p.n;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  const uint32_t idx = ((lo >> (8 * k)) & 0xffu) | (DI > 8 ? ((hi[x] >> (8 * k)) & 0xffu) << 8 : 0u);
+                  const int64_t o = obj_of(x, k);
+                  if (o < p.n) row[o] = (uint16_t)idx;
+                }
+              }
+            } else if constexpr (kPrescaled) {
+              const uint32_t tab = leaf_base + (uint32_t)t * 256u;
+              typename LT::T* gv = gbuf[ti % (kLag + 1)] + 4 * x;
+              gv[0] = lds_leaf<LEAF, true>(__byte_perm(lo, tab, 0x7650u));
+              gv[1] = lds_leaf<LEAF, true>(__byte_perm(lo, tab, 0x7651u));
+              gv[2] = lds_leaf<LEAF, true>(__byte_perm(lo, tab, 0x7652u));
+              gv[3] = lds_leaf<LEAF, true>(__byte_perm(lo, tab, 0x7653u));
             } else {
-              hi[x] |= (pos == 15 ? b7 : (b7 >> (15 - pos))) & (0x01010101u << (pos - 8));
+              const uint32_t tab = leaf_base + (uint32_t)t * kTabStride;
+              uint32_t ix[4];
+              ix[0] = byte_of<0>(lo); ix[1] = byte_of<1>(lo); ix[2] = byte_of<2>(lo); ix[3] = byte_of<3>(lo);
+              if constexpr (DI > 8) {
+                ix[0] |= byte_of<0>(hi[x]) << 8; ix[1] |= byte_of<1>(hi[x]) << 8;
+                ix[2] |= byte_of<2>(hi[x]) << 8; ix[3] |= byte_of<3>(hi[x]) << 8;
+              }
+              typename LT::T* gv = gbuf[ti % (kLag + 1)] + 4 * x;
+#pragma unroll
+              for (int k = 0; k < 4; ++k) gv[k] = lds_leaf<LEAF, true>(tab + (ix[k] << LT::kShift));
             }
           }
         }
+        if constexpr (!WRITE_IDX) {
+          if (it >= kPF + kLag && it - kPF - kLag < kTreeGroup) {  // stage C: fold tree tf (tree order per object)
+            const int tf = it - kPF - kLag;
 #pragma unroll
-        for (int x = 0; x < W; ++x) {
-          const uint32_t lo = lo_even[x] | lo_odd[x];
-          if constexpr (WRITE_IDX) {
-            const int tg = t_base + t;
-            if (tg >= p.tree_begin && tg < p.tree_end) {
-              uint16_t* row = p.idx_out + (int64_t)(tg - p.tree_begin) * p.n;
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const uint32_t idx = ((lo >> (8 * k)) & 0xffu) | (DI > 8 ? ((hi[x] >> (8 * k)) & 0xffu) << 8 : 0u);
-                const int64_t o = obj_of(x, k);
-                if (o < p.n) row[o] = (uint16_t)idx;
-              }
-            }
-          } else if constexpr (kPrescaled) {
-            const uint32_t tab = leaf_base + (uint32_t)t * 256u;
-            acc[4 * x + 0] += LT::widen(lds_leaf<LEAF>(__byte_perm(lo, tab, 0x7650u)));
-            acc[4 * x + 1] += LT::widen(lds_leaf<LEAF>(__byte_perm(lo, tab, 0x7651u)));
-            acc[4 * x + 2] += LT::widen(lds_leaf<LEAF>(__byte_perm(lo, tab, 0x7652u)));
-            acc[4 * x + 3] += LT::widen(lds_leaf<LEAF>(__byte_perm(lo, tab, 0x7653u)));
-          } else {
-            const uint32_t tab = leaf_base + (uint32_t)t * kTabStride;
-            uint32_t ix[4];
-            ix[0] = byte_of<0>(lo); ix[1] = byte_of<1>(lo); ix[2] = byte_of<2>(lo); ix[3] = byte_of<3>(lo);
-            if constexpr (DI > 8) {
-              ix[0] |= byte_of<0>(hi[x]) << 8; ix[1] |= byte_of<1>(hi[x]) << 8;
-              ix[2] |= byte_of<2>(hi[x]) << 8; ix[3] |= byte_of<3>(hi[x]) << 8;
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) acc[4 * x + k] += LT::widen(lds_leaf<LEAF>(tab + (ix[k] << LT::kShift)));
+            for (int k = 0; k < 4 * W; ++k) acc[k] += LT::widen(gbuf[tf % (kLag + 1)][k]);
           }
         }
       }
@@ -1047,6 +1289,113 @@ __global__ void __launch_bounds__(kMultiThreads) apply_multi_kernel(const __grid
     for (int c = 0; c < C; ++c)
       p.out[obj_of(k) * C + c] = p.last ? __dadd_rn(__dmul_rn(acc[k][c], p.scale), p.bias) : acc[k][c];
   }
+}
+
+// ---------------------------------------------------------------------------
+// K4s: sliced multi-output apply.  K4 gathers each object's C-value record with
+// 16-byte loads from one lane, so every warp load touches 32 random L2 lines and a
+// record costs 3 line lookups (the L1 takes about one line per clock: config 5 ran at
+// ~3 lookups per object-tree).  Here the record lives in one aligned slot (64 bytes at
+// C = 10 fp32, never straddling a 128-byte line) and S = ceil(C / V) lanes fetch it
+// together, V values (8 bytes) each: a warp load covers ~32 / S objects with one line
+// each.  Index work stays SWAR (lane = 4 objects of a bucket word, as K4); the leaf
+// index of the lane-word's byte k is then shuffled to the lanes gathering that object:
+// for byte k the warp's 32 objects x S pairs are exactly S loads of 32 lanes, lane l of
+// load s handling object (32 s + l) / S, pair (32 s + l) % S -- so the shuffled word is
+// the same byte k for every lane of a load.  Accumulators: 4 x S x V binary64 per lane
+// (80 registers at C = 10), folded in tree order per (object, output) as K4.
+template <int LEAF, int C> struct MultiSlice {
+  static constexpr int kLS = LEAF == 0 ? 8 : 4;                 // bytes per value
+  static constexpr int V = 8 / kLS;                             // values per lane load
+  static constexpr int S = (C + V - 1) / V;                     // lanes per object
+  static constexpr int kRec = S * 8;                            // used bytes of a slot
+  static constexpr int kSlot = kRec <= 16 ? 16 : kRec <= 32 ? 32 : kRec <= 64 ? 64 : 128;
+};
+
+template <int DI, int CMP, int LEAF, int C>
+__global__ void __launch_bounds__(128) apply_multi_slice_kernel(const __grid_constant__ MultiParams p) {
+  using MS = MultiSlice<LEAF, C>;
+  constexpr int S = MS::S, V = MS::V;
+  static_assert(S <= 32, "slices per object");
+  using leaf_t = typename LeafT<LEAF>::T;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int word = threadIdx.x;  // bucket word of this lane within the 512-object tile
+  const int64_t tile_idx = blockIdx.x;
+  const uint8_t* qrow0 = p.q + tile_idx * (int64_t)p.n_features * p.tile + 4 * word;
+  const int64_t blk = tile_idx * p.tile + warp * 128;  // the warp's 128-object block
+  // gather slots: load s of byte k -> object 32 k + j_s, pair q_s
+  int src[S];
+  uint32_t qoff[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int g = 32 * s + lane;
+    src[s] = g / S;
+    qoff[s] = (uint32_t)(g % S) * 8u;
+  }
+  auto out_index = [&](int k, int s, int v) -> int64_t {  // -1: padding
+    const int g = 32 * s + lane;
+    const int c = (g % S) * V + v;
+    const int64_t o = blk + 32 * k + g / S;
+    return (c < C && o < p.n) ? o * C + c : -1;
+  };
+  double acc[4][S][V];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const int64_t i = out_index(k, s, v);
+        acc[k][s][v] = (p.first || i < 0) ? 0.0 : p.out[i];
+      }
+  for (int t = p.tree_begin; t < p.tree_end; ++t) {
+    const uint2* ds = reinterpret_cast<const uint2*>(p.desc) + (size_t)t * DI;
+    uint32_t lo = 0, hi = 0;
+#pragma unroll
+    for (int d = 0; d < DI; ++d) {
+      const uint2 dd = __ldg(ds + d);  // warp-uniform address: one broadcast
+      uint32_t b7;
+      if constexpr (CMP == 7) {
+        b7 = __ldg(reinterpret_cast<const uint32_t*>(qrow0 + dd.x)) + dd.y;
+      } else {
+        const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(qrow0 + (dd.x >> 8)));
+        b7 = maj3((w & 0x7f7f7f7fu) + (__byte_perm(dd.x, 0u, 0x0000u) & 0x7f7f7f7fu), w, dd.y);
+      }
+      if (d < 8) lo |= (b7 >> (7 - d)) & (0x01010101u << d);
+      else hi |= (b7 >> (15 - d)) & (0x01010101u << (d - 8));
+    }
+    const unsigned char* tab = reinterpret_cast<const unsigned char*>(p.leaves) + ((size_t)t << DI) * MS::kSlot;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      // leaf index of byte k (object 32 k + lane): low 8 bits from lo, the rest from hi
+      const uint32_t mine = DI > 8 ? (__byte_perm(lo, hi, (uint32_t)(k | ((4 + k) << 4))) & 0xffffu)
+                                   : __byte_perm(lo, 0u, 0x4440u | k);
+      uint2 rv[S];
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const uint32_t idx = __shfl_sync(0xffffffffu, mine, src[s]);
+        rv[s] = __ldg(reinterpret_cast<const uint2*>(tab + (size_t)idx * MS::kSlot + qoff[s]));
+      }
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        if constexpr (LEAF == 0) {
+          acc[k][s][0] += __hiloint2double((int)rv[s].y, (int)rv[s].x);
+        } else {
+          acc[k][s][0] += (double)__uint_as_float(rv[s].x);
+          acc[k][s][V - 1] += (double)__uint_as_float(rv[s].y);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const int64_t i = out_index(k, s, v);
+        if (i >= 0) p.out[i] = p.last ? __dadd_rn(__dmul_rn(acc[k][s][v], p.scale), p.bias) : acc[k][s][v];
+      }
 }
 
 }  // namespace obt

@@ -61,6 +61,13 @@ class DeviceModel:
         self.leaf_storage = _native.LEAF_STORAGE_NAMES[info[5].value]
         self.compare_mode = info[6].value
 
+    def quantize_kernel(self) -> tuple[str, int]:
+        """The predict path's quantize search for TMA-eligible inputs: ("cells", compares
+        per value) for the cell-table kernel, ("eytzinger", levels) otherwise."""
+        kind, param = ctypes.c_int32(), ctypes.c_int32()
+        _native.check(self._lib.obt_model_quantize_kernel(self.handle, ctypes.byref(kind), ctypes.byref(param)))
+        return ("cells" if kind.value == 1 else "eytzinger", param.value)
+
     def close(self) -> None:
         if getattr(self, "handle", None) and self.handle.value:
             self._lib.obt_model_destroy(self.handle)
@@ -156,6 +163,10 @@ class Evaluator:
             device = torch.cuda.current_device() if torch.cuda.is_available() else 0
         self.device = int(device)
         self._dev = self.tables.device_model(self.precision, self.device)
+
+    def quantize_kernel(self) -> tuple[str, int]:
+        """("cells", compares) or ("eytzinger", levels): the predict path's quantize search."""
+        return self._dev.quantize_kernel()
 
     @property
     def model(self) -> ObliviousModel:

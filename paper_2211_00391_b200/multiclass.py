@@ -129,6 +129,12 @@ class MultiOutputEvaluator:
         del keep
         self._lib, self.handle = lib, handle
 
+    def quantize_kernel(self) -> tuple[str, int]:
+        """("cells", compares) or ("eytzinger", levels): the predict path's quantize search."""
+        kind, param = ctypes.c_int32(), ctypes.c_int32()
+        _native.check(self._lib.obt_model_quantize_kernel(self.handle, ctypes.byref(kind), ctypes.byref(param)))
+        return ("cells" if kind.value == 1 else "eytzinger", param.value)
+
     def predict_device(self, x, layout: Layout = Layout.OBJECT_MAJOR, out=None, workspace=None):
         """float32 CUDA tensor [n][F] (or [F][n]) -> float64 CUDA tensor [n][C]."""
         import torch

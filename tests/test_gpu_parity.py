@@ -242,10 +242,15 @@ def test_descriptor_sources_and_multi_launch_fold(monkeypatch, source, strategy)
     assert np.array_equal(idx, oracle.leaf_indices(fm, oracle.quantize(fm, x))[1290:1400])
 
 
-@pytest.mark.parametrize("D,C,F,B", [(10, 10, 40, 254), (6, 3, 17, 64), (8, 16, 9, 128), (3, 2, 5, 7)])
-def test_multi_output_bit_exact(D, C, F, B):
-    """Multi-output (config 5 shape family): K4 against the oracle restatement."""
+@pytest.mark.parametrize("kernel", ["slice", "k4"])
+@pytest.mark.parametrize("D,C,F,B", [(10, 10, 40, 254), (6, 3, 17, 64), (8, 16, 9, 128), (3, 2, 5, 7), (12, 7, 13, 30)])
+def test_multi_output_bit_exact(monkeypatch, kernel, D, C, F, B):
+    """Multi-output (config 5 shape family): K4 (default) and K4s (sliced records,
+    OBT_MULTI_SLICE=1) against the oracle restatement, both layouts, with the binary64
+    leaf tables too (OBT_LEAF_STORAGE=64)."""
     from paper_2211_00391_b200 import multiclass
+
+    monkeypatch.setenv("OBT_MULTI_SLICE", "1" if kernel == "slice" else "0")
 
     spec = synthetic.WorkloadSpec("m", 1, F, B, 57, D, 0.01, n_outputs=C, cfg=5)
     arrays = synthetic.model_arrays(spec, seed=D * 100 + C, affine=True)
@@ -261,6 +266,9 @@ def test_multi_output_bit_exact(D, C, F, B):
     assert np.array_equal(got, want)
     dev = ev.predict_device(torch.from_numpy(np.ascontiguousarray(x.T)).cuda(), obt.Layout.FEATURE_MAJOR).cpu().numpy()
     assert np.array_equal(dev, want)
+    monkeypatch.setenv("OBT_LEAF_STORAGE", "64")
+    ev64 = multiclass.MultiOutputEvaluator(model)
+    assert np.array_equal(ev64.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR)), want)
 
 
 def test_multi_output_tree_shard_partials_sum_to_prediction():
@@ -555,3 +563,84 @@ def test_predict_captures_into_cuda_graph():
     g.replay()
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy(), oracle.evaluate_scalar(fm, x2))
+
+
+def _border_model(border_sets, T, D, seed):
+    """A model over hand-made border sets (one feature each), random splits."""
+    rng = np.random.default_rng(seed)
+    feats = tuple(obt.FloatFeatureBorders(f, np.asarray(b, np.float32)) for f, b in enumerate(border_sets))
+    usable = [f for f, b in enumerate(border_sets) if len(b)]
+    trees = []
+    for _ in range(T):
+        splits = []
+        for _ in range(D):
+            f = int(rng.choice(usable))
+            splits.append(obt.SplitCondition(f, int(rng.integers(0, len(border_sets[f])))))
+        trees.append(obt.ObliviousTree(depth=D, splits=tuple(splits), leaf_values=rng.normal(0, 0.1, 1 << D).astype(np.float32)))
+    return obt.ObliviousModel(feats, tuple(trees), scale=1.0, bias=0.0)
+
+
+def _edge_values(border_sets, n, seed):
+    """Values at, just above and just below every border, plus NaN, +-inf, +-0, denormals."""
+    rng = np.random.default_rng(seed)
+    F = len(border_sets)
+    x = np.empty((n, F), np.float32)
+    for f, b in enumerate(border_sets):
+        b = np.asarray(b, np.float32)
+        pool = [np.float32(np.nan), np.float32(np.inf), np.float32(-np.inf), np.float32(0.0), np.float32(-0.0),
+                np.float32(2.0**-140), np.float32(-(2.0**-140)), np.float32(3.4e38), np.float32(-3.4e38)]
+        if b.size:
+            pool += list(b) + list(np.nextafter(b, np.float32(np.inf))) + list(np.nextafter(b, np.float32(-np.inf)))
+            lo, hi = float(b.min()), float(b.max())
+            span = max(hi - lo, 1.0)
+            pool += list(rng.uniform(lo - span, hi + span, 64).astype(np.float32))
+        x[:, f] = np.asarray(pool, np.float32)[rng.integers(0, len(pool), n)]
+    return x
+
+
+_LUT_SETS = {
+    # cfg-like quantile / uniform / integer / lognormal sets, singletons, clustered borders
+    # (up to 4 per cell), denormal and signed-zero borders, an empty feature
+    "mixed": [
+        np.sort(np.random.default_rng(1).normal(0, 1, 64)).astype(np.float32),
+        (100 * np.arange(1, 65) / 65).astype(np.float32),
+        np.unique(np.floor(1000 * np.arange(1, 129) / 129)).astype(np.float32),
+        np.unique(np.exp(np.random.default_rng(2).normal(0, 1, 40))).astype(np.float32),
+        np.array([0.5], np.float32),
+        np.array([-0.0, 2.0**-140, 1.0], np.float32),
+        np.array([0.0, 1e-3, 2e-3, 3e-3, 10.0], np.float32),   # 4 borders share the lowest cell
+        np.array([-5.0, -4.999999, -4.999998, 7.0], np.float32),
+    ],
+    # ranges the affine cell map cannot hold: the Eytzinger search runs instead
+    "fallback": [
+        np.array([1e6, 1000001.0, 1000002.0], np.float32),  # lo * s ~ 2.5e8 > 2^23
+        np.sort(np.random.default_rng(3).normal(0, 1, 16)).astype(np.float32),
+    ],
+    # five borders in one cell: more than the cell kernel's 4 compares
+    "crowded": [
+        np.array([0.0, 1e-6, 2e-6, 3e-6, 4e-6, 100.0], np.float32),
+        np.array([1.0, 2.0], np.float32),
+    ],
+}
+
+
+@pytest.mark.parametrize("name,expect", [("mixed", "cells"), ("fallback", "eytzinger"), ("crowded", "eytzinger")])
+def test_cell_table_quantize_edges(monkeypatch, name, expect):
+    """K1L (cell-table quantize) against the oracle on values at, next to and far from
+    every border, NaN, +-inf, signed zeros and denormals; and equal to the Eytzinger
+    search (OBT_QUANT_LUT=0) bucket for bucket through the predictions and leaf indices."""
+    monkeypatch.setenv("OBT_QUANT_LUT", "1")  # K1L wherever its tables exist (not only where it is faster)
+    sets = [np.asarray(b, np.float32) for b in _LUT_SETS[name]]
+    pad = (-len(sets)) % 4  # F % 4 == 0: the TMA-staged path
+    sets += [np.array([0.25 * (i + 1)], np.float32) for i in range(pad)]
+    model = _border_model(sets, T=40, D=6, seed=len(sets))
+    ev = obt.Evaluator(model)
+    dm = ev.tables.device_model(ev.precision, ev.device)
+    x = _edge_values(sets, 5000, seed=11)
+    fm = oracle.flatten(model)
+    want = oracle.evaluate_scalar(fm, x, oracle.OBJECT_MAJOR, oracle.BINARY64)
+    got = ev.predict_device(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.array_equal(got, want), int(np.count_nonzero(got != want))
+    assert dm.quantize_kernel()[0] == expect
+    monkeypatch.setenv("OBT_QUANT_LUT", "0")
+    assert np.array_equal(ev.predict_device(torch.from_numpy(x).cuda()).cpu().numpy(), want)
