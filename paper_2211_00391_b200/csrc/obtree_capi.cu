@@ -832,8 +832,27 @@ int launch_multi(obt_model* m, const uint8_t* q, int64_t n, double* out, cudaStr
   p.scale = m->scale;
   p.bias = m->bias;
   void* kargs[] = {&p};
-  const dim3 grid((unsigned)((n + kMultiTile - 1) / kMultiTile)), block(m->multi_slice ? kMultiTile / 4 : obt::kMultiThreads);
-  CUDA_TRY(cudaLaunchKernel(fn, grid, block, kargs, 0, stream));
+  const int threads = m->multi_slice ? kMultiTile / 4 : obt::kMultiThreads;
+  const int64_t n_tiles = (n + kMultiTile - 1) / kMultiTile;
+  // persistent grid: the resident CTAs loop over the tiles (OBT_MULTI_PERSIST=0: one CTA per tile)
+  int per_sm = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0));
+  const char* pe = getenv("OBT_MULTI_PERSIST");
+  const int64_t resident = (int64_t)std::max(per_sm, 1) * m->sm_count;
+  const int64_t blocks = (pe && !strcmp(pe, "0")) ? n_tiles : std::min<int64_t>(n_tiles, resident);
+  const dim3 grid((unsigned)blocks), block(threads);
+  // residency cap (experiment knob): reserving shared memory limits the CTAs per SM, so
+  // fewer objects' bucket rows (F bytes each) compete for L2
+  size_t smem = 0;
+  if (const char* e = getenv("OBT_MULTI_CTAS_PER_SM")) {
+    const int k = atoi(e);
+    if (k > 0) {
+      smem = (size_t)(m->smem_optin + 1024) / (size_t)k - 1024;
+      if (smem > (size_t)m->smem_optin) smem = (size_t)m->smem_optin;
+      CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, m->smem_optin));
+    }
+  }
+  CUDA_TRY(cudaLaunchKernel(fn, grid, block, kargs, smem, stream));
   ++g_launches;
   return OBT_OK;
 }

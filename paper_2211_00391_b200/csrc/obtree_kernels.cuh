@@ -1195,99 +1195,142 @@ __host__ __device__ constexpr int multi_record_values(int leaf, int c) {
 #ifndef OBT_MULTI_PF
 #define OBT_MULTI_PF 0  // measured no gain at cfg5 (L2 prefetch 4-16 trees ahead)
 #endif
+#ifndef OBT_MULTI_AHEAD
+// K4: bucket words requested one tree ahead.  Measured at config 5 (128 registers):
+// 590 ms against 565 ms without -- the kernel is bound by how many record round trips
+// the SM keeps in flight, and the held words cost more than the overlap gains
+#define OBT_MULTI_AHEAD 0
+#endif
 
+#ifndef OBT_MULTI_MINB
+// 4 resident CTAs per SM (a 128-register cap) up to C = 10: uncapped, ptxas took 196
+// registers and config 5 ran at 767 ms instead of 565 ms (2 CTAs, half the record
+// loads in flight).  More outputs need the accumulator registers (fewer CTAs).
+#define OBT_MULTI_MINB 4
+#endif
+__host__ __device__ constexpr int multi_min_blocks(int leaf, int c) {
+  return leaf == 0 ? (c <= 5 ? OBT_MULTI_MINB : 2) : (c <= 10 ? OBT_MULTI_MINB : c <= 12 ? 3 : 2);
+}
 template <int DI, int CMP, int LEAF, int C>
-__global__ void __launch_bounds__(kMultiThreads) apply_multi_kernel(const __grid_constant__ MultiParams p) {
+__global__ void __launch_bounds__(kMultiThreads, multi_min_blocks(LEAF, C)) apply_multi_kernel(const __grid_constant__ MultiParams p) {
   using leaf_t = typename LeafT<LEAF>::T;
   constexpr int CP = multi_record_values(LEAF, C);  // record stride: 32-byte rows (fp32), 16-byte (fp64)
   constexpr int OPL = kMultiOPL;
   const int word = threadIdx.x / kMultiLanesPerWord, sub = threadIdx.x % kMultiLanesPerWord;
-  const int64_t tile_idx = blockIdx.x;
-  const uint8_t* qrow0 = p.q + tile_idx * (int64_t)p.n_features * p.tile + 4 * word;
-  const int64_t tile_base = tile_idx * p.tile;
-  auto obj_of = [&](int k) { return word_object(tile_base, word, sub * OPL + k); };  // k < OPL
-  double acc[OPL][C];
+  // persistent CTAs (grid = resident CTAs): every CTA starts its next tile when the
+  // previous one ends, so all CTAs walk the trees nearly in step and the active window of
+  // leaf records stays L2-resident (one launch of 31250 CTAs kept CTAs at every tree
+  // position at once: all 4000 trees' records, 197 MB, competed for L2 at config 5)
+  const int64_t n_tiles = (p.n + p.tile - 1) / p.tile;
+  for (int64_t tile_idx = blockIdx.x; tile_idx < n_tiles; tile_idx += gridDim.x) {
+    const uint8_t* qrow0 = p.q + tile_idx * (int64_t)p.n_features * p.tile + 4 * word;
+    const int64_t tile_base = tile_idx * p.tile;
+    auto obj_of = [&](int k) { return word_object(tile_base, word, sub * OPL + k); };  // k < OPL
+    double acc[OPL][C];
 #pragma unroll
-  for (int k = 0; k < OPL; ++k)
+    for (int k = 0; k < OPL; ++k)
 #pragma unroll
-    for (int c = 0; c < C; ++c)
-      acc[k][c] = (p.first || obj_of(k) >= p.n) ? 0.0 : p.out[obj_of(k) * C + c];
-  for (int t = p.tree_begin; t < p.tree_end; ++t) {
-    if (OBT_MULTI_PF > 0 && t + OBT_MULTI_PF < p.tree_end) {
-      // the bucket rows of a tree OBT_MULTI_PF ahead into L2: the tile's rows do not stay
-      // L2-resident between uses (F = 1000 bytes per object), so without this every
-      // tree's index waits on HBM
-      const uint2* dp = reinterpret_cast<const uint2*>(p.desc) + (size_t)(t + OBT_MULTI_PF) * DI;
+      for (int c = 0; c < C; ++c)
+        acc[k][c] = (p.first || obj_of(k) >= p.n) ? 0.0 : p.out[obj_of(k) * C + c];
+    // OBT_MULTI_AHEAD: bucket words (and descriptors) of tree t + 1 requested before tree
+    // t's records are folded (27% of config 5's long-scoreboard stalls wait on bucket
+    // words, 66% on records; measured slower, see the define)
+    uint32_t wnext[DI];
+    uint2 dnext[DI];
+    auto load_words = [&](int t, uint32_t (&w)[DI], uint2 (&dv)[DI]) {
+      const uint2* ds = reinterpret_cast<const uint2*>(p.desc) + (size_t)t * DI;
 #pragma unroll
       for (int d = 0; d < DI; ++d) {
-        const uint32_t off = CMP == 7 ? __ldg(&dp[d].x) : (__ldg(&dp[d].x) >> 8);
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(qrow0 + off));
+        dv[d] = __ldg(ds + d);  // warp-uniform address: one broadcast
+        w[d] = __ldg(reinterpret_cast<const uint32_t*>(qrow0 + (CMP == 7 ? dv[d].x : (dv[d].x >> 8))));
       }
-    }
-    const uint2* ds = reinterpret_cast<const uint2*>(p.desc) + (size_t)t * DI;
-    uint32_t lo = 0, hi = 0;
+    };
+    if (OBT_MULTI_AHEAD && p.tree_begin < p.tree_end) load_words(p.tree_begin, wnext, dnext);
+    for (int t = p.tree_begin; t < p.tree_end; ++t) {
+      uint32_t wcur[DI];
+      uint2 dcur[DI];
+      if (OBT_MULTI_AHEAD) {
 #pragma unroll
-    for (int d = 0; d < DI; ++d) {
-      const uint2 dd = __ldg(ds + d);  // warp-uniform address: one broadcast
-      uint32_t b7;
-      if constexpr (CMP == 7) {
-        b7 = __ldg(reinterpret_cast<const uint32_t*>(qrow0 + dd.x)) + dd.y;
+        for (int d = 0; d < DI; ++d) { wcur[d] = wnext[d]; dcur[d] = dnext[d]; }
+        if (t + 1 < p.tree_end) load_words(t + 1, wnext, dnext);
       } else {
-        const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(qrow0 + (dd.x >> 8)));
-        b7 = maj3((w & 0x7f7f7f7fu) + (__byte_perm(dd.x, 0u, 0x0000u) & 0x7f7f7f7fu), w, dd.y);
+        load_words(t, wcur, dcur);
       }
-      if (d < 8) lo |= (b7 >> (7 - d)) & (0x01010101u << d);
-      else hi |= (b7 >> (15 - d)) & (0x01010101u << (d - 8));
-    }
-    const leaf_t* tab = reinterpret_cast<const leaf_t*>(p.leaves) + ((size_t)t << DI) * CP;
-    // all 4 objects' records are requested before any is consumed: the L2 round trips
-    // overlap (each record is CP values in 16-byte rows)
-    if constexpr (LEAF == 1 && OBT_MULTI_ROW32) {
-      // fp32 records: one 256-bit load per 32-byte row
-      constexpr int kRows = (C + 7) / 8;
-      float rec[OPL][kRows * 8];
+      if (OBT_MULTI_PF > 0 && t + OBT_MULTI_PF < p.tree_end) {
+        // the bucket rows of a tree OBT_MULTI_PF ahead into L2: the tile's rows do not stay
+        // L2-resident between uses (F = 1000 bytes per object), so without this every
+        // tree's index waits on HBM
+        const uint2* dp = reinterpret_cast<const uint2*>(p.desc) + (size_t)(t + OBT_MULTI_PF) * DI;
 #pragma unroll
-      for (int k = 0; k < OPL; ++k) {
-        const int kb = sub * OPL + k;  // byte of the word
-        const uint32_t idx = ((lo >> (8 * kb)) & 0xffu) | (DI > 8 ? ((hi >> (8 * kb)) & 0xffu) << 8 : 0u);
-        const float* r = reinterpret_cast<const float*>(tab) + (size_t)idx * CP;
-#pragma unroll
-        for (int i = 0; i < kRows; ++i) {
-          float* d = rec[k] + 8 * i;
-          asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                       : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3]), "=f"(d[4]), "=f"(d[5]), "=f"(d[6]), "=f"(d[7])
-                       : "l"(r + 8 * i));
+        for (int d = 0; d < DI; ++d) {
+          const uint32_t off = CMP == 7 ? __ldg(&dp[d].x) : (__ldg(&dp[d].x) >> 8);
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(qrow0 + off));
         }
       }
+      uint32_t lo = 0, hi = 0;
 #pragma unroll
-      for (int k = 0; k < OPL; ++k)
-#pragma unroll
-        for (int c = 0; c < C; ++c) acc[k][c] += (double)rec[k][c];
-    } else {
-      constexpr int kRows = CP * (int)sizeof(leaf_t) / 16;
-      uint4 rec[OPL][kRows];
-#pragma unroll
-      for (int k = 0; k < OPL; ++k) {
-        const int kb = sub * OPL + k;  // byte of the word
-        const uint32_t idx = ((lo >> (8 * kb)) & 0xffu) | (DI > 8 ? ((hi >> (8 * kb)) & 0xffu) << 8 : 0u);
-        const uint4* r = reinterpret_cast<const uint4*>(tab + (size_t)idx * CP);
-#pragma unroll
-        for (int i = 0; i < kRows; ++i) rec[k][i] = __ldg(r + i);
+      for (int d = 0; d < DI; ++d) {
+        const uint2 dd = dcur[d];
+        const uint32_t w = wcur[d];
+        uint32_t b7;
+        if constexpr (CMP == 7) {
+          b7 = w + dd.y;
+        } else {
+          b7 = maj3((w & 0x7f7f7f7fu) + (__byte_perm(dd.x, 0u, 0x0000u) & 0x7f7f7f7fu), w, dd.y);
+        }
+        if (d < 8) lo |= (b7 >> (7 - d)) & (0x01010101u << d);
+        else hi |= (b7 >> (15 - d)) & (0x01010101u << (d - 8));
       }
+      const leaf_t* tab = reinterpret_cast<const leaf_t*>(p.leaves) + ((size_t)t << DI) * CP;
+      // all 4 objects' records are requested before any is consumed: the L2 round trips
+      // overlap (each record is CP values in 16-byte rows)
+      if constexpr (LEAF == 1 && OBT_MULTI_ROW32) {
+        // fp32 records: one 256-bit load per 32-byte row
+        constexpr int kRows = (C + 7) / 8;
+        float rec[OPL][kRows * 8];
 #pragma unroll
-      for (int k = 0; k < OPL; ++k) {
-        const leaf_t* v = reinterpret_cast<const leaf_t*>(rec[k]);
+        for (int k = 0; k < OPL; ++k) {
+          const int kb = sub * OPL + k;  // byte of the word
+          const uint32_t idx = ((lo >> (8 * kb)) & 0xffu) | (DI > 8 ? ((hi >> (8 * kb)) & 0xffu) << 8 : 0u);
+          const float* r = reinterpret_cast<const float*>(tab) + (size_t)idx * CP;
 #pragma unroll
-        for (int c = 0; c < C; ++c) acc[k][c] += (double)v[c];
+          for (int i = 0; i < kRows; ++i) {
+            float* d = rec[k] + 8 * i;
+            asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                         : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3]), "=f"(d[4]), "=f"(d[5]), "=f"(d[6]), "=f"(d[7])
+                         : "l"(r + 8 * i));
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < OPL; ++k)
+#pragma unroll
+          for (int c = 0; c < C; ++c) acc[k][c] += (double)rec[k][c];
+      } else {
+        constexpr int kRows = CP * (int)sizeof(leaf_t) / 16;
+        uint4 rec[OPL][kRows];
+#pragma unroll
+        for (int k = 0; k < OPL; ++k) {
+          const int kb = sub * OPL + k;  // byte of the word
+          const uint32_t idx = ((lo >> (8 * kb)) & 0xffu) | (DI > 8 ? ((hi >> (8 * kb)) & 0xffu) << 8 : 0u);
+          const uint4* r = reinterpret_cast<const uint4*>(tab + (size_t)idx * CP);
+#pragma unroll
+          for (int i = 0; i < kRows; ++i) rec[k][i] = __ldg(r + i);
+        }
+#pragma unroll
+        for (int k = 0; k < OPL; ++k) {
+          const leaf_t* v = reinterpret_cast<const leaf_t*>(rec[k]);
+#pragma unroll
+          for (int c = 0; c < C; ++c) acc[k][c] += (double)v[c];
+        }
       }
     }
-  }
 #pragma unroll
-  for (int k = 0; k < OPL; ++k) {
-    if (obj_of(k) >= p.n) continue;
+    for (int k = 0; k < OPL; ++k) {
+      if (obj_of(k) >= p.n) continue;
 #pragma unroll
-    for (int c = 0; c < C; ++c)
-      p.out[obj_of(k) * C + c] = p.last ? __dadd_rn(__dmul_rn(acc[k][c], p.scale), p.bias) : acc[k][c];
+      for (int c = 0; c < C; ++c)
+        p.out[obj_of(k) * C + c] = p.last ? __dadd_rn(__dmul_rn(acc[k][c], p.scale), p.bias) : acc[k][c];
+    }
   }
 }
 
@@ -1320,82 +1363,88 @@ __global__ void __launch_bounds__(128) apply_multi_slice_kernel(const __grid_con
   using leaf_t = typename LeafT<LEAF>::T;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int word = threadIdx.x;  // bucket word of this lane within the 512-object tile
-  const int64_t tile_idx = blockIdx.x;
-  const uint8_t* qrow0 = p.q + tile_idx * (int64_t)p.n_features * p.tile + 4 * word;
-  const int64_t blk = tile_idx * p.tile + warp * 128;  // the warp's 128-object block
-  // gather slots: load s of byte k -> object 32 k + j_s, pair q_s
-  int src[S];
-  uint32_t qoff[S];
+  // persistent CTAs (grid = resident CTAs): every CTA starts its next tile when the
+  // previous one ends, so all CTAs walk the trees nearly in step and the active window of
+  // leaf records stays L2-resident (one launch of 31250 CTAs kept CTAs at every tree
+  // position at once: all 4000 trees' records, 197 MB, competed for L2 at config 5)
+  const int64_t n_tiles = (p.n + p.tile - 1) / p.tile;
+  for (int64_t tile_idx = blockIdx.x; tile_idx < n_tiles; tile_idx += gridDim.x) {
+    const uint8_t* qrow0 = p.q + tile_idx * (int64_t)p.n_features * p.tile + 4 * word;
+    const int64_t blk = tile_idx * p.tile + warp * 128;  // the warp's 128-object block
+    // gather slots: load s of byte k -> object 32 k + j_s, pair q_s
+    int src[S];
+    uint32_t qoff[S];
 #pragma unroll
-  for (int s = 0; s < S; ++s) {
-    const int g = 32 * s + lane;
-    src[s] = g / S;
-    qoff[s] = (uint32_t)(g % S) * 8u;
-  }
-  auto out_index = [&](int k, int s, int v) -> int64_t {  // -1: padding
-    const int g = 32 * s + lane;
-    const int c = (g % S) * V + v;
-    const int64_t o = blk + 32 * k + g / S;
-    return (c < C && o < p.n) ? o * C + c : -1;
-  };
-  double acc[4][S][V];
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-#pragma unroll
-    for (int s = 0; s < S; ++s)
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        const int64_t i = out_index(k, s, v);
-        acc[k][s][v] = (p.first || i < 0) ? 0.0 : p.out[i];
-      }
-  for (int t = p.tree_begin; t < p.tree_end; ++t) {
-    const uint2* ds = reinterpret_cast<const uint2*>(p.desc) + (size_t)t * DI;
-    uint32_t lo = 0, hi = 0;
-#pragma unroll
-    for (int d = 0; d < DI; ++d) {
-      const uint2 dd = __ldg(ds + d);  // warp-uniform address: one broadcast
-      uint32_t b7;
-      if constexpr (CMP == 7) {
-        b7 = __ldg(reinterpret_cast<const uint32_t*>(qrow0 + dd.x)) + dd.y;
-      } else {
-        const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(qrow0 + (dd.x >> 8)));
-        b7 = maj3((w & 0x7f7f7f7fu) + (__byte_perm(dd.x, 0u, 0x0000u) & 0x7f7f7f7fu), w, dd.y);
-      }
-      if (d < 8) lo |= (b7 >> (7 - d)) & (0x01010101u << d);
-      else hi |= (b7 >> (15 - d)) & (0x01010101u << (d - 8));
+    for (int s = 0; s < S; ++s) {
+      const int g = 32 * s + lane;
+      src[s] = g / S;
+      qoff[s] = (uint32_t)(g % S) * 8u;
     }
-    const unsigned char* tab = reinterpret_cast<const unsigned char*>(p.leaves) + ((size_t)t << DI) * MS::kSlot;
+    auto out_index = [&](int k, int s, int v) -> int64_t {  // -1: padding
+      const int g = 32 * s + lane;
+      const int c = (g % S) * V + v;
+      const int64_t o = blk + 32 * k + g / S;
+      return (c < C && o < p.n) ? o * C + c : -1;
+    };
+    double acc[4][S][V];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      // leaf index of byte k (object 32 k + lane): low 8 bits from lo, the rest from hi
-      const uint32_t mine = DI > 8 ? (__byte_perm(lo, hi, (uint32_t)(k | ((4 + k) << 4))) & 0xffffu)
-                                   : __byte_perm(lo, 0u, 0x4440u | k);
-      uint2 rv[S];
+    for (int k = 0; k < 4; ++k)
 #pragma unroll
-      for (int s = 0; s < S; ++s) {
-        const uint32_t idx = __shfl_sync(0xffffffffu, mine, src[s]);
-        rv[s] = __ldg(reinterpret_cast<const uint2*>(tab + (size_t)idx * MS::kSlot + qoff[s]));
-      }
+      for (int s = 0; s < S; ++s)
 #pragma unroll
-      for (int s = 0; s < S; ++s) {
-        if constexpr (LEAF == 0) {
-          acc[k][s][0] += __hiloint2double((int)rv[s].y, (int)rv[s].x);
+        for (int v = 0; v < V; ++v) {
+          const int64_t i = out_index(k, s, v);
+          acc[k][s][v] = (p.first || i < 0) ? 0.0 : p.out[i];
+        }
+    for (int t = p.tree_begin; t < p.tree_end; ++t) {
+      const uint2* ds = reinterpret_cast<const uint2*>(p.desc) + (size_t)t * DI;
+      uint32_t lo = 0, hi = 0;
+#pragma unroll
+      for (int d = 0; d < DI; ++d) {
+        const uint2 dd = __ldg(ds + d);  // warp-uniform address: one broadcast
+        uint32_t b7;
+        if constexpr (CMP == 7) {
+          b7 = __ldg(reinterpret_cast<const uint32_t*>(qrow0 + dd.x)) + dd.y;
         } else {
-          acc[k][s][0] += (double)__uint_as_float(rv[s].x);
-          acc[k][s][V - 1] += (double)__uint_as_float(rv[s].y);
+          const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(qrow0 + (dd.x >> 8)));
+          b7 = maj3((w & 0x7f7f7f7fu) + (__byte_perm(dd.x, 0u, 0x0000u) & 0x7f7f7f7fu), w, dd.y);
+        }
+        if (d < 8) lo |= (b7 >> (7 - d)) & (0x01010101u << d);
+        else hi |= (b7 >> (15 - d)) & (0x01010101u << (d - 8));
+      }
+      const unsigned char* tab = reinterpret_cast<const unsigned char*>(p.leaves) + ((size_t)t << DI) * MS::kSlot;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        // leaf index of byte k (object 32 k + lane): low 8 bits from lo, the rest from hi
+        const uint32_t mine = DI > 8 ? (__byte_perm(lo, hi, (uint32_t)(k | ((4 + k) << 4))) & 0xffffu)
+                                     : __byte_perm(lo, 0u, 0x4440u | k);
+        uint2 rv[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          const uint32_t idx = __shfl_sync(0xffffffffu, mine, src[s]);
+          rv[s] = __ldg(reinterpret_cast<const uint2*>(tab + (size_t)idx * MS::kSlot + qoff[s]));
+        }
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          if constexpr (LEAF == 0) {
+            acc[k][s][0] += __hiloint2double((int)rv[s].y, (int)rv[s].x);
+          } else {
+            acc[k][s][0] += (double)__uint_as_float(rv[s].x);
+            acc[k][s][V - 1] += (double)__uint_as_float(rv[s].y);
+          }
         }
       }
     }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int s = 0; s < S; ++s)
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const int64_t i = out_index(k, s, v);
+          if (i >= 0) p.out[i] = p.last ? __dadd_rn(__dmul_rn(acc[k][s][v], p.scale), p.bias) : acc[k][s][v];
+        }
   }
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-#pragma unroll
-    for (int s = 0; s < S; ++s)
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        const int64_t i = out_index(k, s, v);
-        if (i >= 0) p.out[i] = p.last ? __dadd_rn(__dmul_rn(acc[k][s][v], p.scale), p.bias) : acc[k][s][v];
-      }
 }
 
 }  // namespace obt
