@@ -352,6 +352,10 @@ void plan_chunks(obt_model* m) {
   const int64_t ring = std::max<int64_t>((int64_t)kStages * per_tree * group, avail - tile_objs * m->n_features);
   int ct = (int)std::max<int64_t>(group, (ring / kStages - 512) / (int64_t)per_tree / group * group);
   ct = std::min(ct, 64);
+  if (const char* e = getenv("OBT_CHUNK_TREES")) {  // tuning override (a multiple of the group)
+    const int v = atoi(e);
+    if (v >= group && v % group == 0) ct = std::min(ct, v);
+  }
   const int groups = (m->n_trees + group - 1) / group;
   if (groups > 0) ct = std::min(ct, groups * group);
   m->chunk_trees = ct;

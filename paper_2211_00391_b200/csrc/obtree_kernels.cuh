@@ -680,11 +680,12 @@ struct ApplyParams {
   double scale, bias;
 };
 
-constexpr int kParamDescWords = 7936;  // 31744 bytes of descriptors + ApplyParams < 32764
+constexpr int kParamDescWords = 8160;  // 32640 bytes of descriptors + ApplyParams (104) <= 32764
 
 template <int DSRC> struct ApplyArgs;
 template <> struct ApplyArgs<0> { ApplyParams p; };
 template <> struct ApplyArgs<1> { ApplyParams p; uint32_t desc[kParamDescWords]; };
+static_assert(sizeof(ApplyArgs<1>) <= 32764, "kernel parameter space");
 
 template <int LEAF> struct LeafT;
 template <> struct LeafT<0> { using T = double; using Acc = double; static constexpr int kShift = 3;
