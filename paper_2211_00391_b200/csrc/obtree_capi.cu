@@ -790,11 +790,26 @@ int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, int tpw, d
       block((unsigned)(obt::kApplyProducerThreads + tile / (4 * k.words) * k.tpw));
   const int per = dsrc ? param_chunks_per_launch(m) : std::max(m->n_chunks, 1);
   const int n_launch = m->n_chunks == 0 ? 1 : (m->n_chunks + per - 1) / per;
+  // Bucket tiles of one region are re-read by every launch.  Launches alternate the tile
+  // order (the first runs last-to-first: the quantize launch wrote the high tiles last),
+  // so each launch's first wave finds the previous pass's last tiles still in L2
+  // (OBT_TILE_ORDER=fwd disables it; cfg2 apply 1.035 -> 1.024 ms).  OBT_L2_NEXT=1 also
+  // has every CTA prefetch the next wave's tile into L2 (measured 1.029 ms: no gain).
+  const char* to = getenv("OBT_TILE_ORDER");
+  const bool alternate = !(to && !strcmp(to, "fwd"));
+  const char* ln = getenv("OBT_L2_NEXT");
+  p.l2_wave = 0;
+  if (ln && !strcmp(ln, "1")) {
+    int per_sm = 1;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, (int)block.x, smem));
+    p.l2_wave = std::max(per_sm, 1) * m->sm_count;
+  }
   for (int l = 0; l < n_launch; ++l) {
     p.chunk_begin = l * per;
     p.chunk_end = std::min(m->n_chunks, (l + 1) * per);
     p.first = l == 0;
     p.last = l == n_launch - 1;
+    p.reverse = alternate && (l % 2 == 0) ? 1 : 0;
     if (dsrc) {
       auto* args = &m->param_args;  // scratch; the driver copies parameters at launch
       std::lock_guard<std::mutex> lock(m->mu);
@@ -894,8 +909,12 @@ Regions plan_regions(const obt_model* m, int64_t n, bool split_ok) {
   Regions r;
   r.count[0] = n;
   r.tile[0] = plan_tile(m, n);
-  const char* e = getenv("OBT_TAIL_SPLIT");
+  const char* e = getenv("OBT_TAIL_SPLIT");  // "0" never, "1" whenever a tail exists
   if (!split_ok || r.tile[0] < 0 || m->n_outputs > 1 || (e && !strcmp(e, "0"))) return r;
+  // Not behind a parameter-bank main region: the tail then runs with shared-memory
+  // descriptors at ~60% of the main region's rate, and one more launch; measured at
+  // cfg2 (3 parameter-bank launches): apply 1.045 ms without the split, 1.081 with it.
+  if (!(e && !strcmp(e, "1")) && use_param_descriptors(m, apply_lanes(m, r.tile[0], false))) return r;
   const int64_t wave = (int64_t)m->sm_count * r.tile[0];
   const int64_t full = n / wave * wave, rest = n - full;
   if (full == 0 || rest == 0) return r;

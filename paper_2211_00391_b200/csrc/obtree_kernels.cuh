@@ -119,6 +119,17 @@ __device__ __forceinline__ void bulk_g2s_split(void* dst, const void* src, uint3
   }
 }
 
+// L2 prefetch of a global range by the TMA engine (no shared-memory destination), in
+// pieces of at most 64 KiB.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  constexpr uint32_t kPiece = 65536;
+  for (uint32_t done = 0; done < bytes; done += kPiece) {
+    const uint32_t len = (bytes - done) < kPiece ? (bytes - done) : kPiece;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(static_cast<const char*>(src) + done), "r"(len)
+                 : "memory");
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Tile layout of the bucket matrix Q[tile][F][TILE]: within each 128-object block of a
 // tile, bucket word p (bytes 4p..4p+3 of every feature row) holds objects p, p+32, p+64,
@@ -677,6 +688,10 @@ struct ApplyParams {
   int32_t n_stages;
   int32_t tree_begin, tree_end;  // index mode: trees written
   int32_t first, last;       // start the fold at 0 / finalize into predictions
+  // tile order and next-wave L2 prefetch: CTA b takes tile (reverse ? grid - 1 - b : b)
+  // and, when l2_wave > 0, prefetches into L2 the bucket tile of CTA b + l2_wave (the
+  // next wave's), so that wave's tile loads hit L2 instead of waiting on HBM
+  int32_t reverse, l2_wave;
   double scale, bias;
 };
 
@@ -800,7 +815,7 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid
 
   const int tid = threadIdx.x;
   const int n_consumer_warps = (blockDim.x - kApplyProducerThreads) / 32;
-  const int64_t tile_idx = blockIdx.x;
+  const int64_t tile_idx = p.reverse ? (int64_t)(gridDim.x - 1 - blockIdx.x) : (int64_t)blockIdx.x;
   const int n_chunks = p.chunk_end - p.chunk_begin;
   if (tid == 0) {
     for (int i = 0; i < p.n_stages; ++i) {
@@ -820,6 +835,11 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid
     if (tid == 0) {
       mbar_expect_tx(tile_bar, p.q_tile_bytes);
       bulk_g2s_split(qtile, p.q + tile_idx * (int64_t)p.q_tile_bytes, p.q_tile_bytes, tile_bar);
+      if (p.l2_wave > 0 && blockIdx.x + (unsigned)p.l2_wave < gridDim.x) {
+        const unsigned nb = blockIdx.x + (unsigned)p.l2_wave;
+        const int64_t nt = p.reverse ? (int64_t)(gridDim.x - 1 - nb) : (int64_t)nb;
+        bulk_prefetch_l2(p.q + nt * (int64_t)p.q_tile_bytes, p.q_tile_bytes);
+      }
       for (int c = 0; c < n_chunks; ++c) {
         const int s = c % p.n_stages;
         if (c >= p.n_stages) mbar_wait(&empty[s], (uint32_t)(c / p.n_stages - 1) & 1u);
@@ -1055,7 +1075,7 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_split_kernel(const 
 
   const int tid = threadIdx.x;
   const int n_consumers = blockDim.x - kApplyProducerThreads;
-  const int64_t tile_idx = blockIdx.x;
+  const int64_t tile_idx = p.reverse ? (int64_t)(gridDim.x - 1 - blockIdx.x) : (int64_t)blockIdx.x;
   const int n_chunks = p.chunk_end - p.chunk_begin;
   if (tid == 0) {
     for (int i = 0; i < p.n_stages; ++i) {
@@ -1071,6 +1091,11 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_split_kernel(const 
     if (tid == 0) {
       mbar_expect_tx(tile_bar, p.q_tile_bytes);
       bulk_g2s_split(qtile, p.q + tile_idx * (int64_t)p.q_tile_bytes, p.q_tile_bytes, tile_bar);
+      if (p.l2_wave > 0 && blockIdx.x + (unsigned)p.l2_wave < gridDim.x) {
+        const unsigned nb = blockIdx.x + (unsigned)p.l2_wave;
+        const int64_t nt = p.reverse ? (int64_t)(gridDim.x - 1 - nb) : (int64_t)nb;
+        bulk_prefetch_l2(p.q + nt * (int64_t)p.q_tile_bytes, p.q_tile_bytes);
+      }
       for (int c = 0; c < n_chunks; ++c) {
         const int s = c % p.n_stages;
         if (c >= p.n_stages) mbar_wait(&empty[s], (uint32_t)(c / p.n_stages - 1) & 1u);

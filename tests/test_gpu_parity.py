@@ -644,3 +644,17 @@ def test_cell_table_quantize_edges(monkeypatch, name, expect):
     assert dm.quantize_kernel()[0] == expect
     monkeypatch.setenv("OBT_QUANT_LUT", "0")
     assert np.array_equal(ev.predict_device(torch.from_numpy(x).cuda()).cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("split", ["1", "0", "auto"])
+def test_tail_split_behind_parameter_bank(monkeypatch, split):
+    """A parameter-bank main region (7-bit compare, one lane per word) skips the tail
+    split by default; forced on (OBT_TAIL_SPLIT=1) or off, predictions stay bit-exact."""
+    if split != "auto":
+        monkeypatch.setenv("OBT_TAIL_SPLIT", split)
+    model = _model(48, 64, 40, 6, seed=77)
+    n = 400001  # past one wave of the largest tile at F = 48
+    x = _features(model, n, seed=78, specials=False)
+    want = oracle.evaluate_scalar(oracle.flatten(model), x)
+    got = obt.Evaluator(model).predict_device(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.array_equal(got, want)

@@ -1,0 +1,13 @@
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu17.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_gpu17.log; grep -E "^E |FAILED" gpurun_out/pytest_gpu17.log | head
+run() { # name config env...
+  name=$1; c=$2; shift 2
+  env "$@" timeout 900 python bench.py --config $c --steps 50 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/b17_$name.json 2>gpurun_out/b17_$name.err
+  python -c "import json;d=json.load(open('gpurun_out/b17_$name.json'));print('$name', round(d['ms_per_step'],4), d['kernels']['apply_ms'], d['gpu_launches'])" 2>&1 | tail -1
+}
+run c2 2 X=1
+run c2_fwd 2 OBT_TILE_ORDER=fwd
+run c2_nol2 2 OBT_L2_NEXT=0
+run c2_plain 2 OBT_TILE_ORDER=fwd OBT_L2_NEXT=0
+run c3 3 X=1
+run c4 4 X=1
+run c4_plain 4 OBT_TILE_ORDER=fwd OBT_L2_NEXT=0
