@@ -723,10 +723,11 @@ int launch_quantize(const obt_model* m, const float* x, int64_t n, int layout, u
       p.lut = lt.d_lut;
       p.lrec = lt.d_rec;
       p.lrec_stride = lt.rec_stride;
+      p.chunk_inner = use_lut ? 1 : 0;
       const size_t smem = use_lut ? obt::kQTSmemFixed + lut_fixed + (size_t)std::min(fc, F) * (obt::kLutCells + lt.rec_stride)
                                   : obt::kQTSmemFixed + (bt.levels > 0 ? (size_t)std::min(fc, F) * bt.pitch * 4 : 16);
       CUDA_TRY(cudaFuncSetAttribute(tfn, cudaFuncAttributeMaxDynamicSharedMemorySize, m->smem_optin));
-      const dim3 grid(blocks, (unsigned)((F + fc - 1) / fc));
+      const dim3 grid(blocks * (unsigned)((F + fc - 1) / fc));
       tfn<<<grid, obt::kQTThreads, smem, stream>>>(map, p);
       ++g_launches;
       CUDA_TRY(cudaGetLastError());
@@ -742,7 +743,7 @@ int launch_quantize(const obt_model* m, const float* x, int64_t n, int layout, u
   // the opt-in maximum, not this launch's size: the attribute is per function and
   // process-wide, so every caller must set the same value (concurrent launches race otherwise)
   CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, m->smem_optin));
-  const dim3 grid(blocks, (unsigned)((F + fc - 1) / fc));
+  const dim3 grid(blocks * (unsigned)((F + fc - 1) / fc));
   fn<<<grid, obt::kQuantThreads, smem, stream>>>(p);
   ++g_launches;
   CUDA_TRY(cudaGetLastError());
