@@ -448,6 +448,7 @@ def run_ours(args, world, rank, local):
                    "leaves": "fp16 (binary32 fold)" if spec.half_leaves else "fp32 values (binary64 fold)",
                    "leaf_storage_on_device": ev.leaf_storage,
                    "quantize_search": quantize_search(ev),
+                   **({"multi_apply": ev.apply_kernel()} if hasattr(ev, "apply_kernel") else {}),
                    "l2": "inputs larger than L2 (features 4NF bytes, buckets NF bytes > 126 MB)",
                    "parallelism": f"objects sharded over {world} GPU(s), no data-path collective",
                    "launch": "CUDA graph replay of one predict" if graph is not None else "stream launches"},

@@ -93,6 +93,11 @@ int obt_model_info(const obt_model* model, int32_t* n_features, int32_t* n_trees
  * quantize.py:171). */
 int obt_model_quantize_kernel(const obt_model* model, int32_t* kind, int32_t* param);
 
+/* Which multi-output apply kernel a model with n_outputs > 1 runs: 0 = K4 (records
+ * gathered from L2), 1 = K4s (sliced records), 2 = K5 (tables and bucket rows staged in
+ * shared memory); -1 for single-output models.  Diagnostics, like the above. */
+int obt_model_multi_kernel(const obt_model* model, int32_t* kind);
+
 /* Bytes of scratch obt_predict_dev needs for n objects (the blocked bucket matrix). */
 int obt_workspace_size(const obt_model* model, int64_t n_objects, size_t* bytes);
 

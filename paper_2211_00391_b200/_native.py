@@ -34,6 +34,7 @@ EXPORTED_SYMBOLS = (
     "obt_model_destroy",
     "obt_model_info",
     "obt_model_quantize_kernel",
+    "obt_model_multi_kernel",
     "obt_workspace_size",
     "obt_predict_dev",
     "obt_predict_host",
@@ -107,6 +108,7 @@ def load_library() -> ctypes.CDLL:
         "obt_model_destroy": (ctypes.c_int, [vp]),
         "obt_model_info": (ctypes.c_int, [vp, p_i32, p_i32, p_i32, p_i32, p_i32, p_i32, p_i32]),
         "obt_model_quantize_kernel": (ctypes.c_int, [vp, p_i32, p_i32]),
+        "obt_model_multi_kernel": (ctypes.c_int, [vp, p_i32]),
         "obt_workspace_size": (ctypes.c_int, [vp, i64, ctypes.POINTER(sz)]),
         "obt_predict_dev": (ctypes.c_int, [vp, vp, i64, i32, vp, vp, sz, vp]),
         "obt_predict_host": (ctypes.c_int, [vp, vp, i64, i32, vp, vp]),

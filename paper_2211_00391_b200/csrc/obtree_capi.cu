@@ -108,6 +108,9 @@ struct obt_model {
   LutTable used_lut;         // cell tables of `used` (K1L), kmax 0 if not applicable
   void* d_multi_leaves = nullptr;   // multi-output records [T][2^DI][CP] (K4) or [T][2^DI] slots (K4s)
   int multi_slice = 0;              // 1: sliced kernel K4s with multi_slot-byte record slots
+  int multi_staged = 0;             // 1: K5 (tree tables + bucket rows staged in shared memory)
+  int staged_stages = 0;
+  uint32_t staged_table_bytes = 0, staged_stage_bytes = 0;
   int multi_slot = 0;
   uint32_t* d_multi_desc = nullptr; // multi-output descriptors [T][DI][2] for kMultiTile
   double scale = 1.0, bias = 0.0;
@@ -528,7 +531,7 @@ constexpr int kMaxParamLaunches = 4;
 // Largest tile (multiple of 256 objects) whose bucket tile fits next to the stage ring;
 // then shrink for small batches so the grid still covers the SMs.
 int plan_tile(const obt_model* m, int64_t n) {
-  if (m->n_outputs > 1) return kMultiTile;  // the multi-output kernel reads buckets through L1
+  if (m->n_outputs > 1) return m->multi_staged ? obt::kStagedTile : kMultiTile;
   const int64_t fixed = 512 + (int64_t)kStages * m->chunk_bytes;
   int64_t tmax = (m->smem_optin - fixed) / m->n_features;
   tmax = std::min<int64_t>(tmax / kTileQuantum * kTileQuantum, 4 * (obt::kApplyMaxThreads - obt::kApplyProducerThreads) / kTileQuantum * kTileQuantum);
@@ -830,7 +833,37 @@ int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, int tpw, d
   return OBT_OK;
 }
 
+int launch_multi_staged(obt_model* m, const uint8_t* q, int64_t n, double* out, cudaStream_t stream) {
+  int di = 0;
+  const void* fn = obt::pick_multi_staged(m->depth_inst, m->compare_mode, m->n_outputs, &di);
+  if (!fn || di != m->depth_inst) return fail(OBT_E_UNSUPPORTED, "no staged multi-output kernel for depth %d", di);
+  obt::StagedParams p{};
+  p.q = q;
+  p.desc = m->d_multi_desc;
+  p.leaves = static_cast<const float*>(m->d_multi_leaves);
+  p.out = out;
+  p.n = n;
+  p.n_features = m->n_features;
+  p.tree_begin = 0;
+  p.tree_end = m->n_trees;
+  p.first = 1;
+  p.last = 1;
+  p.n_stages = m->staged_stages;
+  p.table_bytes = m->staged_table_bytes;
+  p.stage_bytes = m->staged_stage_bytes;
+  p.scale = m->scale;
+  p.bias = m->bias;
+  const size_t smem = 128 + 128 + (size_t)p.n_stages * p.stage_bytes;
+  CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, m->smem_optin));
+  void* kargs[] = {&p};
+  const dim3 grid((unsigned)((n + obt::kStagedTile - 1) / obt::kStagedTile)), block(obt::kStagedThreads);
+  CUDA_TRY(cudaLaunchKernel(fn, grid, block, kargs, smem, stream));
+  ++g_launches;
+  return OBT_OK;
+}
+
 int launch_multi(obt_model* m, const uint8_t* q, int64_t n, double* out, cudaStream_t stream) {
+  if (m->multi_staged) return launch_multi_staged(m, q, n, out, stream);
   int di = 0;
   const void* fn = m->multi_slice ? obt::pick_multi_slice(m->depth_inst, m->compare_mode, m->leaf_storage, m->n_outputs, &di)
                                   : obt::pick_multi(m->depth_inst, m->compare_mode, m->leaf_storage, m->n_outputs, &di);
@@ -1054,6 +1087,24 @@ int obt_model_create(const obt_model_desc* d, int device, obt_model** out) {
     // SM); kept as the OBT_MULTI_SLICE=1 knob
     const char* ms = getenv("OBT_MULTI_SLICE");
     m->multi_slice = (ms && !strcmp(ms, "1")) ? 1 : 0;
+    // K5 (staged tables and rows) for fp32 records, C <= 10, depth <= 10, when at least
+    // two stages (one tree's table + its bucket rows each) fit shared memory
+    {
+      const char* mst = getenv("OBT_MULTI_STAGED");  // A/B knob: 0 = K4
+      const int CPs = (C + 3) / 4 * 4;
+      const uint32_t table = (uint32_t)(per_tree * CPs * 4);
+      const uint32_t stage = (table + (uint32_t)DI * obt::kStagedTile + 127u) & ~127u;
+      const int stages = std::min(8, (int)(((size_t)m->smem_optin - 512) / stage));
+      int sdi = 0;
+      const bool ok = !m->multi_slice && m->leaf_storage == 1 && C <= 10 && stages >= 2 &&
+                      obt::pick_multi_staged(DI, m->compare_mode, C, &sdi) != nullptr && sdi == DI;
+      if (ok && !(mst && !strcmp(mst, "0"))) {
+        m->multi_staged = 1;
+        m->staged_stages = stages;
+        m->staged_table_bytes = table;
+        m->staged_stage_bytes = stage;
+      }
+    }
     m->multi_slot = m->multi_slice ? obt::multi_slice_slot(m->leaf_storage, C)
                                    : obt::multi_record_values(m->leaf_storage, C) * (int)ls;
     std::vector<uint8_t> rec((size_t)std::max(m->n_trees, 1) * per_tree * m->multi_slot, 0);
@@ -1121,6 +1172,12 @@ int obt_model_quantize_kernel(const obt_model* m, int32_t* kind, int32_t* param)
   const bool lut = lut_preferred(m);
   if (kind) *kind = lut ? 1 : 0;
   if (param) *param = lut ? m->used_lut.kmax : m->used.levels;
+  return OBT_OK;
+}
+
+int obt_model_multi_kernel(const obt_model* m, int32_t* kind) {
+  if (!m || !kind) return fail(OBT_E_INVALID, "null argument");
+  *kind = m->n_outputs <= 1 ? -1 : m->multi_staged ? 2 : m->multi_slice ? 1 : 0;
   return OBT_OK;
 }
 

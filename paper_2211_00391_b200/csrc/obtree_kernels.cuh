@@ -1495,4 +1495,131 @@ __global__ void __launch_bounds__(128) apply_multi_slice_kernel(const __grid_con
   }
 }
 
+// ---------------------------------------------------------------------------
+// K5: staged multi-output apply (fp32 records).  K4 gathers records from L2 and is bound
+// by the round trips each SM keeps in flight.  Here one CTA owns a 2048-object tile (16
+// consumer warps, 4 objects per lane, C binary64 accumulators per object in registers)
+// and a producer warp streams, per tree, the tree's whole record table (2^D x CP fp32,
+// 48 KB at config 5) plus the tile's D bucket rows that tree reads (D x 2048 bytes) into
+// an S-stage ring with bulk TMA copies.  Consumers read bucket words and records from
+// shared memory only: one table load serves 2048 objects (24 B of L2 traffic per
+// object-tree instead of a 48-byte record fetch), and every load the fold waits on is a
+// shared-memory load.  Descriptors come from the K4 array ({f * 512, k} / {(f*512) << 8 | k, s}).
+constexpr int kStagedThreadsConsumers = 512;
+constexpr int kStagedTile = 4 * kStagedThreadsConsumers;  // 2048 objects
+constexpr int kStagedThreads = kStagedThreadsConsumers + 32;
+
+struct StagedParams {
+  const uint8_t* q;          // tiled buckets [n_tiles][F][2048]
+  const uint32_t* desc;      // K4 descriptors [T][DI][2] (tile 512 offsets)
+  const float* leaves;       // [T][2^DI][CP] fp32 records
+  double* out;               // [n][C]
+  int64_t n;
+  int32_t n_features;
+  int32_t tree_begin, tree_end;
+  int32_t first, last;
+  int32_t n_stages;
+  uint32_t table_bytes;      // 2^DI * CP * 4
+  uint32_t stage_bytes;      // table_bytes + DI * 2048, 128-byte multiple
+  double scale, bias;
+};
+
+template <int DI, int CMP, int C>
+__global__ void __launch_bounds__(kStagedThreads, 1) apply_multi_staged_kernel(const __grid_constant__ StagedParams p) {
+  constexpr int CP = (C + 3) / 4 * 4;  // fp32 record values (16-byte rows)
+  constexpr int kRows = CP / 4;
+  extern __shared__ __align__(128) unsigned char st_raw[];
+  unsigned char* smem = st_raw + ((128u - (smem_u32(st_raw) & 127u)) & 127u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [S]
+  uint64_t* empty = full + 8;                          // [S]
+  unsigned char* stages = smem + 128;
+  const int tid = threadIdx.x;
+  const int n_trees = p.tree_end - p.tree_begin;
+  if (tid == 0) {
+    for (int i = 0; i < p.n_stages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kStagedThreadsConsumers);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int64_t tile_idx = blockIdx.x;
+  const uint8_t* qtile = p.q + tile_idx * (int64_t)p.n_features * kStagedTile;
+  const int warp_id = __shfl_sync(0xffffffffu, tid / 32, 0);
+  if (warp_id == 0) {
+    if (tid == 0) {
+      for (int i = 0; i < n_trees; ++i) {
+        const int t = p.tree_begin + i;
+        const int s = i % p.n_stages;
+        if (i >= p.n_stages) mbar_wait(&empty[s], (uint32_t)(i / p.n_stages - 1) & 1u);
+        unsigned char* dst = stages + (size_t)s * p.stage_bytes;
+        mbar_expect_tx(&full[s], p.table_bytes + (uint32_t)DI * kStagedTile);
+        bulk_g2s_split(dst, p.leaves + ((size_t)t << DI) * CP, p.table_bytes, &full[s]);
+        const uint2* ds = reinterpret_cast<const uint2*>(p.desc) + (size_t)t * DI;
+#pragma unroll
+        for (int d = 0; d < DI; ++d) {
+          const uint2 dd = __ldg(ds + d);
+          const uint32_t off512 = CMP == 7 ? dd.x : (dd.x >> 8);  // f * 512 (sentinel splits: 0)
+          bulk_g2s(dst + p.table_bytes + (size_t)d * kStagedTile, qtile + (size_t)(off512 / 512u) * kStagedTile,
+                   kStagedTile, &full[s]);
+        }
+      }
+    }
+    return;
+  }
+  const int word = tid - 32;  // bucket word of this thread: objects word_object(.., word, k)
+  const int64_t tile_base = tile_idx * kStagedTile;
+  auto obj_of = [&](int k) { return word_object(tile_base, word, k); };
+  double acc[4][C];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[k][c] = (p.first || obj_of(k) >= p.n) ? 0.0 : p.out[obj_of(k) * C + c];
+  const uint32_t stages_s = smem_u32(stages);
+  for (int i = 0; i < n_trees; ++i) {
+    const int t = p.tree_begin + i;
+    const int s = i % p.n_stages;
+    mbar_wait_warp(&full[s], (uint32_t)(i / p.n_stages) & 1u);
+    const uint32_t tab = stages_s + (uint32_t)s * p.stage_bytes;
+    const uint32_t rows = tab + p.table_bytes + 4u * (uint32_t)word;
+    const uint2* ds = reinterpret_cast<const uint2*>(p.desc) + (size_t)t * DI;
+    uint32_t lo = 0, hi = 0;
+#pragma unroll
+    for (int d = 0; d < DI; ++d) {
+      const uint2 dd = __ldg(ds + d);  // warp-uniform: one broadcast
+      const uint32_t w = lds_u32(rows + (uint32_t)d * kStagedTile);
+      uint32_t b7;
+      if constexpr (CMP == 7) {
+        b7 = w + dd.y;
+      } else {
+        b7 = maj3((w & 0x7f7f7f7fu) + (__byte_perm(dd.x, 0u, 0x0000u) & 0x7f7f7f7fu), w, dd.y);
+      }
+      if (d < 8) lo |= (b7 >> (7 - d)) & (0x01010101u << d);
+      else hi |= (b7 >> (15 - d)) & (0x01010101u << (d - 8));
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t idx = ((lo >> (8 * k)) & 0xffu) | (DI > 8 ? ((hi >> (8 * k)) & 0xffu) << 8 : 0u);
+      const uint32_t rec = tab + idx * (uint32_t)(CP * 4);
+      float v[CP];
+#pragma unroll
+      for (int r = 0; r < kRows; ++r) {
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(v[4 * r]), "=f"(v[4 * r + 1]), "=f"(v[4 * r + 2]), "=f"(v[4 * r + 3])
+                     : "r"(rec + 16u * r));
+      }
+#pragma unroll
+      for (int c = 0; c < C; ++c) acc[k][c] += (double)v[c];
+    }
+    mbar_arrive(&empty[s]);
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (obj_of(k) >= p.n) continue;
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+      p.out[obj_of(k) * C + c] = p.last ? __dadd_rn(__dmul_rn(acc[k][c], p.scale), p.bias) : acc[k][c];
+  }
+}
+
 }  // namespace obt

@@ -242,27 +242,32 @@ def test_descriptor_sources_and_multi_launch_fold(monkeypatch, source, strategy)
     assert np.array_equal(idx, oracle.leaf_indices(fm, oracle.quantize(fm, x))[1290:1400])
 
 
-@pytest.mark.parametrize("kernel", ["slice", "k4"])
-@pytest.mark.parametrize("D,C,F,B", [(10, 10, 40, 254), (6, 3, 17, 64), (8, 16, 9, 128), (3, 2, 5, 7), (12, 7, 13, 30)])
+@pytest.mark.parametrize("kernel", ["staged", "k4", "slice"])
+@pytest.mark.parametrize("D,C,F,B", [(10, 10, 40, 254), (6, 3, 17, 64), (8, 16, 9, 128), (3, 2, 5, 7), (12, 7, 13, 30),
+                                     (10, 9, 33, 100), (4, 5, 8, 200)])
 def test_multi_output_bit_exact(monkeypatch, kernel, D, C, F, B):
-    """Multi-output (config 5 shape family): K4 (default) and K4s (sliced records,
+    """Multi-output (config 5 shape family): K5 (staged tables, default where it applies:
+    fp32 records, C <= 10, depth <= 10), K4 (OBT_MULTI_STAGED=0) and K4s (sliced records,
     OBT_MULTI_SLICE=1) against the oracle restatement, both layouts, with the binary64
-    leaf tables too (OBT_LEAF_STORAGE=64)."""
+    leaf tables too (OBT_LEAF_STORAGE=64, which K5 leaves to K4)."""
     from paper_2211_00391_b200 import multiclass
 
     monkeypatch.setenv("OBT_MULTI_SLICE", "1" if kernel == "slice" else "0")
+    monkeypatch.setenv("OBT_MULTI_STAGED", "1" if kernel == "staged" else "0")
 
     spec = synthetic.WorkloadSpec("m", 1, F, B, 57, D, 0.01, n_outputs=C, cfg=5)
     arrays = synthetic.model_arrays(spec, seed=D * 100 + C, affine=True)
     model = multiclass.from_arrays(arrays)
     x = _features(obt.ObliviousModel(tuple(obt.FloatFeatureBorders(f, b) for f, b in enumerate(arrays["borders"])),
-                                      (), 1.0, 0.0), 1031, seed=D + C)
+                                      (), 1.0, 0.0), 4097, seed=D + C)
     fm = oracle.FlatModel(np.stack(arrays["borders"]), np.full(F, B, np.int32), np.full(57, D, np.int32),
                           arrays["split_feature"], arrays["split_ordinal"], arrays["leaves"], model.scale, model.bias)
     want = oracle.evaluate_scalar(fm, x)
     ev = multiclass.MultiOutputEvaluator(model)
     got = ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
-    assert got.shape == (1031, C)
+    assert got.shape == (4097, C)
+    if kernel == "staged" and C <= 10 and D <= 10:
+        assert ev.apply_kernel() == "staged"
     assert np.array_equal(got, want)
     dev = ev.predict_device(torch.from_numpy(np.ascontiguousarray(x.T)).cuda(), obt.Layout.FEATURE_MAJOR).cpu().numpy()
     assert np.array_equal(dev, want)
