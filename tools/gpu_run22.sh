@@ -1,0 +1,9 @@
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu22.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_gpu22.log; grep -E "^E |FAILED" gpurun_out/pytest_gpu22.log | head
+run() { # name config env...
+  name=$1; c=$2; shift 2
+  env "$@" timeout 900 python bench.py --config $c --steps 100 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/b22_$name.json 2>gpurun_out/b22_$name.err
+  python -c "import json;d=json.load(open('gpurun_out/b22_$name.json'));print('$name', round(d['ms_per_step'],4), d['kernels']['apply_ms'])" 2>&1 | tail -1
+}
+run c2 2 X=1
+run c3 3 X=1
+run c2b 2 X=1
