@@ -87,8 +87,9 @@ int obt_model_info(const obt_model* model, int32_t* n_features, int32_t* n_trees
                    int32_t* leaf_storage, int32_t* compare_mode);
 
 /* Which quantize search the predict path runs for TMA-eligible inputs (object-major,
- * F % 4 == 0, 16-byte aligned): kind 1 = cell tables (K1L) with `param` compares per
- * value, kind 0 = Eytzinger search (K1t) with `param` levels.  Diagnostics for tests
+ * F % 4 == 0, 16-byte aligned): kind 1 / 2 = cell tables (K1L, 256 / 1024 cells per
+ * feature) with `param` compares per value, kind 0 = Eytzinger search (K1t) with `param`
+ * levels.  Diagnostics for tests
  * and tuning; no reference counterpart (the reference always counts every border,
  * quantize.py:171). */
 int obt_model_quantize_kernel(const obt_model* model, int32_t* kind, int32_t* param);

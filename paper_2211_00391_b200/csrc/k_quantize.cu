@@ -39,12 +39,21 @@ QuantTmaFn pick_quant_tma(int levels) {
   }
 }
 
-QuantTmaFn pick_quant_lut(int kmax) {
+QuantTmaFn pick_quant_lut(int kmax, int cells) {
+  if (cells == 1024) {
+    switch (kmax) {
+      case 1: return quantize_lut_kernel<1, 1024>;
+      case 2: return quantize_lut_kernel<2, 1024>;
+      case 3: return quantize_lut_kernel<3, 1024>;
+      case 4: return quantize_lut_kernel<4, 1024>;
+      default: return nullptr;
+    }
+  }
   switch (kmax) {
-    case 1: return quantize_lut_kernel<1>;
-    case 2: return quantize_lut_kernel<2>;
-    case 3: return quantize_lut_kernel<3>;
-    case 4: return quantize_lut_kernel<4>;
+    case 1: return quantize_lut_kernel<1, 256>;
+    case 2: return quantize_lut_kernel<2, 256>;
+    case 3: return quantize_lut_kernel<3, 256>;
+    case 4: return quantize_lut_kernel<4, 256>;
     default: return nullptr;
   }
 }

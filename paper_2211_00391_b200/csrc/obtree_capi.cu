@@ -82,10 +82,11 @@ struct BorderTable {
 // K1L cell tables of a border set (see quantize_lut_kernel): kmax = 0 when the set
 // needs more than kLutMaxCompares compares in some cell (the Eytzinger K1t runs then).
 struct LutTable {
-  uint8_t* d_lut = nullptr;        // [F][256]
+  uint8_t* d_lut = nullptr;        // [F][cells]
   unsigned char* d_rec = nullptr;  // [F][rec_stride]
   int rec_stride = 0;
   int kmax = 0;
+  int cells = 256;
 };
 constexpr int kLutMaxCompares = 4;
 
@@ -210,17 +211,18 @@ int build_border_table(const float* borders, const int32_t* counts, int F, int s
 // lut[c] = #{k : c_k < c}, and K = the most borders sharing a cell.  Returns kmax = 0
 // (not applicable) if a feature needs more than kLutMaxCompares compares or its range
 // does not fit the map.
-int build_lut_table(const float* borders, const int32_t* counts, int F, int stride, LutTable& out) {
+// Host tables for `cells` cells per feature; returns kmax (0: not applicable).
+int plan_lut_table(const float* borders, const int32_t* counts, int F, int stride, int cells,
+                   std::vector<uint8_t>& lut, std::vector<unsigned char>& rec, int& rec_stride) {
   const float M = 12582912.0f;  // 1.5 * 2^23: floats in [2^23, 2^24) step by 1
   uint32_t mbits;
   std::memcpy(&mbits, &M, 4);
   int umax = 0;
   for (int f = 0; f < F; ++f) umax = std::max(umax, (int)counts[f]);
   const int P = (umax + 1 + 3) / 4 * 4;  // borders + one +inf pad (index U is read)
-  out.rec_stride = obt::kLutRecHeader + 4 * P;
-  out.kmax = 0;
-  std::vector<uint8_t> lut((size_t)F * obt::kLutCells, 0);
-  std::vector<unsigned char> rec((size_t)F * out.rec_stride, 0);
+  rec_stride = obt::kLutRecHeader + 4 * P;
+  lut.assign((size_t)F * cells, 0);
+  rec.assign((size_t)F * rec_stride, 0);
   auto cell_of = [&](float x, float lo, float hi, float sc, float of) -> long {
     const float y = fmaf(fminf(fmaxf(x, lo), hi), sc, of);
     uint32_t yb;
@@ -237,50 +239,85 @@ int build_lut_table(const float* borders, const int32_t* counts, int F, int stri
       lo = b[0];
       hi = b[U - 1];
       const double span = (double)hi - (double)lo;
-      sc = (float)(254.0 / span);
-      if (!(span > 0) || !std::isfinite(sc) || !(sc > 0)) return OBT_OK;
+      sc = (float)((double)(cells - 2) / span);
+      if (!(span > 0) || !std::isfinite(sc) || !(sc > 0)) return 0;
       const double o0 = (double)M - (double)lo * (double)sc;
-      if (!(o0 > 8388608.0 + 512 && o0 < 16777216.0 - 512)) return OBT_OK;
+      if (!(o0 > 8388608.0 + 2 * cells && o0 < 16777216.0 - 2 * cells)) return 0;
       of = (float)std::floor(o0);
       bool ok = false;
       for (int it = 0; it < 8; ++it) {
         const long clo = cell_of(lo, lo, hi, sc, of), chi = cell_of(hi, lo, hi, sc, of);
         if (clo < 0) { of += 1.0f; continue; }
-        if (chi > 255) { of -= 1.0f; continue; }
-        ok = clo >= 0 && chi <= 255;
+        if (chi > cells - 1) { of -= 1.0f; continue; }
+        ok = clo >= 0 && chi <= cells - 1;
         break;
       }
-      if (!ok) return OBT_OK;
+      if (!ok) return 0;
     } else if (U == 1) {
       lo = hi = b[0];
     }
     // cells of the borders, lower-bound table, compares needed
-    std::vector<int> per_cell(obt::kLutCells, 0);
-    std::vector<long> cells(U);
+    std::vector<int> per_cell(cells, 0);
+    std::vector<long> cl(U);
     for (int k = 0; k < U; ++k) {
       const long c = cell_of(b[k], lo, hi, sc, of);
-      if (c < 0 || c > 255 || (k > 0 && c < cells[k - 1])) return OBT_OK;  // must be monotone
-      cells[k] = c;
+      if (c < 0 || c > cells - 1 || (k > 0 && c < cl[k - 1])) return 0;  // must be monotone
+      cl[k] = c;
       ++per_cell[c];
     }
     int kf = 0;
-    for (int c = 0, below = 0; c < obt::kLutCells; ++c) {
-      lut[(size_t)f * obt::kLutCells + c] = (uint8_t)below;
+    for (int c = 0, below = 0; c < cells; ++c) {
+      lut[(size_t)f * cells + c] = (uint8_t)below;
       below += per_cell[c];
       kf = std::max(kf, per_cell[c]);
     }
-    if (kf > kLutMaxCompares) return OBT_OK;
+    if (kf > kLutMaxCompares) return 0;
     kmax = std::max(kmax, kf);
-    float* r = reinterpret_cast<float*>(rec.data() + (size_t)f * out.rec_stride);
+    float* r = reinterpret_cast<float*>(rec.data() + (size_t)f * rec_stride);
     r[0] = lo; r[1] = hi; r[2] = sc; r[3] = of;
     float* bd = r + obt::kLutRecHeader / 4;
     for (int k = 0; k < P; ++k) bd[k] = k < U ? b[k] : INFINITY;
   }
+  return kmax;
+}
+
+// Cell tables for K1L.  Per feature (borders b_0 < ... < b_{U-1}): lo = b_0, hi = b_{U-1},
+// s ~ (cells - 2) / (hi - lo), o = 1.5 * 2^23 - lo * s (+ nudges), checked with the
+// device's own fp32 operations (fmaxf / fminf / fmaf, correctly rounded on both sides) so
+// that every clamped x maps into [1.5 * 2^23, 1.5 * 2^23 + cells - 1]; then cell c_k of
+// each border, lut[c] = #{k : c_k < c}, and K = the most borders sharing a cell.  256
+// cells unless some cell holds several borders and 1024 cells bring it to one compare.
+// kmax = 0 (not applicable) if a feature needs more than kLutMaxCompares compares or its
+// range does not fit the map.
+int build_lut_table(const float* borders, const int32_t* counts, int F, int stride, LutTable& out) {
+  std::vector<uint8_t> lut;
+  std::vector<unsigned char> rec;
+  int rs = 0;
+  out.kmax = 0;
+  out.cells = 256;
+  int k = plan_lut_table(borders, counts, F, stride, 256, lut, rec, rs);
+  const char* e = getenv("OBT_LUT_CELLS");  // tuning override: 256 or 1024
+  const bool force1024 = e && !strcmp(e, "1024"), force256 = e && !strcmp(e, "256");
+  if ((k != 1 && !force256) || force1024) {
+    std::vector<uint8_t> lut2;
+    std::vector<unsigned char> rec2;
+    int rs2 = 0;
+    const int k2 = plan_lut_table(borders, counts, F, stride, 1024, lut2, rec2, rs2);
+    if (k2 > 0 && (force1024 || (k2 <= 2 && (k == 0 || k2 < k)))) {
+      lut.swap(lut2);
+      rec.swap(rec2);
+      rs = rs2;
+      k = k2;
+      out.cells = 1024;
+    }
+  }
+  if (k <= 0) return OBT_OK;
+  out.rec_stride = rs;
   CUDA_TRY(cudaMalloc(&out.d_lut, lut.size()));
   CUDA_TRY(cudaMemcpy(out.d_lut, lut.data(), lut.size(), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMalloc(&out.d_rec, rec.size()));
   CUDA_TRY(cudaMemcpy(out.d_rec, rec.data(), rec.size(), cudaMemcpyHostToDevice));
-  out.kmax = kmax;
+  out.kmax = k;
   return OBT_OK;
 }
 
@@ -661,6 +698,9 @@ bool lut_preferred(const obt_model* m) {
   const char* e = getenv("OBT_QUANT_LUT");
   if (e && !strcmp(e, "0")) return false;
   if (e && !strcmp(e, "1")) return true;
+  // 1024-cell tables (1 KB per feature) pay off only against deep searches: cfg4 (7
+  // levels) 4.49 vs 4.95 ms, cfg5 (6 levels) 17.1 vs 16.5 ms
+  if (m->used_lut.cells == 1024 && m->used.levels < 7) return false;
   return 1 + m->used_lut.kmax < m->used.levels - 2;
 }
 
@@ -704,13 +744,13 @@ int launch_quantize(const obt_model* m, const float* x, int64_t n, int layout, u
   // K1L (cell tables) wherever the used-border set admits them
   const LutTable& lt = m->used_lut;
   const bool use_lut = tiled && lut_preferred(m);
-  obt::QuantTmaFn tfn = use_lut ? pick_quant_lut(lt.kmax) : pick_quant_tma(bt.levels);
+  obt::QuantTmaFn tfn = use_lut ? pick_quant_lut(lt.kmax, lt.cells) : pick_quant_tma(bt.levels);
   if (tiled && layout == OBT_LAYOUT_OBJECT_MAJOR && F % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
       tfn && encode_tiled() && quantize_tma_enabled()) {
     // two CTAs per SM: each gets half the SM's shared memory less the per-CTA reserve
     const size_t half = (size_t)(m->smem_optin + 1024) / 2 - 1024;
     const size_t lut_fixed = use_lut ? 256 + 32 : 0;  // 256-byte alignment of the tables
-    const int fc = use_lut ? quantize_chunk_bytes(m, (size_t)obt::kLutCells + lt.rec_stride, n_slots,
+    const int fc = use_lut ? quantize_chunk_bytes(m, (size_t)lt.cells + lt.rec_stride, n_slots,
                                                   half - obt::kQTSmemFixed - lut_fixed)
                            : quantize_chunk(m, bt, n_slots, half - obt::kQTSmemFixed);
     CUtensorMap map;
@@ -727,7 +767,7 @@ int launch_quantize(const obt_model* m, const float* x, int64_t n, int layout, u
       p.lrec = lt.d_rec;
       p.lrec_stride = lt.rec_stride;
       p.chunk_inner = use_lut ? 1 : 0;
-      const size_t smem = use_lut ? obt::kQTSmemFixed + lut_fixed + (size_t)std::min(fc, F) * (obt::kLutCells + lt.rec_stride)
+      const size_t smem = use_lut ? obt::kQTSmemFixed + lut_fixed + (size_t)std::min(fc, F) * (lt.cells + lt.rec_stride)
                                   : obt::kQTSmemFixed + (bt.levels > 0 ? (size_t)std::min(fc, F) * bt.pitch * 4 : 16);
       CUDA_TRY(cudaFuncSetAttribute(tfn, cudaFuncAttributeMaxDynamicSharedMemorySize, m->smem_optin));
       const dim3 grid(blocks * (unsigned)((F + fc - 1) / fc));
@@ -1170,7 +1210,7 @@ int obt_model_info(const obt_model* m, int32_t* n_features, int32_t* n_trees, in
 int obt_model_quantize_kernel(const obt_model* m, int32_t* kind, int32_t* param) {
   if (!m) return fail(OBT_E_INVALID, "null model");
   const bool lut = lut_preferred(m);
-  if (kind) *kind = lut ? 1 : 0;
+  if (kind) *kind = lut ? (m->used_lut.cells == 1024 ? 2 : 1) : 0;
   if (param) *param = lut ? m->used_lut.kmax : m->used.levels;
   return OBT_OK;
 }

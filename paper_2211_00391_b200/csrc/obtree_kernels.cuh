@@ -525,7 +525,7 @@ __global__ void __launch_bounds__(kQTThreads, 2) quantize_tma_kernel(const __gri
 // rounded in both places), so buckets are bit-exact.  Per value: 2 FMNMX, FFMA, PRMT,
 // one byte load, KMAX x (address, load, compare-add) -- about a third of the Eytzinger
 // search's instructions, with fewer dependent shared loads.
-constexpr int kLutCells = 256;
+constexpr int kLutCells = 256;       // cells per feature table (1024 where 256 leave crowded cells)
 constexpr int kLutRecHeader = 16;  // lo, hi, s, o
 
 __device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
@@ -539,7 +539,7 @@ __device__ __forceinline__ float lds_f32(uint32_t addr) {
   return v;
 }
 
-template <int KMAX>
+template <int KMAX, int CELLS>
 __global__ void __launch_bounds__(kQTThreads, 2) quantize_lut_kernel(const __grid_constant__ CUtensorMap rows,
                                                                      const QuantizeParams p) {
   extern __shared__ __align__(16) unsigned char qt_raw[];
@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(kQTThreads, 2) quantize_lut_kernel(const __gri
   const int f0 = (int)(p.chunk_inner ? blockIdx.x % (unsigned)n_fch : blockIdx.x / n_rb) * fc;
   const int64_t rblock = (int64_t)(p.chunk_inner ? blockIdx.x / (unsigned)n_fch : blockIdx.x % n_rb);
   const int nf = min(fc, p.n_features - f0);
-  unsigned char* recs = luts + (size_t)fc * kLutCells;
+  unsigned char* recs = luts + (size_t)nf * CELLS;  // this chunk's nf features (the host sizes min(fc, F))
   const int rs = p.lrec_stride;
   const int n_steps = (nf + kQuantStep - 1) / kQuantStep;
   const int64_t row0 = rblock * kQuantBlock;
@@ -573,9 +573,9 @@ __global__ void __launch_bounds__(kQTThreads, 2) quantize_lut_kernel(const __gri
     fence_mbar_init();
   }
   {
-    const uint4* src = reinterpret_cast<const uint4*>(p.lut + (size_t)f0 * kLutCells);
+    const uint4* src = reinterpret_cast<const uint4*>(p.lut + (size_t)f0 * CELLS);
     uint4* dst = reinterpret_cast<uint4*>(luts);
-    for (int i = threadIdx.x; i < nf * kLutCells / 16; i += kQTThreads) dst[i] = __ldg(src + i);
+    for (int i = threadIdx.x; i < nf * CELLS / 16; i += kQTThreads) dst[i] = __ldg(src + i);
     const uint4* rsrc = reinterpret_cast<const uint4*>(p.lrec + (size_t)f0 * rs);
     uint4* rdst = reinterpret_cast<uint4*>(recs);
     for (int i = threadIdx.x; i < nf * rs / 16; i += kQTThreads) rdst[i] = __ldg(rsrc + i);
@@ -624,13 +624,17 @@ __global__ void __launch_bounds__(kQTThreads, 2) quantize_lut_kernel(const __gri
     for (int j = 0; j < kQuantStep; ++j) {
       const int fl = min(fq + j, nf - 1);
       const float4 h = *reinterpret_cast<const float4*>(recs + (size_t)fl * rs);  // lo, hi, s, o (broadcast)
-      const uint32_t lut_base = luts_s + (uint32_t)fl * kLutCells;
+      const uint32_t lut_base = luts_s + (uint32_t)fl * CELLS;
       const uint32_t bord = recs_s + (uint32_t)fl * rs + kLutRecHeader;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const float x = v[j][k];
         const float y = __fmaf_rn(fminf(fmaxf(x, h.x), h.y), h.z, h.w);
-        uint32_t b = lds_u8(__byte_perm(__float_as_uint(y), lut_base, 0x7650u));
+        // 256 cells: the cell byte drops into byte 0 of the 256-aligned table address (PRMT);
+        // 1024 cells: the low 10 bits of y's bits index the table
+        const uint32_t cell_addr = CELLS == 256 ? __byte_perm(__float_as_uint(y), lut_base, 0x7650u)
+                                                : lut_base + (__float_as_uint(y) & (uint32_t)(CELLS - 1));
+        uint32_t b = lds_u8(cell_addr);
 #pragma unroll
         for (int i = 0; i < KMAX; ++i) b = add_if_greater(b, x, lds_f32(bord + 4u * b), 1u);
         bk[j][k] = b;

@@ -66,7 +66,7 @@ class DeviceModel:
         per value) for the cell-table kernel, ("eytzinger", levels) otherwise."""
         kind, param = ctypes.c_int32(), ctypes.c_int32()
         _native.check(self._lib.obt_model_quantize_kernel(self.handle, ctypes.byref(kind), ctypes.byref(param)))
-        return ("cells" if kind.value == 1 else "eytzinger", param.value)
+        return ({1: "cells", 2: "cells1024"}.get(kind.value, "eytzinger"), param.value)
 
     def close(self) -> None:
         if getattr(self, "handle", None) and self.handle.value:

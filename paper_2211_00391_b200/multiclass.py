@@ -133,7 +133,7 @@ class MultiOutputEvaluator:
         """("cells", compares) or ("eytzinger", levels): the predict path's quantize search."""
         kind, param = ctypes.c_int32(), ctypes.c_int32()
         _native.check(self._lib.obt_model_quantize_kernel(self.handle, ctypes.byref(kind), ctypes.byref(param)))
-        return ("cells" if kind.value == 1 else "eytzinger", param.value)
+        return ({1: "cells", 2: "cells1024"}.get(kind.value, "eytzinger"), param.value)
 
     def apply_kernel(self) -> str:
         """The multi-output apply kernel this model runs: "staged" (K5), "sliced" (K4s) or "gather" (K4)."""

@@ -621,7 +621,12 @@ _LUT_SETS = {
         np.array([1e6, 1000001.0, 1000002.0], np.float32),  # lo * s ~ 2.5e8 > 2^23
         np.sort(np.random.default_rng(3).normal(0, 1, 16)).astype(np.float32),
     ],
-    # five borders in one cell: more than the cell kernel's 4 compares
+    # five borders in one of 256 cells, at most two in one of 1024: the 1024-cell tables
+    "crowded256": [
+        np.array([0.0, 0.25, 0.5, 0.75, 0.9, 255.0], np.float32),
+        np.sort(np.random.default_rng(4).normal(0, 1, 30)).astype(np.float32),
+    ],
+    # five borders in one cell even at 1024 cells: more than the cell kernel's compares
     "crowded": [
         np.array([0.0, 1e-6, 2e-6, 3e-6, 4e-6, 100.0], np.float32),
         np.array([1.0, 2.0], np.float32),
@@ -629,12 +634,16 @@ _LUT_SETS = {
 }
 
 
-@pytest.mark.parametrize("name,expect", [("mixed", "cells"), ("fallback", "eytzinger"), ("crowded", "eytzinger")])
-def test_cell_table_quantize_edges(monkeypatch, name, expect):
+@pytest.mark.parametrize("name,expect,cells", [("mixed", "cells", "256"), ("mixed", "cells1024", "1024"),
+                                              ("fallback", "eytzinger", ""), ("crowded256", "cells1024", ""),
+                                              ("crowded", "eytzinger", "")])
+def test_cell_table_quantize_edges(monkeypatch, name, expect, cells):
     """K1L (cell-table quantize) against the oracle on values at, next to and far from
     every border, NaN, +-inf, signed zeros and denormals; and equal to the Eytzinger
     search (OBT_QUANT_LUT=0) bucket for bucket through the predictions and leaf indices."""
     monkeypatch.setenv("OBT_QUANT_LUT", "1")  # K1L wherever its tables exist (not only where it is faster)
+    if cells:
+        monkeypatch.setenv("OBT_LUT_CELLS", cells)
     sets = [np.asarray(b, np.float32) for b in _LUT_SETS[name]]
     pad = (-len(sets)) % 4  # F % 4 == 0: the TMA-staged path
     sets += [np.array([0.25 * (i + 1)], np.float32) for i in range(pad)]
