@@ -1509,6 +1509,9 @@ __global__ void __launch_bounds__(128) apply_multi_slice_kernel(const __grid_con
 // shared memory only: one table load serves 2048 objects (24 B of L2 traffic per
 // object-tree instead of a 48-byte record fetch), and every load the fold waits on is a
 // shared-memory load.  Descriptors come from the K4 array ({f * 512, k} / {(f*512) << 8 | k, s}).
+#ifndef OBT_STAGED_V2
+#define OBT_STAGED_V2 0  // K5 record reads as 8-byte loads (C values) instead of 16-byte rows
+#endif
 constexpr int kStagedThreadsConsumers = 512;
 constexpr int kStagedTile = 4 * kStagedThreadsConsumers;  // 2048 objects
 constexpr int kStagedThreads = kStagedThreadsConsumers + 32;
@@ -1606,11 +1609,18 @@ __global__ void __launch_bounds__(kStagedThreads, 1) apply_multi_staged_kernel(c
       const uint32_t idx = ((lo >> (8 * k)) & 0xffu) | (DI > 8 ? ((hi >> (8 * k)) & 0xffu) << 8 : 0u);
       const uint32_t rec = tab + idx * (uint32_t)(CP * 4);
       float v[CP];
+      if constexpr (OBT_STAGED_V2) {
+        // 8-byte loads of the C values only (no padding read): half-warp phases
 #pragma unroll
-      for (int r = 0; r < kRows; ++r) {
-        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                     : "=f"(v[4 * r]), "=f"(v[4 * r + 1]), "=f"(v[4 * r + 2]), "=f"(v[4 * r + 3])
-                     : "r"(rec + 16u * r));
+        for (int r = 0; r < (C + 1) / 2; ++r)
+          asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v[2 * r]), "=f"(v[2 * r + 1]) : "r"(rec + 8u * r));
+      } else {
+#pragma unroll
+        for (int r = 0; r < kRows; ++r) {
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(v[4 * r]), "=f"(v[4 * r + 1]), "=f"(v[4 * r + 2]), "=f"(v[4 * r + 3])
+                       : "r"(rec + 16u * r));
+        }
       }
 #pragma unroll
       for (int c = 0; c < C; ++c) acc[k][c] += (double)v[c];
