@@ -799,7 +799,7 @@ int launch_quantize(const obt_model* m, const float* x, int64_t n, int layout, u
 // `tpw` (lanes per bucket word, from apply_lanes) must match the layout the quantize
 // launch wrote: tpw > 1 reads the swizzled K2s layout.
 int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, int tpw, double* out, uint16_t* idx_out,
-                 int tree_begin, int tree_end, cudaStream_t stream) {
+                 int tree_begin, int tree_end, cudaStream_t stream, uint32_t* flags = nullptr) {
   const bool write_idx = idx_out != nullptr;
   const int dsrc = use_param_descriptors(m, tpw);
   const TilePlan* tp = nullptr;
@@ -839,8 +839,19 @@ int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, int tpw, d
   // so each launch's first wave finds the previous pass's last tiles still in L2
   // (OBT_TILE_ORDER=fwd disables it; cfg2 apply 1.035 -> 1.024 ms).  OBT_L2_NEXT=1 also
   // has every CTA prefetch the next wave's tile into L2 (measured 1.029 ms: no gain).
+  // Launch chaining (parameter-bank folds of several launches): launch k > 0 goes out
+  // as a programmatic dependent launch, so its CTAs start on the SMs launch k - 1's
+  // partial last wave leaves idle; a CTA waits only for its own tile's carry (per-tile
+  // flags).  Not under stream capture.  OBT_PDL=0 disables it.
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  CUDA_TRY(cudaStreamIsCapturing(stream, &cap));
+  const char* pe = getenv("OBT_PDL");
+  const bool chain = flags && dsrc && !write_idx && n_launch > 1 && k.words == 1 && cap == cudaStreamCaptureStatusNone &&
+                     !(pe && !strcmp(pe, "0"));
+  if (chain) CUDA_TRY(cudaMemsetAsync(flags, 0, (size_t)n_tiles * 4, stream));
+  p.tile_flags = flags;
   const char* to = getenv("OBT_TILE_ORDER");
-  const bool alternate = !(to && !strcmp(to, "fwd"));
+  const bool alternate = !chain && !(to && !strcmp(to, "fwd"));  // chained launches keep one order
   const char* ln = getenv("OBT_L2_NEXT");
   p.l2_wave = 0;
   if (ln && !strcmp(ln, "1")) {
@@ -854,6 +865,8 @@ int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, int tpw, d
     p.first = l == 0;
     p.last = l == n_launch - 1;
     p.reverse = alternate && (l % 2 == 0) ? 1 : 0;
+    p.flag_wait = chain ? l : 0;
+    p.flag_set = chain && l < n_launch - 1 ? l + 1 : 0;
     if (dsrc) {
       auto* args = &m->param_args;  // scratch; the driver copies parameters at launch
       std::lock_guard<std::mutex> lock(m->mu);
@@ -862,7 +875,21 @@ int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, int tpw, d
       const size_t words = (size_t)(p.chunk_end - p.chunk_begin) * m->chunk_trees * per_tree;
       std::memcpy(args->desc, tp->param_desc.data() + (size_t)p.chunk_begin * m->chunk_trees * per_tree, words * 4);
       void* kargs[] = {args};
-      CUDA_TRY(cudaLaunchKernel(k.fn, grid, block, kargs, smem, stream));
+      if (chain && l > 0) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = grid;
+        cfg.blockDim = block;
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CUDA_TRY(cudaLaunchKernelExC(&cfg, k.fn, kargs));
+      } else {
+        CUDA_TRY(cudaLaunchKernel(k.fn, grid, block, kargs, smem, stream));
+      }
     } else {
       obt::ApplyArgs<0> small{p};
       void* kargs[] = {&small};
@@ -1003,10 +1030,16 @@ Regions plan_regions(const obt_model* m, int64_t n, bool split_ok) {
   return r;
 }
 
-size_t regions_workspace(const obt_model* m, const Regions& r) {
+size_t regions_bucket_bytes(const obt_model* m, const Regions& r) {
   size_t b = 0;
   for (int i = 0; i < r.n_reg; ++i) b += workspace_bytes(m, r.count[i], r.tile[i]);
   return b;
+}
+
+// Bucket tiles of every region, then one 32-bit launch-chaining flag per tile of region 0.
+size_t regions_workspace(const obt_model* m, const Regions& r) {
+  const int64_t tiles0 = r.tile[0] > 0 ? (r.count[0] + r.tile[0] - 1) / r.tile[0] : 0;
+  return regions_bucket_bytes(m, r) + (size_t)((tiles0 * 4 + 255) / 256 * 256);
 }
 
 int check_layout(int layout) {
@@ -1283,6 +1316,7 @@ static int predict_impl(obt_model* m, const float* x, int64_t n, int32_t layout,
   // one quantize launch writes both regions' bucket tiles (each laid out for its tile
   // size and lanes per word), then one apply launch per region
   uint8_t* qr[2] = {q, q + workspace_bytes(m, reg.count[0], reg.tile[0])};
+  uint32_t* flags = reinterpret_cast<uint32_t*>(q + regions_bucket_bytes(m, reg));
   int tpw[2] = {1, 1};
   for (int i = 0; i < reg.n_reg; ++i) tpw[i] = apply_lanes(m, reg.tile[i], idx_out != nullptr);
   if (ev_begin) CUDA_TRY(cudaEventRecord(ev_begin, stream));
@@ -1303,7 +1337,8 @@ static int predict_impl(obt_model* m, const float* x, int64_t n, int32_t layout,
       rc = idx_out ? fail(OBT_E_UNSUPPORTED, "leaf-index dumps are implemented for single-output models")
                    : launch_multi(m, qr[i], c, out + b * m->n_outputs, stream);
     } else {
-      rc = launch_apply(m, qr[i], c, reg.tile[i], tpw[i], out ? out + b : nullptr, idx_out, tree_begin, tree_end, stream);
+      rc = launch_apply(m, qr[i], c, reg.tile[i], tpw[i], out ? out + b : nullptr, idx_out, tree_begin, tree_end, stream,
+                        i == 0 && reg.n_reg == 1 ? flags : nullptr);
     }
   }
   if (rc == OBT_OK && ev_end) CUDA_TRY(cudaEventRecord(ev_end, stream));

@@ -119,6 +119,32 @@ __device__ __forceinline__ void bulk_g2s_split(void* dst, const void* src, uint3
   }
 }
 
+// Launch chaining: let the dependent launch start (its CTAs take SMs as ours finish).
+__device__ __forceinline__ void launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* a) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(uint32_t* a, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+
+// Spin until *a >= want (bounded: a lost dependency traps instead of hanging the GPU).
+__device__ __forceinline__ void wait_flag(const uint32_t* a, uint32_t want) {
+  uint32_t spins = 0;
+  while (ld_acquire_gpu(a) < want) {
+    __nanosleep(256);
+    if (++spins > (1u << 26)) asm volatile("trap;");
+  }
+}
+
+// Named barrier among the CTA's consumer warps (id 1; the producer warp has left).
+__device__ __forceinline__ void consumer_sync(int n_threads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(n_threads) : "memory");
+}
+
 // L2 prefetch of a global range by the TMA engine (no shared-memory destination), in
 // pieces of at most 64 KiB.
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
@@ -718,10 +744,16 @@ struct ApplyParams {
   // and, when l2_wave > 0, prefetches into L2 the bucket tile of CTA b + l2_wave (the
   // next wave's), so that wave's tile loads hit L2 instead of waiting on HBM
   int32_t reverse, l2_wave;
+  // launch chaining (programmatic dependent launch): a CTA waits until tile_flags[tile]
+  // >= flag_wait before reading the fold carry, and after its outputs stores flag_set
+  // (0: neither); launches chained this way let the next launch fill the SMs the
+  // previous one's partial last wave leaves idle
+  uint32_t* tile_flags;
+  int32_t flag_wait, flag_set;
   double scale, bias;
 };
 
-constexpr int kParamDescWords = 8160;  // 32640 bytes of descriptors + ApplyParams (104) <= 32764
+constexpr int kParamDescWords = 8144;  // 32576 bytes of descriptors + ApplyParams (128) <= 32764
 
 template <int DSRC> struct ApplyArgs;
 template <> struct ApplyArgs<0> { ApplyParams p; };
@@ -843,6 +875,7 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid
   const int n_consumer_warps = (blockDim.x - kApplyProducerThreads) / 32;
   const int64_t tile_idx = p.reverse ? (int64_t)(gridDim.x - 1 - blockIdx.x) : (int64_t)blockIdx.x;
   const int n_chunks = p.chunk_end - p.chunk_begin;
+  if (p.flag_set > 0) launch_dependents();
   if (tid == 0) {
     for (int i = 0; i < p.n_stages; ++i) {
       mbar_init(&full[i], 1);
@@ -884,6 +917,12 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid
   // accumulator 4x + k: byte k of this thread's word x
   auto obj_of = [&](int x, int k) { return word_object(tile_base, W * ctid + x, k); };
   acc_t acc[kObj];
+  if (p.flag_wait > 0) {
+    // the previous launch of this fold may still run (chained launch): its CTA for this
+    // tile publishes the carry with a release store
+    if (ctid == 0) wait_flag(p.tile_flags + tile_idx, (uint32_t)p.flag_wait);
+    consumer_sync(n_consumer_warps * 32);
+  }
 #pragma unroll
   for (int k = 0; k < kObj; ++k) {
     // continue the fold of the previous launch (exact: the carry holds acc_t values)
@@ -1052,6 +1091,13 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid
       if (o < p.n) {
         // finalize: f64(acc) * scale + bias, two roundings (evaluate.py:298-299, oracle.py:53-54)
         p.out[o] = p.last ? __dadd_rn(__dmul_rn((double)acc[k], p.scale), p.bias) : (double)acc[k];
+      }
+    }
+    if (p.flag_set > 0) {
+      consumer_sync(n_consumer_warps * 32);
+      if (ctid == 0) {
+        __threadfence();
+        st_release_gpu(p.tile_flags + tile_idx, (uint32_t)p.flag_set);
       }
     }
   }
