@@ -494,9 +494,11 @@ int build_tile_plan(obt_model* m, int tile, int variant, TilePlan& out) {
     tree_descriptors(m, t, tile, words.data());
     if (m->compare_mode == 7) std::memcpy(out.param_desc.data() + (size_t)t * DI * 2, words.data(), (size_t)DI * 8);
     if (variant == 1) {
-      // K2s: 16 bytes per split in paired level order, row offsets +- 64 for odd rows
+      // K2s: 16 bytes per split in paired level order, row offsets +- 64 for odd rows;
+      // half-major: DI entries {off + sw, k} then DI entries {off - sw, k}
       split_level_order(m, t, perm.data(), wild.data());
       uint32_t* dst = reinterpret_cast<uint32_t*>(rec + (size_t)tl * DI * obt::kSplitDescBytes);
+      uint32_t* dst_hi = dst + 2 * DI;
       for (int j = 0; j < DI; ++j) {
         const int d = perm[j];
         const bool sentinel = t >= m->n_trees || m->split_ordinal[(size_t)t * DI + d] == kSentinel;
@@ -506,10 +508,10 @@ int build_tile_plan(obt_model* m, int tile, int variant, TilePlan& out) {
         const uint32_t w1 = sentinel ? 0u : words[2 * d + 1];
         const uint32_t k7 = sentinel ? 0u : kpart;
         if (m->compare_mode == 7) {
-          dst[4 * j + 0] = off + sw; dst[4 * j + 1] = w1; dst[4 * j + 2] = off - sw; dst[4 * j + 3] = w1;
+          dst[2 * j + 0] = off + sw; dst[2 * j + 1] = w1; dst_hi[2 * j + 0] = off - sw; dst_hi[2 * j + 1] = w1;
         } else {
-          dst[4 * j + 0] = ((off + sw) << 8) | k7; dst[4 * j + 1] = w1;
-          dst[4 * j + 2] = ((off - sw) << 8) | k7; dst[4 * j + 3] = w1;
+          dst[2 * j + 0] = ((off + sw) << 8) | k7; dst[2 * j + 1] = w1;
+          dst_hi[2 * j + 0] = ((off - sw) << 8) | k7; dst_hi[2 * j + 1] = w1;
         }
       }
       uint8_t* leaf_dst = rec + desc_bytes + (size_t)tl * stride;

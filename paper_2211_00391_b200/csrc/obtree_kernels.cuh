@@ -1119,10 +1119,10 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid
 // half for even rows and in the other for odd rows, and the host orders each tree's
 // levels so the two lanes of a pair read rows of opposite parity wherever the tree
 // allows (the leaf table is permuted to match; the selected leaf is unchanged).
-// Descriptors come from the shared-memory ring as 16 bytes per split,
-// {off+, k, off-, k} (7-bit) or {(off+ << 8) | k, s, (off- << 8) | k, s} (8-bit):
-// off+- = row offset +- 64 for odd rows, and a lane takes the half that matches bit 6
-// of its own word offset (warp-uniform), so the swizzle costs no instruction.
+// Descriptors come from the shared-memory ring as 16 bytes per split, stored half-major:
+// per tree DI entries {off+, k} then DI entries {off-, k} (7-bit; 8-bit: {(off << 8) | k, s}),
+// off+- = row offset +- 64 for odd rows; a lane takes the half that matches bit 6 of its
+// own word offset (warp-uniform), so the swizzle costs no instruction.
 constexpr int kSplitDescBytes = 16;
 template <int DI, int CMP, int LEAF, int TPW>
 __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_split_kernel(const __grid_constant__ ApplyArgs<0> args) {
@@ -1200,8 +1200,11 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_split_kernel(const 
   for (int k = 0; k < kOPT; ++k) acc[k] = (p.first || obj_of(k) >= p.n) ? (acc_t)0 : (acc_t)p.out[obj_of(k)];
   mbar_wait_warp(tile_bar, 0);
 
-  // this lane's first descriptor in a tree: its part's first split, the half for its bit 6
-  const uint32_t my_desc = (uint32_t)(part * kDPT) * kSplitDescBytes + (((4u * word) >> 6) & 1u) * 8u;
+  // this lane's first descriptor in a tree: records are half-major, 8-byte {off, k}
+  // entries [half][level], so a lane's kDPT levels are contiguous (two per 128-bit load
+  // when kDPT is even: half the descriptor loads, and their wavefronts)
+  const uint32_t my_desc = ((((4u * word) >> 6) & 1u) * (uint32_t)DI + (uint32_t)(part * kDPT)) * 8u;
+  constexpr bool kPairDesc = (kDPT % 2) == 0;
   for (int c = 0; c < n_chunks; ++c) {
     const int s = c % p.n_stages;
     mbar_wait_warp(&full[s], (uint32_t)(c / p.n_stages) & 1u);
@@ -1214,10 +1217,20 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_split_kernel(const 
         const int t = g * kTreeGroup + tt;
         const uint32_t tree_desc = desc_base + (uint32_t)t * (uint32_t)(DI * kSplitDescBytes);
         uint32_t part_a = 0, part_b = 0;
+        uint32_t dsc[kDPT][2];
+#pragma unroll
+        for (int i = 0; i < kDPT; i += (kPairDesc ? 2 : 1)) {
+          if constexpr (kPairDesc) {
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(dsc[i][0]), "=r"(dsc[i][1]), "=r"(dsc[i + 1][0]), "=r"(dsc[i + 1][1])
+                         : "r"(tree_desc + 8u * i));
+          } else {
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(dsc[i][0]), "=r"(dsc[i][1]) : "r"(tree_desc + 8u * i));
+          }
+        }
 #pragma unroll
         for (int i = 0; i < kDPT; ++i) {
-          uint32_t d0, d1;
-          asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(d0), "=r"(d1) : "r"(tree_desc + (uint32_t)kSplitDescBytes * i));
+          const uint32_t d0 = dsc[i][0], d1 = dsc[i][1];
           uint32_t b7;
           if constexpr (CMP == 7) {
             b7 = lds_u32(my_q + d0) + d1;

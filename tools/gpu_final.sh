@@ -15,3 +15,6 @@ SKIP=0 timeout 900 bash tools/prof.sh fs4main 'apply_split' --config 4 > gpurun_
 for r in fa2main fa2last fq2lut fs4main; do python tools/ncu_source_summary.py gpurun_out/$r.ncu-rep > gpurun_out/final/${r}_by_opcode.txt 2>&1; done
 cat gpurun_out/final/prof_*.txt | cut -c1-300
 for f in gpurun_out/final/bench_*.json; do python -c "import json,sys;d=json.loads(open('$f').read().strip().splitlines()[-1]);print('$f', d.get('ms_per_step'), d.get('value'), (d.get('e2e') or {}).get('value'), (d.get('roofline') or {}).get('frac'))"; done
+SKIP=0 timeout 900 bash tools/prof.sh fa5staged 'apply_multi_staged' --config 5 > gpurun_out/final/prof_fa5staged.txt 2>&1; head -c 600 gpurun_out/final/prof_fa5staged.txt
+python tools/ncu_source_summary.py gpurun_out/fa5staged.ncu-rep > gpurun_out/final/fa5staged_by_opcode.txt 2>&1
+SKIP=0 timeout 900 bash tools/prof.sh fq4lut 'quantize_lut' --config 4 > gpurun_out/final/prof_fq4lut.txt 2>&1; head -c 600 gpurun_out/final/prof_fq4lut.txt
