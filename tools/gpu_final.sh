@@ -1,6 +1,7 @@
 # Round measurements: every config's bench line, the reference arm, the cfg2 launch list
 # and ncu captures of the dominant kernels (each after its own plain run exits 0).
 mkdir -p gpurun_out/final
+export NCU_DIR=/tmp/ncu_reps
 timeout 900 python bench.py > gpurun_out/final/bench_cfg2.json 2> gpurun_out/final/bench_cfg2.err; echo "cfg2 rc=$?"
 timeout 600 python bench.py --config 1 > gpurun_out/final/bench_cfg1.json 2> gpurun_out/final/bench_cfg1.err; echo "cfg1 rc=$?"
 timeout 900 python bench.py --config 3 --no-cpu-baseline > gpurun_out/final/bench_cfg3.json 2> gpurun_out/final/bench_cfg3.err; echo "cfg3 rc=$?"
@@ -12,9 +13,9 @@ SKIP=0 timeout 600 bash tools/prof.sh fa2main 'apply_kernel' --config 2 > gpurun
 SKIP=2 timeout 600 bash tools/prof.sh fa2last 'apply_kernel' --config 2 > gpurun_out/final/prof_fa2last.txt 2>&1
 SKIP=1 timeout 600 bash tools/prof.sh fq2lut 'quantize_lut' --config 2 > gpurun_out/final/prof_fq2lut.txt 2>&1
 SKIP=0 timeout 900 bash tools/prof.sh fs4main 'apply_split' --config 4 > gpurun_out/final/prof_fs4main.txt 2>&1
-for r in fa2main fa2last fq2lut fs4main; do python tools/ncu_source_summary.py gpurun_out/$r.ncu-rep > gpurun_out/final/${r}_by_opcode.txt 2>&1; done
+for r in fa2main fa2last fq2lut fs4main; do cp gpurun_out/${r}_by_opcode.txt gpurun_out/final/; done
 cat gpurun_out/final/prof_*.txt | cut -c1-300
 for f in gpurun_out/final/bench_*.json; do python -c "import json,sys;d=json.loads(open('$f').read().strip().splitlines()[-1]);print('$f', d.get('ms_per_step'), d.get('value'), (d.get('e2e') or {}).get('value'), (d.get('roofline') or {}).get('frac'))"; done
 SKIP=0 timeout 900 bash tools/prof.sh fa5staged 'apply_multi_staged' --config 5 > gpurun_out/final/prof_fa5staged.txt 2>&1; head -c 600 gpurun_out/final/prof_fa5staged.txt
-python tools/ncu_source_summary.py gpurun_out/fa5staged.ncu-rep > gpurun_out/final/fa5staged_by_opcode.txt 2>&1
+cp gpurun_out/fa5staged_by_opcode.txt gpurun_out/final/
 SKIP=0 timeout 900 bash tools/prof.sh fq4lut 'quantize_lut' --config 4 > gpurun_out/final/prof_fq4lut.txt 2>&1; head -c 600 gpurun_out/final/prof_fq4lut.txt
