@@ -31,6 +31,8 @@ int multi_depth(int d);
 // K4s sliced multi-output (same depths / outputs); record slot bytes for leaf storage
 const void* pick_multi_slice(int di, int cmp, int leaf, int c, int* di_out);
 int multi_slice_slot(int leaf, int c);
+// K2f fanned-out small-batch apply (depths 1..8)
+const void* pick_fan(int di, int cmp, int leaf);
 // K5 staged multi-output (fp32 records; depths 4/6/8/10, outputs 2..10)
 const void* pick_multi_staged(int di, int cmp, int c, int* di_out);
 

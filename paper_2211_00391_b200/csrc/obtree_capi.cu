@@ -902,6 +902,43 @@ int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, int tpw, d
   return OBT_OK;
 }
 
+size_t fan_smem(const obt_model* m);
+int fan_stages(const obt_model* m);
+
+int launch_fan(obt_model* m, const uint8_t* q, int64_t n, double* out, cudaStream_t stream) {
+  const void* fn = obt::pick_fan(m->depth_inst, m->compare_mode, m->leaf_storage);
+  if (!fn) return fail(OBT_E_UNSUPPORTED, "no fanned-out apply kernel for depth %d", m->depth_inst);
+  const TilePlan* tp = nullptr;
+  int rc = get_tile_plan(m, 128, 0, &tp);
+  if (rc != OBT_OK) return rc;
+  obt::ApplyParams p{};
+  p.q = q;
+  p.chunks = tp->d_chunks;
+  p.out = out;
+  p.n = n;
+  p.tile = 128;
+  p.chunk_trees = m->chunk_trees;
+  p.chunk_begin = 0;
+  p.chunk_end = m->n_chunks;
+  p.chunk_bytes = m->chunk_bytes;
+  p.desc_bytes = m->desc_bytes;
+  p.q_tile_bytes = (uint32_t)((size_t)m->n_features * 128);
+  p.n_stages = fan_stages(m);
+  p.tree_begin = 0;
+  p.tree_end = m->n_trees;
+  p.first = 1;
+  p.last = 1;
+  p.scale = m->scale;
+  p.bias = m->bias;
+  const size_t smem = fan_smem(m);
+  CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, m->smem_optin));
+  void* kargs[] = {&p};
+  const dim3 grid((unsigned)((n + 127) / 128)), block(obt::kFanThreads);
+  CUDA_TRY(cudaLaunchKernel(fn, grid, block, kargs, smem, stream));
+  ++g_launches;
+  return OBT_OK;
+}
+
 int launch_multi_staged(obt_model* m, const uint8_t* q, int64_t n, double* out, cudaStream_t stream) {
   int di = 0;
   const void* fn = obt::pick_multi_staged(m->depth_inst, m->compare_mode, m->n_outputs, &di);
@@ -1006,11 +1043,39 @@ struct Regions {
   int n_reg = 1;
   int64_t begin[2] = {0, 0}, count[2] = {0, 0};
   int tile[2] = {-1, -1};
+  bool fan = false;  // K2f: 128-object blocks, trees fanned out over the CTA's warps
 };
+
+// K2f for small batches: the 128-object blocks fill no more than two waves, the model
+// has trees for every compute warp, and the CTA's ring, value panel and bucket tile fit.
+// OBT_FAN=0 / 1 forbids / forces it (where it can run).
+size_t fan_fixed_smem(const obt_model* m) {
+  return 512 + 2 * (size_t)m->chunk_trees * 128 * leaf_size(m->leaf_storage) + (size_t)m->n_features * 128;
+}
+int fan_stages(const obt_model* m) {
+  const int64_t room = ((int64_t)m->smem_optin - (int64_t)fan_fixed_smem(m)) / (int64_t)m->chunk_bytes;
+  return (int)std::max<int64_t>(0, std::min<int64_t>({room, 8, std::max(m->n_chunks, 2)}));
+}
+size_t fan_smem(const obt_model* m) { return fan_fixed_smem(m) + (size_t)fan_stages(m) * m->chunk_bytes; }
+bool fan_eligible(const obt_model* m, int64_t n) {
+  if (m->n_outputs > 1 || m->depth_inst > 8 || m->n_trees == 0 || n <= 0) return false;
+  if (fan_stages(m) < 2 || fan_smem(m) > (size_t)m->smem_optin) return false;
+  if (!obt::pick_fan(m->depth_inst, m->compare_mode, m->leaf_storage)) return false;
+  const char* e = getenv("OBT_FAN");
+  if (e && !strcmp(e, "0")) return false;
+  if (e && !strcmp(e, "1")) return true;
+  const int64_t blocks = (n + 127) / 128;
+  return blocks <= 2 * (int64_t)m->sm_count && m->n_trees >= 4 * obt::kFanComputeWarps;
+}
 
 Regions plan_regions(const obt_model* m, int64_t n, bool split_ok) {
   Regions r;
   r.count[0] = n;
+  if (split_ok && fan_eligible(m, n)) {
+    r.tile[0] = 128;
+    r.fan = true;
+    return r;
+  }
   r.tile[0] = plan_tile(m, n);
   const char* e = getenv("OBT_TAIL_SPLIT");  // "0" never, "1" whenever a tail exists
   if (!split_ok || r.tile[0] < 0 || m->n_outputs > 1 || (e && !strcmp(e, "0"))) return r;
@@ -1320,7 +1385,7 @@ static int predict_impl(obt_model* m, const float* x, int64_t n, int32_t layout,
   uint8_t* qr[2] = {q, q + workspace_bytes(m, reg.count[0], reg.tile[0])};
   uint32_t* flags = reinterpret_cast<uint32_t*>(q + regions_bucket_bytes(m, reg));
   int tpw[2] = {1, 1};
-  for (int i = 0; i < reg.n_reg; ++i) tpw[i] = apply_lanes(m, reg.tile[i], idx_out != nullptr);
+  for (int i = 0; i < reg.n_reg; ++i) tpw[i] = reg.fan ? 1 : apply_lanes(m, reg.tile[i], idx_out != nullptr);
   if (ev_begin) CUDA_TRY(cudaEventRecord(ev_begin, stream));
   SecondRegion r2;
   int64_t n_slots = ((reg.count[0] + reg.tile[0] - 1) / reg.tile[0]) * (int64_t)reg.tile[0];
@@ -1338,6 +1403,8 @@ static int predict_impl(obt_model* m, const float* x, int64_t n, int32_t layout,
     if (m->n_outputs > 1) {
       rc = idx_out ? fail(OBT_E_UNSUPPORTED, "leaf-index dumps are implemented for single-output models")
                    : launch_multi(m, qr[i], c, out + b * m->n_outputs, stream);
+    } else if (reg.fan) {
+      rc = launch_fan(m, qr[i], c, out + b, stream);
     } else {
       rc = launch_apply(m, qr[i], c, reg.tile[i], tpw[i], out ? out + b : nullptr, idx_out, tree_begin, tree_end, stream,
                         i == 0 && reg.n_reg == 1 ? flags : nullptr);

@@ -772,6 +772,9 @@ __device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) {
   return (a & b) | (a & c) | (b & c);
 }
 
+// Byte k (runtime-unrolled constant) of a packed index word, zero-extended.
+__device__ __forceinline__ uint32_t byte_of_rt(uint32_t w, int k) { return (w >> (8 * k)) & 0xffu; }
+
 // Byte k of a packed index word, zero-extended (one PRMT).
 template <int K>
 __device__ __forceinline__ uint32_t byte_of(uint32_t w) {
@@ -1099,6 +1102,139 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid
         __threadfence();
         st_release_gpu(p.tile_flags + tile_idx, (uint32_t)p.flag_set);
       }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2f: fanned-out apply for small batches.  K2 walks every tree of the model in order
+// inside one CTA per tile, so a batch of a few thousand objects runs on a few SMs with
+// one to three warps each (config 1: 79 CTAs of 128 objects, 18.5 us for 500 trees).
+// Here a CTA owns one 128-object block and 16 warps: 12 compute warps split each chunk's
+// trees among themselves (tree t of the chunk -> warp t mod 12; lane = 4 objects as in
+// K2) and write the gathered leaves to a shared value panel [tree][object]; 4 fold warps
+// (one object per thread) then add the panel's rows in tree order -- the binary64 (or
+// binary32) fold is still the reference's left fold, only the index and gather work is
+// spread.  Chunk records (descriptors + tables, the K2 shared-memory format for a
+// 128-object tile) stream through an S-stage TMA ring (as many stages as fit, up to 8:
+// a chunk's compute is short next to its load latency); the value panel is double buffered.
+constexpr int kFanComputeWarps = 12;
+constexpr int kFanFoldWarps = 4;
+constexpr int kFanThreads = 32 * (kFanComputeWarps + kFanFoldWarps);
+
+template <int DI, int CMP, int LEAF>
+__global__ void __launch_bounds__(kFanThreads, 1) apply_fan_kernel(const __grid_constant__ ApplyParams p) {
+  using LT = LeafT<LEAF>;
+  using leaf_t = typename LT::T;
+  using acc_t = typename LT::Acc;
+  constexpr int kDW = desc_words(CMP);
+  constexpr int kTabStride = leaf_table_stride(DI, (int)sizeof(leaf_t));
+  extern __shared__ __align__(128) unsigned char fan_raw[];
+  unsigned char* smem = fan_raw + ((256u - (smem_u32(fan_raw) & 255u)) & 255u);
+  const int S = p.n_stages;                            // chunk-record ring depth (<= 8)
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [S] chunk record landed
+  uint64_t* sfree = full + 8;                          // [S] chunk record consumed (compute warps)
+  uint64_t* vfull = full + 16;                         // [2] value panel written (compute warps)
+  uint64_t* vfree = full + 18;                         // [2] value panel folded (fold warps)
+  uint64_t* tile_bar = full + 20;
+  unsigned char* stages = smem + 256;
+  const int ct = p.chunk_trees;
+  leaf_t* panel = reinterpret_cast<leaf_t*>(stages + (size_t)S * p.chunk_bytes);  // [2][ct][128]
+  unsigned char* qtile = reinterpret_cast<unsigned char*>(panel + 2 * (size_t)ct * 128);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n_chunks = p.chunk_end - p.chunk_begin;
+  const int64_t blk = (int64_t)blockIdx.x * 128;
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&sfree[i], 32 * kFanComputeWarps);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&vfull[i], 32 * kFanComputeWarps);
+      mbar_init(&vfree[i], 32 * kFanFoldWarps);
+    }
+    mbar_init(tile_bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp < kFanFoldWarps) {
+    // fold warps: thread j folds object blk + j (word j & 31, byte j >> 5) in tree order
+    const int j = tid;
+    const int64_t o = blk + j;
+    acc_t acc = (p.first || o >= p.n) ? (acc_t)0 : (acc_t)p.out[o];
+    for (int c = 0; c < n_chunks; ++c) {
+      const int v = c & 1;
+      mbar_wait_warp(&vfull[v], (uint32_t)(c >> 1) & 1u);
+      const leaf_t* row = panel + (size_t)v * ct * 128 + j;
+      // eight loads (and widenings) ahead of their adds: only the add chain is serial
+      int t = 0;
+      for (; t + 8 <= ct; t += 8) {
+        acc_t w[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) w[u] = LT::widen(row[(size_t)(t + u) * 128]);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += w[u];
+      }
+      for (; t < ct; ++t) acc += LT::widen(row[(size_t)t * 128]);
+      mbar_arrive(&vfree[v]);
+    }
+    if (o < p.n) p.out[o] = p.last ? __dadd_rn(__dmul_rn((double)acc, p.scale), p.bias) : (double)acc;
+    return;
+  }
+  // compute warps
+  const int cw = warp - kFanFoldWarps;
+  if (cw == 0 && lane == 0) {
+    mbar_expect_tx(tile_bar, p.q_tile_bytes);
+    bulk_g2s_split(qtile, p.q + (int64_t)blockIdx.x * p.q_tile_bytes, p.q_tile_bytes, tile_bar);
+    for (int c = 0; c < S && c < n_chunks; ++c) {
+      mbar_expect_tx(&full[c], p.chunk_bytes);
+      bulk_g2s_split(stages + (size_t)c * p.chunk_bytes, p.chunks + (size_t)(p.chunk_begin + c) * p.chunk_bytes,
+                     p.chunk_bytes, &full[c]);
+    }
+  }
+  const uint32_t my_q = smem_u32(qtile) + 4 * lane;
+  mbar_wait_warp(tile_bar, 0);
+  for (int c = 0; c < n_chunks; ++c) {
+    const int s = c % S, v = c & 1;
+    mbar_wait_warp(&full[s], (uint32_t)(c / S) & 1u);
+    if (c >= 2) mbar_wait_warp(&vfree[v], (uint32_t)((c >> 1) - 1) & 1u);
+    const unsigned char* st = stages + (size_t)s * p.chunk_bytes;
+    const uint32_t* dw = reinterpret_cast<const uint32_t*>(st);
+    const uint32_t leaf_base = smem_u32(st + p.desc_bytes);
+    leaf_t* prow = panel + (size_t)v * ct * 128;
+#pragma unroll 4
+    for (int t = cw; t < ct; t += kFanComputeWarps) {
+      uint32_t lo = 0, hi = 0;
+#pragma unroll
+      for (int d = 0; d < DI; ++d) {
+        const uint32_t d0 = dw[(t * DI + d) * kDW], d1 = dw[(t * DI + d) * kDW + (kDW - 1)];
+        uint32_t b7;
+        if constexpr (CMP == 7 && kDW == 1) {
+          b7 = lds_u32(my_q + (d0 >> 8)) + __byte_perm(d0, 0u, 0x0000u);
+        } else if constexpr (CMP == 7) {
+          b7 = lds_u32(my_q + d0) + d1;
+        } else {
+          const uint32_t w = lds_u32(my_q + (d0 >> 8));
+          b7 = maj3((w & 0x7f7f7f7fu) + (__byte_perm(d0, 0u, 0x0000u) & 0x7f7f7f7fu), w, d1);
+        }
+        if (d < 8) lo |= (b7 >> (7 - d)) & (0x01010101u << d);
+        else hi |= (b7 >> (15 - d)) & (0x01010101u << (d - 8));
+      }
+      const uint32_t tab = leaf_base + (uint32_t)t * kTabStride;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t idx = byte_of_rt(lo, k) | (DI > 8 ? byte_of_rt(hi, k) << 8 : 0u);
+        prow[(size_t)t * 128 + lane + 32 * k] = lds_leaf<LEAF>(tab + (idx << LT::kShift));
+      }
+    }
+    mbar_arrive(&sfree[s]);
+    mbar_arrive(&vfull[v]);
+    // refill stage s with chunk c + S once every compute thread has read it
+    if (cw == 0 && lane == 0 && c + S < n_chunks) {
+      mbar_wait(&sfree[s], (uint32_t)(c / S) & 1u);
+      mbar_expect_tx(&full[s], p.chunk_bytes);
+      bulk_g2s_split(stages + (size_t)s * p.chunk_bytes, p.chunks + (size_t)(p.chunk_begin + c + S) * p.chunk_bytes,
+                     p.chunk_bytes, &full[s]);
     }
   }
 }

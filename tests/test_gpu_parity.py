@@ -230,6 +230,7 @@ def test_descriptor_sources_and_multi_launch_fold(monkeypatch, source, strategy)
     parameter path folds across 3 launches through the carried accumulators; the
     shared-memory path streams all descriptors in one launch.  Both are bit-exact."""
     monkeypatch.setenv("OBT_DESC_SOURCE", source)
+    monkeypatch.setenv("OBT_FAN", "0")  # the K2 / K2s paths, not the small-batch K2f
     model = _model(12, 50, 3001, 6, seed=77)
     x = _features(model, 2500, seed=78)
     prec = oracle.BINARY64 if strategy is obt.LeafStrategy.NAIVE else oracle.BINARY16
@@ -300,6 +301,7 @@ def test_no_writes_outside_outputs_and_workspace(monkeypatch, n, tpw):
     vector and the bucket workspace must be untouched after a predict (ragged n, both
     apply kernels), and results must still match the oracle."""
     monkeypatch.setenv("OBT_TPW", tpw)
+    monkeypatch.setenv("OBT_FAN", "0")  # the K2 / K2s paths, not the small-batch K2f
     model = _model(24, 60, 75, 6, seed=n)
     x = _features(model, n, seed=n)
     ev = obt.Evaluator(model)
@@ -364,6 +366,7 @@ def test_reference_corpus_on_gpu():
 def test_depth_split_lanes_bit_exact(monkeypatch, tpw, D, F, B, T):
     """K2s: TPW lanes per bucket word (OBT_TPW forces it) keep the tree-order fold exact."""
     monkeypatch.setenv("OBT_TPW", tpw)
+    monkeypatch.setenv("OBT_FAN", "0")  # the K2 / K2s paths, not the small-batch K2f
     model = _model(F, B, T, D, seed=D * 100 + F)
     x = _features(model, 3001, seed=D + F)
     fm = oracle.flatten(model)
@@ -672,3 +675,38 @@ def test_tail_split_behind_parameter_bank(monkeypatch, split):
     want = oracle.evaluate_scalar(oracle.flatten(model), x)
     got = obt.Evaluator(model).predict_device(torch.from_numpy(x).cuda()).cpu().numpy()
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("D", [1, 3, 6, 8])
+@pytest.mark.parametrize("B", [16, 200])
+@pytest.mark.parametrize("n", [1, 127, 129, 5000])
+def test_fanned_out_small_batch_apply(monkeypatch, D, B, n):
+    """K2f (small batches: trees fanned out over a CTA's compute warps, the fold in tree
+    order by the fold warps) bit-exact against the oracle in both precision families, and
+    equal to the K2 / K2s path (OBT_FAN=0)."""
+    model = _model(21, B, 131, D, seed=D * 31 + B)  # 131 trees: a ragged last chunk
+    x = _features(model, n, seed=n + D)
+    fm = oracle.flatten(model)
+    for strategy, prec in ((obt.LeafStrategy.NAIVE, oracle.BINARY64), (obt.LeafStrategy.NAIVE16, oracle.BINARY16)):
+        monkeypatch.setenv("OBT_FAN", "1")
+        ev = obt.Evaluator(model, obt.EvalConfig(strategy=strategy))
+        got = ev.predict_device(torch.from_numpy(x).cuda()).cpu().numpy()
+        want = oracle.evaluate_scalar(fm, x, oracle.OBJECT_MAJOR, prec)
+        assert np.array_equal(got, want), (strategy, int(np.count_nonzero(got != want)))
+        monkeypatch.setenv("OBT_FAN", "0")
+        assert np.array_equal(ev.predict_device(torch.from_numpy(x).cuda()).cpu().numpy(), want)
+
+
+def test_fanned_out_binary64_leaf_tables(monkeypatch):
+    """K2f with binary64 leaf tables (leaves not exactly binary32)."""
+    monkeypatch.setenv("OBT_FAN", "1")
+    rng = np.random.default_rng(5)
+    base = _model(13, 40, 97, 5, seed=5)
+    trees = tuple(obt.ObliviousTree(depth=t.depth, splits=t.splits, leaf_values=rng.normal(0, 1, 1 << t.depth))
+                  for t in base.trees)
+    model = obt.ObliviousModel(base.float_features, trees, scale=1.5, bias=0.25)
+    x = _features(model, 3000, seed=6)
+    ev = obt.Evaluator(model)
+    got = ev.predict_device(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert ev.leaf_storage == "fp64"
+    assert np.array_equal(got, oracle.evaluate_scalar(oracle.flatten(model), x))
