@@ -40,9 +40,12 @@ FALLBACK_HBM_GBS = 6650.0
 FALLBACK_SM_MHZ = 1965.0
 
 
-def quantize_search(ev) -> str:
+def quantize_search(ev, n_features: int) -> str:
     """The predict path's quantize search: cells(k) = cell-table kernel with k compares
-    per value, eytzinger(L) = L-level search."""
+    per value, eytzinger(L) = L-level search; rows that are not 16-byte multiples
+    (F % 4 != 0) take the LDG-loaded Eytzinger kernel instead of the TMA-staged ones."""
+    if n_features % 4:
+        return "eytzinger (LDG rows: F % 4 != 0)"
     if not hasattr(ev, "quantize_kernel"):
         return "n/a"
     kind, param = ev.quantize_kernel()
@@ -447,9 +450,11 @@ def run_ours(args, world, rank, local):
                    "borders": spec.borders, "trees": spec.n_trees, "depth": spec.depth,
                    "leaves": "fp16 (binary32 fold)" if spec.half_leaves else "fp32 values (binary64 fold)",
                    "leaf_storage_on_device": ev.leaf_storage,
-                   "quantize_search": quantize_search(ev),
+                   "quantize_search": quantize_search(ev, spec.n_features),
                    **({"multi_apply": ev.apply_kernel()} if hasattr(ev, "apply_kernel") else {}),
-                   "l2": "inputs larger than L2 (features 4NF bytes, buckets NF bytes > 126 MB)",
+                   "l2": ("inputs larger than L2 (features 4NF bytes, buckets NF bytes > 126 MB)"
+                          if 4 * N * spec.n_features > 126e6 else
+                          "inputs L2-resident between steps (features 4NF bytes < 126 MB; a launch-bound size)"),
                    "parallelism": f"objects sharded over {world} GPU(s), no data-path collective",
                    "launch": "CUDA graph replay of one predict" if graph is not None else "stream launches"},
         "e2e": e2e,
