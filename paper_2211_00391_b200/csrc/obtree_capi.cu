@@ -1231,8 +1231,8 @@ int obt_model_create(const obt_model_desc* d, int device, obt_model** out) {
     // two stages (one tree's table + its bucket rows each) fit shared memory
     {
       const char* mst = getenv("OBT_MULTI_STAGED");  // A/B knob: 0 = K4
-      const int CPs = (C + 3) / 4 * 4;
-      const uint32_t table = (uint32_t)(per_tree * CPs * 4);
+      const int CPs = obt::staged_record_values(C);
+      const uint32_t table = (uint32_t)((per_tree * CPs * 4 + 15) / 16 * 16);
       const uint32_t stage = (table + (uint32_t)DI * obt::kStagedTile + 127u) & ~127u;
       const int stages = std::min(8, (int)(((size_t)m->smem_optin - 512) / stage));
       int sdi = 0;
@@ -1245,8 +1245,9 @@ int obt_model_create(const obt_model_desc* d, int device, obt_model** out) {
         m->staged_stage_bytes = stage;
       }
     }
-    m->multi_slot = m->multi_slice ? obt::multi_slice_slot(m->leaf_storage, C)
-                                   : obt::multi_record_values(m->leaf_storage, C) * (int)ls;
+    m->multi_slot = m->multi_slice    ? obt::multi_slice_slot(m->leaf_storage, C)
+                    : m->multi_staged ? obt::staged_record_values(C) * (int)ls
+                                      : obt::multi_record_values(m->leaf_storage, C) * (int)ls;
     std::vector<uint8_t> rec((size_t)std::max(m->n_trees, 1) * per_tree * m->multi_slot, 0);
     for (int t = 0; t < m->n_trees; ++t)
       for (int c = 0; c < C; ++c)

@@ -1704,6 +1704,15 @@ __global__ void __launch_bounds__(128) apply_multi_slice_kernel(const __grid_con
 // shared memory only: one table load serves 2048 objects (24 B of L2 traffic per
 // object-tree instead of a 48-byte record fetch), and every load the fold waits on is a
 // shared-memory load.  Descriptors come from the K4 array ({f * 512, k} / {(f*512) << 8 | k, s}).
+#ifndef OBT_STAGED_ODD
+// K5 records with an odd stride (C or C + 1 fp32 values) read as 4-byte loads, so the
+// 32 lanes' records start on all 32 banks: measured 441 vs 334 ms at config 5 (ten
+// loads of ~3.5 wavefronts each cost more than three 16-byte loads of ~10)
+#define OBT_STAGED_ODD 0
+#endif
+__host__ __device__ constexpr int staged_record_values(int c) {
+  return OBT_STAGED_ODD ? (c % 2 ? c : c + 1) : (c + 3) / 4 * 4;
+}
 #ifndef OBT_STAGED_V2
 #define OBT_STAGED_V2 0  // K5 record reads as 8-byte loads (C values) instead of 16-byte rows
 #endif
@@ -1728,7 +1737,7 @@ struct StagedParams {
 
 template <int DI, int CMP, int C>
 __global__ void __launch_bounds__(kStagedThreads, 1) apply_multi_staged_kernel(const __grid_constant__ StagedParams p) {
-  constexpr int CP = (C + 3) / 4 * 4;  // fp32 record values (16-byte rows)
+  constexpr int CP = staged_record_values(C);
   constexpr int kRows = CP / 4;
   extern __shared__ __align__(128) unsigned char st_raw[];
   unsigned char* smem = st_raw + ((128u - (smem_u32(st_raw) & 127u)) & 127u);
@@ -1804,7 +1813,11 @@ __global__ void __launch_bounds__(kStagedThreads, 1) apply_multi_staged_kernel(c
       const uint32_t idx = ((lo >> (8 * k)) & 0xffu) | (DI > 8 ? ((hi >> (8 * k)) & 0xffu) << 8 : 0u);
       const uint32_t rec = tab + idx * (uint32_t)(CP * 4);
       float v[CP];
-      if constexpr (OBT_STAGED_V2) {
+      if constexpr (OBT_STAGED_ODD) {
+        // odd record stride: value c of 32 random records spreads over all 32 banks
+#pragma unroll
+        for (int c = 0; c < C; ++c) v[c] = lds_leaf<1>(rec + 4u * c);
+      } else if constexpr (OBT_STAGED_V2) {
         // 8-byte loads of the C values only (no padding read): half-warp phases
 #pragma unroll
         for (int r = 0; r < (C + 1) / 2; ++r)
