@@ -847,7 +847,7 @@ int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, int tpw, d
   // flags).  Not under stream capture.  OBT_PDL=0 disables it.
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   CUDA_TRY(cudaStreamIsCapturing(stream, &cap));
-  const char* pe = getenv("OBT_PDL");
+  const char* pe = getenv("OBT_PDL");  // read per call
   const bool chain = flags && dsrc && !write_idx && n_launch > 1 && k.words == 1 && cap == cudaStreamCaptureStatusNone &&
                      !(pe && !strcmp(pe, "0"));
   if (chain) CUDA_TRY(cudaMemsetAsync(flags, 0, (size_t)n_tiles * 4, stream));

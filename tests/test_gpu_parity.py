@@ -710,3 +710,19 @@ def test_fanned_out_binary64_leaf_tables(monkeypatch):
     got = ev.predict_device(torch.from_numpy(x).cuda()).cpu().numpy()
     assert ev.leaf_storage == "fp64"
     assert np.array_equal(got, oracle.evaluate_scalar(oracle.flatten(model), x))
+
+
+def test_chained_parameter_bank_launches(monkeypatch):
+    """Launch chaining (programmatic dependent launches with per-tile carry flags): a
+    2000-tree depth-6 model folds over 3 parameter-bank launches of 2 waves each; the
+    chained and the plainly serialised launches equal the oracle bit for bit."""
+    model = _model(24, 64, 2000, 6, seed=91)
+    n = 600001
+    x = _features(model, n, seed=92, specials=False)
+    want = oracle.evaluate_scalar(oracle.flatten(model), x)
+    ev = obt.Evaluator(model)
+    xd = torch.from_numpy(x).cuda()
+    for pdl in ("1", "0", "1"):
+        monkeypatch.setenv("OBT_PDL", pdl)
+        got = ev.predict_device(xd).cpu().numpy()
+        assert np.array_equal(got, want), (pdl, int(np.count_nonzero(got != want)))
