@@ -20,6 +20,8 @@ QuantFn pick_quant(int levels, int layout, bool tiled);
 QuantTmaFn pick_quant_tma(int levels);
 // K1L, cell-table quantize with kmax (1..4) compares per value, 256 or 1024 cells
 QuantTmaFn pick_quant_lut(int kmax, int cells);
+// K1 (LDG-loaded rows) with the cell-table search, tiled output
+QuantFn pick_quant_ldg_lut(int kmax, int cells, int layout);
 // K2, depths {1..8, 10, 12}
 ApplyKernel pick_apply(int di, int cmp, int leaf, bool write_idx, int dsrc);
 // K2s, depth-split (tpw 2: depths 2/4/6/8, tpw 4: depths 4/8)

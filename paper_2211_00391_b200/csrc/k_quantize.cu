@@ -39,6 +39,22 @@ QuantTmaFn pick_quant_tma(int levels) {
   }
 }
 
+template <int LAYOUT, int CELLS>
+static QuantFn ldg_lut(int kmax) {
+  switch (kmax) {
+    case 1: return quantize_kernel<1, LAYOUT, true, CELLS>;
+    case 2: return quantize_kernel<2, LAYOUT, true, CELLS>;
+    case 3: return quantize_kernel<3, LAYOUT, true, CELLS>;
+    case 4: return quantize_kernel<4, LAYOUT, true, CELLS>;
+    default: return nullptr;
+  }
+}
+
+QuantFn pick_quant_ldg_lut(int kmax, int cells, int layout) {
+  if (cells == 1024) return layout == 0 ? ldg_lut<0, 1024>(kmax) : ldg_lut<1, 1024>(kmax);
+  return layout == 0 ? ldg_lut<0, 256>(kmax) : ldg_lut<1, 256>(kmax);
+}
+
 QuantTmaFn pick_quant_lut(int kmax, int cells) {
   if (cells == 1024) {
     switch (kmax) {

@@ -780,11 +780,19 @@ int launch_quantize(const obt_model* m, const float* x, int64_t n, int layout, u
     }
   }
 
-  QuantFn fn = pick_quant(bt.levels, layout, tiled);
+  // K1 (rows loaded by each lane): the cell-table search where K1L would run, else Eytzinger
+  const char* le = getenv("OBT_LDG_LUT");  // A/B knob: 0 = Eytzinger in the LDG kernel
+  const bool ldg_lut = use_lut && !(le && !strcmp(le, "0"));
+  QuantFn fn = ldg_lut ? obt::pick_quant_ldg_lut(lt.kmax, lt.cells, layout) : pick_quant(bt.levels, layout, tiled);
   if (!fn) return fail(OBT_E_UNSUPPORTED, "no quantize kernel for %d levels", bt.levels);
-  const int fc = quantize_chunk(m, bt, n_slots, obt::kQuantSmem);
-  const size_t smem = bt.levels > 0 ? (size_t)std::min(fc, F) * bt.pitch * 4 : 16;
+  const int fc = ldg_lut ? quantize_chunk_bytes(m, (size_t)lt.cells + lt.rec_stride, n_slots, obt::kQuantSmem - 256)
+                         : quantize_chunk(m, bt, n_slots, obt::kQuantSmem);
+  const size_t smem = ldg_lut ? 256 + (size_t)std::min(fc, F) * (lt.cells + lt.rec_stride)
+                              : (bt.levels > 0 ? (size_t)std::min(fc, F) * bt.pitch * 4 : 16);
   p.chunk_features = fc;
+  p.lut = lt.d_lut;
+  p.lrec = lt.d_rec;
+  p.lrec_stride = lt.rec_stride;
   // the opt-in maximum, not this launch's size: the attribute is per function and
   // process-wide, so every caller must set the same value (concurrent launches race otherwise)
   CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, m->smem_optin));

@@ -349,10 +349,16 @@ __device__ __forceinline__ void quantize_step(const QuantizeParams& p, const flo
 // bucket stores (each warp writes 128 contiguous bytes of a feature row of the tile).
 // The fallback for inputs the TMA-staged kernel (K1t) does not take, and the plain
 // [F][n] output of obt_quantize_dev.
-template <int L, int LAYOUT, bool TILED>
+template <int KMAX, int CELLS>
+__device__ __forceinline__ void lut_step(const QuantizeParams& p, uint32_t luts_s, const unsigned char* recs,
+                                         uint32_t recs_s, const float (&v)[kQuantStep][4], int f0, int fq, int nf,
+                                         int64_t base, int lane, bool full_objs);
+// LUT_CELLS > 0: the cell-table search (K1L's, tiled output only) with L = KMAX compares;
+// the shared memory then holds the chunk's cell tables instead of Eytzinger arrays.
+template <int L, int LAYOUT, bool TILED, int LUT_CELLS = 0>
 __global__ void __launch_bounds__(kQuantThreads, 2) quantize_kernel(QuantizeParams p) {
   extern __shared__ __align__(16) unsigned char qsm[];
-  constexpr int kE = (1 << L) - 1;
+  constexpr int kE = LUT_CELLS ? 0 : (1 << L) - 1;
   constexpr int S = kQuantStep;
   float* ey = reinterpret_cast<float*>(qsm);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -370,6 +376,17 @@ __global__ void __launch_bounds__(kQuantThreads, 2) quantize_kernel(QuantizePara
   if (kE > 0) {
     const float* src = p.eytz + (int64_t)f0 * kE;
     for (int i = threadIdx.x; i < nf * kE; i += kQuantThreads) ey[i] = __ldg(src + i);
+  }
+  // cell tables: luts 256-aligned (the PRMT address trick), recs right behind them
+  unsigned char* luts = qsm + ((256u - (smem_u32(qsm) & 255u)) & 255u);
+  unsigned char* recs = luts + (size_t)nf * (LUT_CELLS ? LUT_CELLS : 1);
+  if constexpr (LUT_CELLS > 0) {
+    const uint4* src = reinterpret_cast<const uint4*>(p.lut + (size_t)f0 * LUT_CELLS);
+    uint4* dst = reinterpret_cast<uint4*>(luts);
+    for (int i = threadIdx.x; i < nf * LUT_CELLS / 16; i += kQuantThreads) dst[i] = __ldg(src + i);
+    const uint4* rsrc = reinterpret_cast<const uint4*>(p.lrec + (size_t)f0 * p.lrec_stride);
+    uint4* rdst = reinterpret_cast<uint4*>(recs);
+    for (int i = threadIdx.x; i < nf * p.lrec_stride / 16; i += kQuantThreads) rdst[i] = __ldg(rsrc + i);
   }
   __syncthreads();
 
@@ -432,7 +449,12 @@ __global__ void __launch_bounds__(kQuantThreads, 2) quantize_kernel(QuantizePara
   for (int fq = 0; fq < nf; fq += S) {
     float v[S][4];
     load_step(v, fq);
-    quantize_step<L, TILED>(p, ey, v, f0, fq, nf, base, lane, full_objs);
+    if constexpr (LUT_CELLS > 0) {
+      static_assert(TILED, "cell tables cover the used borders: tiled output only");
+      lut_step<L, LUT_CELLS>(p, smem_u32(luts), recs, smem_u32(recs), v, f0, fq, nf, base, lane, full_objs);
+    } else {
+      quantize_step<L, TILED>(p, ey, v, f0, fq, nf, base, lane, full_objs);
+    }
   }
 }
 
@@ -565,6 +587,43 @@ __device__ __forceinline__ float lds_f32(uint32_t addr) {
   return v;
 }
 
+// The cell-table searches of one step (8 features x a lane's 4 objects) and its 8 packed
+// bucket-word stores (tiled output); luts / recs hold the chunk's tables in shared memory.
+template <int KMAX, int CELLS>
+__device__ __forceinline__ void lut_step(const QuantizeParams& p, uint32_t luts_s, const unsigned char* recs,
+                                         uint32_t recs_s, const float (&v)[kQuantStep][4], int f0, int fq, int nf,
+                                         int64_t base, int lane, bool full_objs) {
+  const int rs = p.lrec_stride;
+  uint32_t bk[kQuantStep][4];
+#pragma unroll
+  for (int j = 0; j < kQuantStep; ++j) {
+    const int fl = min(fq + j, nf - 1);
+    const float4 h = *reinterpret_cast<const float4*>(recs + (size_t)fl * rs);  // lo, hi, s, o (broadcast)
+    const uint32_t lut_base = luts_s + (uint32_t)fl * CELLS;
+    const uint32_t bord = recs_s + (uint32_t)fl * rs + kLutRecHeader;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float x = v[j][k];
+      const float y = __fmaf_rn(fminf(fmaxf(x, h.x), h.y), h.z, h.w);
+      // 256 cells: the cell byte drops into byte 0 of the 256-aligned table address (PRMT);
+      // 1024 cells: the low 10 bits of y's bits index the table
+      const uint32_t cell_addr = CELLS == 256 ? __byte_perm(__float_as_uint(y), lut_base, 0x7650u)
+                                              : lut_base + (__float_as_uint(y) & (uint32_t)(CELLS - 1));
+      uint32_t b = lds_u8(cell_addr);
+#pragma unroll
+      for (int i = 0; i < KMAX; ++i) b = add_if_greater(b, x, lds_f32(bord + 4u * b), 1u);
+      bk[j][k] = b;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kQuantStep; ++j) {
+    if (fq + j >= nf) break;
+    uint32_t word = bk[j][3] * 256u + bk[j][2];
+    word = word * 256u + bk[j][1];
+    word = word * 256u + bk[j][0];
+    store_bucket_word<true>(p, word, f0 + fq + j, base, lane, full_objs);
+  }
+}
 template <int KMAX, int CELLS>
 __global__ void __launch_bounds__(kQTThreads, 2) quantize_lut_kernel(const __grid_constant__ CUtensorMap rows,
                                                                      const QuantizeParams p) {
@@ -644,36 +703,7 @@ __global__ void __launch_bounds__(kQTThreads, 2) quantize_lut_kernel(const __gri
       v[4][k] = b.x; v[5][k] = b.y; v[6][k] = b.z; v[7][k] = b.w;
     }
     mbar_arrive(&empty[s]);
-    const int fq = st * kQuantStep;
-    uint32_t bk[kQuantStep][4];
-#pragma unroll
-    for (int j = 0; j < kQuantStep; ++j) {
-      const int fl = min(fq + j, nf - 1);
-      const float4 h = *reinterpret_cast<const float4*>(recs + (size_t)fl * rs);  // lo, hi, s, o (broadcast)
-      const uint32_t lut_base = luts_s + (uint32_t)fl * CELLS;
-      const uint32_t bord = recs_s + (uint32_t)fl * rs + kLutRecHeader;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float x = v[j][k];
-        const float y = __fmaf_rn(fminf(fmaxf(x, h.x), h.y), h.z, h.w);
-        // 256 cells: the cell byte drops into byte 0 of the 256-aligned table address (PRMT);
-        // 1024 cells: the low 10 bits of y's bits index the table
-        const uint32_t cell_addr = CELLS == 256 ? __byte_perm(__float_as_uint(y), lut_base, 0x7650u)
-                                                : lut_base + (__float_as_uint(y) & (uint32_t)(CELLS - 1));
-        uint32_t b = lds_u8(cell_addr);
-#pragma unroll
-        for (int i = 0; i < KMAX; ++i) b = add_if_greater(b, x, lds_f32(bord + 4u * b), 1u);
-        bk[j][k] = b;
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < kQuantStep; ++j) {
-      if (fq + j >= nf) break;
-      uint32_t word = bk[j][3] * 256u + bk[j][2];
-      word = word * 256u + bk[j][1];
-      word = word * 256u + bk[j][0];
-      store_bucket_word<true>(p, word, f0 + fq + j, base, lane, full_objs);
-    }
+    lut_step<KMAX, CELLS>(p, luts_s, recs, recs_s, v, f0, st * kQuantStep, nf, base, lane, full_objs);
   }
 }
 

@@ -659,8 +659,12 @@ def test_cell_table_quantize_edges(monkeypatch, name, expect, cells):
     got = ev.predict_device(torch.from_numpy(x).cuda()).cpu().numpy()
     assert np.array_equal(got, want), int(np.count_nonzero(got != want))
     assert dm.quantize_kernel()[0] == expect
+    # the LDG-loaded kernel (feature-major rows) runs the same cell-table search
+    xt = torch.from_numpy(np.ascontiguousarray(x.T)).cuda()
+    assert np.array_equal(ev.predict_device(xt, layout=obt.Layout.FEATURE_MAJOR).cpu().numpy(), want)
     monkeypatch.setenv("OBT_QUANT_LUT", "0")
     assert np.array_equal(ev.predict_device(torch.from_numpy(x).cuda()).cpu().numpy(), want)
+    assert np.array_equal(ev.predict_device(xt, layout=obt.Layout.FEATURE_MAJOR).cpu().numpy(), want)
 
 
 @pytest.mark.parametrize("split", ["1", "0", "auto"])
