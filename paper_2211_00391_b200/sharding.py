@@ -93,9 +93,14 @@ class ObjectShardedEvaluator:
         self.rank, self.world = dist.get_rank(), dist.get_world_size()
         self.model = model
         if local_predict is None:
-            from .evaluate import Evaluator
+            if hasattr(model, "subset"):  # a multi-output model (config 5): [n][C] scores per shard
+                from .multiclass import MultiOutputEvaluator
 
-            ev = Evaluator(model, config, device=device)
+                ev = MultiOutputEvaluator(model, device=device)
+            else:
+                from .evaluate import Evaluator
+
+                ev = Evaluator(model, config, device=device)
             local_predict = lambda m, x: ev.predict(x)  # noqa: E731
         self._predict = local_predict
 

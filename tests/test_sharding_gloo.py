@@ -57,6 +57,16 @@ def _worker(rank, world, port, case):
                 local = ev.predict(m, gather=False)
                 b, e = sharding.object_shard(x.shape[0], rank, world)
                 assert np.array_equal(local, full[b:e])
+        elif case == "objects_multi":
+            from paper_2211_00391_b200 import multiclass, synthetic
+
+            spec = synthetic.WorkloadSpec("m", 1, 9, 40, 101, 10, 0.01, n_outputs=10, cfg=5)
+            mm = multiclass.from_arrays(synthetic.model_arrays(spec, seed=3, affine=True))
+            full_m = oracle.evaluate_scalar(_flat(mm), x)
+            ev = sharding.ObjectShardedEvaluator(mm, local_predict=_oracle_predict)
+            got = ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
+            assert got.shape == (x.shape[0], 10)
+            assert np.array_equal(got, full_m), "object sharding of a multi-output model must be bit-exact"
         elif case == "trees_multi":
             from paper_2211_00391_b200 import multiclass, synthetic
 
@@ -79,7 +89,7 @@ def _worker(rank, world, port, case):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case", ["objects", "trees", "trees_multi"])
+@pytest.mark.parametrize("case", ["objects", "objects_multi", "trees", "trees_multi"])
 def test_two_rank_gloo(case):
     mp.spawn(_worker, args=(2, _free_port(), case), nprocs=2, join=True)
 
