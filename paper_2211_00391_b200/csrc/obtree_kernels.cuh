@@ -927,8 +927,10 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid
     if (tid == 0) {
       mbar_expect_tx(tile_bar, p.q_tile_bytes);
       bulk_g2s_split(qtile, p.q + tile_idx * (int64_t)p.q_tile_bytes, p.q_tile_bytes, tile_bar);
-      if (p.l2_wave > 0 && blockIdx.x + (unsigned)p.l2_wave < gridDim.x) {
-        const unsigned nb = blockIdx.x + (unsigned)p.l2_wave;
+      if (p.l2_wave > 0 && (blockIdx.x + (unsigned)p.l2_wave < gridDim.x || p.flag_set > 0)) {
+        // the next wave's tile; in the last wave of a chained launch, wrap to the first
+        // wave's tiles (the next launch starts there, same order)
+        const unsigned nb = (blockIdx.x + (unsigned)p.l2_wave) % gridDim.x;
         const int64_t nt = p.reverse ? (int64_t)(gridDim.x - 1 - nb) : (int64_t)nb;
         bulk_prefetch_l2(p.q + nt * (int64_t)p.q_tile_bytes, p.q_tile_bytes);
       }
