@@ -15,6 +15,19 @@
 //      packed leaf indices.  Leaves are gathered from shared memory and added in
 //      tree order in binary64 (binary32 for the binary16 family), exactly the
 //      reference fold, then out = acc * scale + bias with two roundings.
+//
+// Kernel index (DESIGN.md section 4 has each one's bound and measurements):
+//   K1   quantize_kernel          LDG-loaded rows; Eytzinger search or cell tables
+//   K1t  quantize_tma_kernel      TMA-staged rows, Eytzinger search
+//   K1L  quantize_lut_kernel      TMA-staged rows, cell-table search (256 / 1024 cells)
+//   K2   apply_kernel             one lane per bucket word; software-pipelined; descriptors
+//                                 from the parameter bank (chained launches) or the ring
+//   K2f  apply_fan_kernel         small batches: trees fanned out over 12 warps, in-order
+//                                 fold by 4 fold warps
+//   K2s  apply_split_kernel       depth-split lanes (wide feature sets)
+//   K4   apply_multi_kernel       multi-output, records gathered from L2
+//   K4s  apply_multi_slice_kernel multi-output, sliced records (knob)
+//   K5   apply_multi_staged_kernel multi-output, per-tree tables + bucket rows staged by TMA
 #pragma once
 
 #include <cuda.h>
