@@ -245,7 +245,7 @@ def test_descriptor_sources_and_multi_launch_fold(monkeypatch, source, strategy)
 
 @pytest.mark.parametrize("kernel", ["staged", "k4", "slice"])
 @pytest.mark.parametrize("D,C,F,B", [(10, 10, 40, 254), (6, 3, 17, 64), (8, 16, 9, 128), (3, 2, 5, 7), (12, 7, 13, 30),
-                                     (10, 9, 33, 100), (4, 5, 8, 200)])
+                                     (10, 9, 33, 100), (4, 5, 8, 200), (10, 4, 2, 254)])  # last: 8-bit compare
 def test_multi_output_bit_exact(monkeypatch, kernel, D, C, F, B):
     """Multi-output (config 5 shape family): K5 (staged tables, default where it applies:
     fp32 records, C <= 10, depth <= 10), K4 (OBT_MULTI_STAGED=0) and K4s (sliced records,
@@ -699,6 +699,18 @@ def test_fanned_out_small_batch_apply(monkeypatch, D, B, n):
         assert np.array_equal(got, want), (strategy, int(np.count_nonzero(got != want)))
         monkeypatch.setenv("OBT_FAN", "0")
         assert np.array_equal(ev.predict_device(torch.from_numpy(x).cuda()).cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("D", [4, 8])
+def test_fanned_out_eight_bit_compare(monkeypatch, D):
+    """K2f with the 8-bit compare (more than 127 used borders on a feature)."""
+    monkeypatch.setenv("OBT_FAN", "1")
+    model = _model(2, 254, 160, D, seed=D)  # 320+ splits on each of 2 features: > 127 used borders
+    x = _features(model, 2000, seed=D + 1)
+    ev = obt.Evaluator(model)
+    got = ev.predict_device(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert ev.tables.device_model(ev.precision, ev.device).compare_mode == 8
+    assert np.array_equal(got, oracle.evaluate_scalar(oracle.flatten(model), x))
 
 
 def test_fanned_out_binary64_leaf_tables(monkeypatch):
