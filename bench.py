@@ -229,6 +229,19 @@ def cpu_baseline(spec, model, seconds: float, verify_fn=None) -> dict:
     return out
 
 
+def load_ncu_mio(cfg: int):
+    """The dominant kernel's shared-memory wavefront rate as a fraction of peak (ncu), the
+    resource that binds this path on B200."""
+    path = ROOT / "profiles" / "ncu_apply_summary.json"
+    if not path.exists():
+        return None
+    try:
+        v = json.loads(path.read_text()).get(f"cfg{cfg}", {}).get("smem_wavefront_pct_of_peak")
+        return None if v is None else v / 100.0
+    except Exception:
+        return None
+
+
 def load_ncu_traffic(cfg: int):
     path = ROOT / "profiles" / "ncu_apply_summary.json"
     if not path.exists():
@@ -463,6 +476,8 @@ def run_ours(args, world, rank, local):
             "bound": "issue", "kernel": "apply_kernel (leaf index + gather + fold)",
             "achieved": apply_achieved / 1e12, "peak": p_int / 1e12, "unit": "Tlane-op/s",
             "frac": apply_achieved / p_int, "traffic": load_ncu_traffic(args.config),
+            "binding_resource": {"what": "shared-memory wavefronts (one 128-byte wavefront per SM per clock)",
+                                 "frac_of_peak_ncu": load_ncu_mio(args.config)},
             "algorithmic_ops_per_launch": terms["apply_ops"], "ms_per_launch": a_ms,
             "ops_definition": "N*T*D split compares + N*T*C leaf gathers (SURVEY.md 8d)",
             "peak_source": f"{n_sm} SMs x 128 lanes x {pk['sm_max_mhz']:.0f} MHz",
