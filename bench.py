@@ -167,6 +167,39 @@ def roofline_terms(spec) -> dict:
     }
 
 
+def gather_wavefronts(table_bytes: int, trials: int = 4000, seed: int = 7) -> float:
+    """Expected shared-memory wavefronts of one warp-wide random gather from a table of
+    `table_bytes` (4-byte banks, 32 banks, 32 lanes, uniform random 4-byte words; a
+    wavefront serves one distinct word per bank): E[max over banks of distinct words]."""
+    import numpy as np
+
+    words = max(1, table_bytes // 4)
+    if words <= 32:
+        return 1.0
+    rng = np.random.default_rng(seed)
+    idx = rng.integers(0, words, size=(trials, 32))
+    total = 0
+    for row in idx:
+        u = np.unique(row)
+        total += np.bincount(u % 32, minlength=32).max()
+    return total / trials
+
+
+def roofline_smem(spec, n_sm: int, sm_hz: float, hbm_gbs: float, leaf_bytes: int) -> dict:
+    """The B200 floor of this path: the apply kernel is bound by the
+    shared-memory pipe -- one 128-byte wavefront per SM per clock -- at D bucket bytes per
+    object-tree (a warp's 32 lanes x 4 objects read 128 bytes per depth) plus one random
+    gather per object-tree from a 2^D-leaf table; the quantize by HBM (4NF read + NF
+    written).  Single-output configs; the two phases are serial within a predict."""
+    N, F, T, D = spec.n_objects, spec.n_features, spec.n_trees, spec.depth
+    wf_per_ot = D / 128.0 + gather_wavefronts((1 << D) * leaf_bytes) / 32.0
+    t_apply = N * T * wf_per_ot / (n_sm * sm_hz)
+    t_quant = (4 * N * F + N * F) / (hbm_gbs * 1e9)
+    return {"t_apply_floor_ms": t_apply * 1e3, "t_quantize_floor_ms": t_quant * 1e3,
+            "wavefronts_per_object_tree": wf_per_ot,
+            "model": "apply: shared-memory wavefronts (1 per SM per clock); quantize: HBM bytes"}
+
+
 def flat_model(model):
     """The oracle's flat layout for an ObliviousModel or a multiclass.MultiOutputModel."""
     import numpy as np
@@ -489,6 +522,11 @@ def run_ours(args, world, rank, local):
                     "apply_ms": a_ms},
         "clocks": clk,
     }
+    if not multi:
+        rs = roofline_smem(spec, n_sm, pk["sm_max_mhz"] * 1e6, pk["hbm_gbs"], 2 if spec.half_leaves else 4)
+        t_floor = (rs["t_apply_floor_ms"] + rs["t_quantize_floor_ms"]) / 1e3
+        line["roofline_smem"] = {**rs, "t_floor_ms": t_floor * 1e3, "t_step_ms": step_s * 1e3, "frac": t_floor / step_s,
+                                 "apply_frac": rs["t_apply_floor_ms"] / a_ms}
     if multi:
         line["config"]["outputs"] = spec.n_outputs
         line["config"]["parallelism"] = (f"trees sharded over {world} GPU(s); NCCL all_reduce of fp64 partials "
