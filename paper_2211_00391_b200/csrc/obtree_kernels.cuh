@@ -815,6 +815,20 @@ __device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) {
   return (a & b) | (a & c) | (b & c);
 }
 
+#ifndef OBT_FADD2
+#define OBT_FADD2 1  // binary16 family: fold two objects per packed FADD2
+#endif
+// a += x, b += y as one packed f32x2 add (sm_100)
+__device__ __forceinline__ void fadd2(float& a, float& b, float x, float y) {
+  unsigned long long r, p, q;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(p) : "f"(a), "f"(b));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(q) : "f"(x), "f"(y));
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(p), "l"(q));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+template <typename T>
+__device__ __forceinline__ void fadd2(T&, T&, T, T) {}  // other accumulator types never reach it
+
 // Byte k (runtime-unrolled constant) of a packed index word, zero-extended.
 __device__ __forceinline__ uint32_t byte_of_rt(uint32_t w, int k) { return (w >> (8 * k)) & 0xffu; }
 
@@ -1124,7 +1138,16 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid
           if (it >= kPF + kLag && it - kPF - kLag < kTreeGroup) {  // stage C: fold tree tf (tree order per object)
             const int tf = it - kPF - kLag;
 #pragma unroll
-            for (int k = 0; k < 4 * W; ++k) acc[k] += LT::widen(gbuf[tf % (kLag + 1)][k]);
+            for (int k = 0; k < 4 * W; k += 2) {
+              if constexpr (LEAF == 2 && OBT_FADD2) {
+                // binary32 fold of two objects in one packed FADD2 (two independent
+                // round-to-nearest adds: the same bits as two FADDs)
+                fadd2(acc[k], acc[k + 1], LT::widen(gbuf[tf % (kLag + 1)][k]), LT::widen(gbuf[tf % (kLag + 1)][k + 1]));
+              } else {
+                acc[k] += LT::widen(gbuf[tf % (kLag + 1)][k]);
+                acc[k + 1] += LT::widen(gbuf[tf % (kLag + 1)][k + 1]);
+              }
+            }
           }
         }
       }
