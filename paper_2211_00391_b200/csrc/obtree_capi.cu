@@ -750,7 +750,11 @@ int launch_quantize(const obt_model* m, const float* x, int64_t n, int layout, u
   if (tiled && layout == OBT_LAYOUT_OBJECT_MAJOR && F % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
       tfn && encode_tiled() && quantize_tma_enabled()) {
     // two CTAs per SM: each gets half the SM's shared memory less the per-CTA reserve
-    const size_t half = (size_t)(m->smem_optin + 1024) / 2 - 1024;
+    // two CTAs per SM: each gets half the SM's shared memory (OBT_QUANT_ONE_CTA=1: one CTA
+    // per SM with every feature of its rows, so no L2 line is shared between CTAs)
+    const char* oc = getenv("OBT_QUANT_ONE_CTA");
+    const size_t half = (oc && !strcmp(oc, "1")) ? (size_t)m->smem_optin - 1024
+                                                 : (size_t)(m->smem_optin + 1024) / 2 - 1024;
     const size_t lut_fixed = use_lut ? 256 + 32 : 0;  // 256-byte alignment of the tables
     const int fc = use_lut ? quantize_chunk_bytes(m, (size_t)lt.cells + lt.rec_stride, n_slots,
                                                   half - obt::kQTSmemFixed - lut_fixed)
