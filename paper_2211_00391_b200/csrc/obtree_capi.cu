@@ -866,6 +866,8 @@ int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, int tpw, d
   p.tile_flags = flags;
   const char* to = getenv("OBT_TILE_ORDER");
   const bool alternate = !chain && !(to && !strcmp(to, "fwd"));  // chained launches keep one order
+  const char* co = getenv("OBT_CHAIN_ORDER");  // "fwd": chained launches first-to-last
+  const bool chain_rev = !(co && !strcmp(co, "fwd"));
   const char* ln = getenv("OBT_L2_NEXT");
   p.l2_wave = 0;
   if (ln && !strcmp(ln, "1")) {
@@ -878,7 +880,9 @@ int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, int tpw, d
     p.chunk_end = std::min(m->n_chunks, (l + 1) * per);
     p.first = l == 0;
     p.last = l == n_launch - 1;
-    p.reverse = alternate && (l % 2 == 0) ? 1 : 0;
+    // chained launches share one order; last-to-first by default, so the first launch's
+    // first waves read the tiles the quantize wrote last (still in L2)
+    p.reverse = chain ? (chain_rev ? 1 : 0) : (alternate && (l % 2 == 0) ? 1 : 0);
     p.flag_wait = chain ? l : 0;
     p.flag_set = chain && l < n_launch - 1 ? l + 1 : 0;
     if (dsrc) {
