@@ -237,6 +237,9 @@ __device__ __forceinline__ uint32_t eytz_level(uint32_t o, float x, const float*
   return add_if_greater(o * two + four, x, b, four);
 }
 
+#ifndef OBT_BUCKETS_EVICT_LAST
+#define OBT_BUCKETS_EVICT_LAST 0  // bucket-tile stores with an L2 evict-last policy (experiment)
+#endif
 // Store the packed buckets of one feature for a lane's 4 objects (base + lane + 32k):
 // tiled -> word `lane` of the 128-object block's row, plain -> 4 bytes of row f.
 template <bool TILED>
@@ -254,7 +257,14 @@ __device__ __forceinline__ void store_bucket_word(const QuantizeParams& p, uint3
     const int64_t tl = second ? p.tile2 : p.tile;
     const bool sw = (second ? p.swizzle2 : p.swizzle) && (f & 1);
     const int64_t t = rb / tl, w = (rb - t * tl + 4 * lane) ^ (sw ? 64 : 0);
-    *reinterpret_cast<uint32_t*>((second ? p.out2 : p.out) + (t * p.n_features + f) * tl + w) = word;
+    uint32_t* dst = reinterpret_cast<uint32_t*>((second ? p.out2 : p.out) + (t * p.n_features + f) * tl + w);
+    if constexpr (OBT_BUCKETS_EVICT_LAST) {
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+      asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(dst), "r"(word), "l"(pol) : "memory");
+    } else {
+      *dst = word;
+    }
   } else {
 #pragma unroll
     for (int k = 0; k < 4; ++k)
