@@ -93,6 +93,8 @@ constexpr int kLutMaxCompares = 4;
 struct TilePlan {
   uint8_t* d_chunks = nullptr;          // [n_chunks][chunk_bytes] descriptor + leaf records
   std::vector<uint32_t> param_desc;     // [padded_trees][DI][2] {off, k replicated} for the parameter bank
+  uint8_t* d_tables = nullptr;          // [n_chunks][tables_chunk_bytes] leaf tables only (parameter-bank launches)
+  uint32_t tables_chunk_bytes = 0;
 };
 
 }  // namespace
@@ -129,7 +131,10 @@ struct obt_model {
   std::map<int, TilePlan> plans;
   obt::ApplyArgs<1> param_args;  // launch-parameter staging (32 KB), guarded by mu
   ~obt_model() {
-    for (auto& kv : plans) cudaFree(kv.second.d_chunks);
+    for (auto& kv : plans) {
+      cudaFree(kv.second.d_chunks);
+      if (kv.second.d_tables) cudaFree(kv.second.d_tables);
+    }
     if (full.d) cudaFree(full.d);
     if (d_multi_leaves) cudaFree(d_multi_leaves);
     if (d_multi_desc) cudaFree(d_multi_desc);
@@ -484,6 +489,10 @@ int build_tile_plan(obt_model* m, int tile, int variant, TilePlan& out) {
   const int ct = m->chunk_trees;
   const size_t desc_bytes = m->desc_bytes, chunk_bytes = m->chunk_bytes;
   std::vector<uint8_t> host((size_t)std::max(m->n_chunks, 1) * chunk_bytes, 0);
+  // parameter-bank launches read descriptors from the launch parameters: their ring
+  // carries the leaf tables alone (27% fewer bytes per chunk at cfg2)
+  const uint32_t tcb = (uint32_t)((stride * ct + 255) & ~(size_t)255);
+  std::vector<uint8_t> host_tables(variant == 0 ? (size_t)std::max(m->n_chunks, 1) * tcb : 0, 0);
   out.param_desc.assign((size_t)m->padded_trees * DI * 2, 0u);
   std::vector<uint32_t> words((size_t)DI * 2);
   std::vector<int> perm(DI), wild(DI);
@@ -541,9 +550,15 @@ int build_tile_plan(obt_model* m, int tile, int variant, TilePlan& out) {
     } else {
       write_null_leaves(m, leaf_dst);
     }
+    if (!host_tables.empty()) std::memcpy(host_tables.data() + (size_t)c * tcb + (size_t)tl * stride, leaf_dst, stride);
   }
   CUDA_TRY(cudaMalloc(&out.d_chunks, host.size()));
   CUDA_TRY(cudaMemcpy(out.d_chunks, host.data(), host.size(), cudaMemcpyHostToDevice));
+  if (!host_tables.empty()) {
+    CUDA_TRY(cudaMalloc(&out.d_tables, host_tables.size()));
+    CUDA_TRY(cudaMemcpy(out.d_tables, host_tables.data(), host_tables.size(), cudaMemcpyHostToDevice));
+    out.tables_chunk_bytes = tcb;
+  }
   return OBT_OK;
 }
 
@@ -823,21 +838,24 @@ int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, int tpw, d
                           : pick_apply(m->depth_inst, m->compare_mode, m->leaf_storage, write_idx, dsrc);
   if (!k.fn) return fail(OBT_E_UNSUPPORTED, "no apply kernel for depth %d", m->depth_inst);
   const int64_t n_tiles = (n + tile - 1) / tile;
-  const size_t smem = 512 + (size_t)kStages * m->chunk_bytes + (size_t)m->n_features * tile;
+  const char* te = getenv("OBT_PARAM_TABLES");  // A/B knob: 0 = parameter launches stream full records
+  const bool tables_only = dsrc && tp->d_tables && !(te && !strcmp(te, "0"));
+  const uint32_t ring_chunk = tables_only ? tp->tables_chunk_bytes : m->chunk_bytes;
+  const size_t smem = 512 + (size_t)kStages * ring_chunk + (size_t)m->n_features * tile;
   if (smem > (size_t)m->smem_optin)
     return fail(OBT_E_UNSUPPORTED, "tile of %d objects needs %zu bytes of shared memory", tile, smem);
   CUDA_TRY(cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, m->smem_optin));
 
   obt::ApplyParams p{};
   p.q = q;
-  p.chunks = tp->d_chunks;
+  p.chunks = tables_only ? tp->d_tables : tp->d_chunks;
   p.out = out;
   p.idx_out = idx_out;
   p.n = n;
   p.tile = tile;
   p.chunk_trees = m->chunk_trees;
-  p.chunk_bytes = m->chunk_bytes;
-  p.desc_bytes = m->desc_bytes;
+  p.chunk_bytes = ring_chunk;
+  p.desc_bytes = tables_only ? 0u : m->desc_bytes;
   p.q_tile_bytes = (uint32_t)((size_t)m->n_features * tile);
   p.n_stages = kStages;
   p.tree_begin = tree_begin;
