@@ -841,7 +841,15 @@ int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, int tpw, d
   const char* te = getenv("OBT_PARAM_TABLES");  // A/B knob: 0 = parameter launches stream full records
   const bool tables_only = dsrc && tp->d_tables && !(te && !strcmp(te, "0"));
   const uint32_t ring_chunk = tables_only ? tp->tables_chunk_bytes : m->chunk_bytes;
-  const size_t smem = 512 + (size_t)kStages * ring_chunk + (size_t)m->n_features * tile;
+  // the smaller tables-only chunks may leave room for more ring stages (OBT_PARAM_STAGES)
+  int stages = kStages;
+  if (tables_only) {
+    const char* ps = getenv("OBT_PARAM_STAGES");
+    const int want = ps ? std::max(2, std::min(8, atoi(ps))) : kStages;
+    while (stages < want && 512 + (size_t)(stages + 1) * ring_chunk + (size_t)m->n_features * tile <= (size_t)m->smem_optin)
+      ++stages;
+  }
+  const size_t smem = 512 + (size_t)stages * ring_chunk + (size_t)m->n_features * tile;
   if (smem > (size_t)m->smem_optin)
     return fail(OBT_E_UNSUPPORTED, "tile of %d objects needs %zu bytes of shared memory", tile, smem);
   CUDA_TRY(cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, m->smem_optin));
@@ -857,7 +865,7 @@ int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, int tpw, d
   p.chunk_bytes = ring_chunk;
   p.desc_bytes = tables_only ? 0u : m->desc_bytes;
   p.q_tile_bytes = (uint32_t)((size_t)m->n_features * tile);
-  p.n_stages = kStages;
+  p.n_stages = stages;
   p.tree_begin = tree_begin;
   p.tree_end = tree_end;
   p.scale = m->scale;
