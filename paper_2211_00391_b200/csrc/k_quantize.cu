@@ -52,10 +52,20 @@ static QuantFn ldg_lut(int kmax) {
 
 QuantFn pick_quant_ldg_lut(int kmax, int cells, int layout) {
   if (cells == 1024) return layout == 0 ? ldg_lut<0, 1024>(kmax) : ldg_lut<1, 1024>(kmax);
+  if (cells == 512) return layout == 0 ? ldg_lut<0, 512>(kmax) : ldg_lut<1, 512>(kmax);
   return layout == 0 ? ldg_lut<0, 256>(kmax) : ldg_lut<1, 256>(kmax);
 }
 
 QuantTmaFn pick_quant_lut(int kmax, int cells) {
+  if (cells == 512) {
+    switch (kmax) {
+      case 1: return quantize_lut_kernel<1, 512>;
+      case 2: return quantize_lut_kernel<2, 512>;
+      case 3: return quantize_lut_kernel<3, 512>;
+      case 4: return quantize_lut_kernel<4, 512>;
+      default: return nullptr;
+    }
+  }
   if (cells == 1024) {
     switch (kmax) {
       case 1: return quantize_lut_kernel<1, 1024>;

@@ -301,19 +301,20 @@ int build_lut_table(const float* borders, const int32_t* counts, int F, int stri
   out.kmax = 0;
   out.cells = 256;
   int k = plan_lut_table(borders, counts, F, stride, 256, lut, rec, rs);
-  const char* e = getenv("OBT_LUT_CELLS");  // tuning override: 256 or 1024
-  const bool force1024 = e && !strcmp(e, "1024"), force256 = e && !strcmp(e, "256");
-  if ((k != 1 && !force256) || force1024) {
+  const char* e = getenv("OBT_LUT_CELLS");  // tuning override: 256, 512 or 1024
+  const int forced = e ? atoi(e) : 0;
+  const int big = (forced == 512 || forced == 1024) ? forced : 1024;
+  if ((k != 1 && forced != 256) || forced == 512 || forced == 1024) {
     std::vector<uint8_t> lut2;
     std::vector<unsigned char> rec2;
     int rs2 = 0;
-    const int k2 = plan_lut_table(borders, counts, F, stride, 1024, lut2, rec2, rs2);
-    if (k2 > 0 && (force1024 || (k2 <= 2 && (k == 0 || k2 < k)))) {
+    const int k2 = plan_lut_table(borders, counts, F, stride, big, lut2, rec2, rs2);
+    if (k2 > 0 && (forced == big || (k2 <= 2 && (k == 0 || k2 < k)))) {
       lut.swap(lut2);
       rec.swap(rec2);
       rs = rs2;
       k = k2;
-      out.cells = 1024;
+      out.cells = big;
     }
   }
   if (k <= 0) return OBT_OK;
@@ -717,7 +718,7 @@ bool lut_preferred(const obt_model* m) {
   if (e && !strcmp(e, "1")) return true;
   // 1024-cell tables (1 KB per feature) pay off only against deep searches: cfg4 (7
   // levels) 4.49 vs 4.95 ms, cfg5 (6 levels) 17.1 vs 16.5 ms
-  if (m->used_lut.cells == 1024 && m->used.levels < 7) return false;
+  if (m->used_lut.cells > 256 && m->used.levels < 7) return false;
   return 1 + m->used_lut.kmax < m->used.levels - 2;
 }
 
