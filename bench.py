@@ -1,22 +1,31 @@
 #!/usr/bin/env python
 """Benchmark: object-trees/s of oblivious-ensemble predict on B200, with roofline.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
 
-One "step" is one predict over one batch of the workload (BASELINE.json configs[1]
-by default: 1,000,000 objects x 200 features, 64 borders, 2,000 depth-6 trees, fp32
-leaves).  Under torchrun each rank owns one GPU and its own batch of that size
-(object sharding, no data-path collective: weak scaling); NCCL carries only the
-barrier and the max-over-ranks of the device-timed region.
+One "step" is one predict over one batch of the workload.  The default workload is
+BASELINE.json configs[3] (config 4: 8,000,000 objects x 500 features, 128 borders,
+8,000 depth-8 trees, fp32 leaves) -- the largest configuration that runs on one GPU,
+"objects sharded over 1/2/4/8 GPUs": at N GPUs each rank owns 8M/N of the objects
+(strong scaling, no data-path collective).  Configs 1-3 default to weak scaling (every
+rank its own batch of the configuration's size); config 5 shards trees (NCCL
+all_reduce of binary64 partials + finalize inside every step), or objects / a 2-D grid
+with --shard.  `--gpus N` without torchrun re-launches itself under
+torch.distributed.run with N ranks (127.0.0.1 rendezvous).
 
 Printed on rank 0 as ONE JSON line:
   value      whole-job object-trees/s, features resident in HBM, CUDA-event timed
+  verify     the timed batch's outputs (a strided sample of ~64k rows from every rank,
+             first and last tiles included) against the CPU oracle: bit-exact flag
   e2e        the same metric through Evaluator.predict with pinned host buffers
-             (host->device features and device->host scores inside the timed region)
+             (host->device features and device->host scores inside the timed region);
+             e2e_pageable: the literal drop-in call (numpy input, fresh output)
   roofline   the dominant kernel (tree apply) against the integer-issue peak, plus the
-             whole-step roofline of BASELINE.md section 6
-  cpu_baseline  the C oracle port of the reference algorithm on this host's cores
-`--impl reference` times that CPU port alone on the same config and metric.
+             whole-step roofline of SURVEY.md section 8d
+  cpu_baseline  the C oracle port of the reference algorithm on this host's cores, and
+             (reference_pkg) the reference package itself, 1 core and all cores
+  fp16_vs_fp32  (config 3) deviation metrics / flips of the fp16-leaf predictions
+`--impl reference` times the CPU port alone on the same config and metric.
 """
 
 from __future__ import annotations
@@ -200,6 +209,33 @@ def roofline_smem(spec, n_sm: int, sm_hz: float, hbm_gbs: float, leaf_bytes: int
             "model": "apply: shared-memory wavefronts (1 per SM per clock); quantize: HBM bytes"}
 
 
+def reduce_over_ranks(values, world: int, op: str):
+    """Element-wise MAX / MIN / SUM of a list of floats over ranks."""
+    if world == 1:
+        return list(values)
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor(list(values), dtype=torch.float64, device=reduce_device())
+    dist.all_reduce(t, op={"max": dist.ReduceOp.MAX, "min": dist.ReduceOp.MIN, "sum": dist.ReduceOp.SUM}[op])
+    return [float(v) for v in t.cpu()]
+
+
+def free_port() -> int:
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(argv, n: int) -> int:
+    """`--gpus N` outside torchrun: re-launch this script as N ranks on this node."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", str(Path(__file__).resolve()), *argv]
+    return subprocess.call(cmd)
+
+
 def flat_model(model):
     """The oracle's flat layout for an ObliviousModel or a multiclass.MultiOutputModel."""
     import numpy as np
@@ -216,82 +252,189 @@ def flat_model(model):
                             model.split_ordinal, model.leaves, model.scale, model.bias)
 
 
-def cpu_baseline(spec, model, seconds: float, verify_fn=None) -> dict:
-    """The C oracle port of the reference algorithm on this host's cores, on a bounded
-    prefix sample of the same workload (doubling until the run takes >= `seconds`/4)."""
+def sample_rows(n: int, target: int, edge: int = 1024):
+    """Deterministic rows of an n-object batch: the first and last `edge` rows (first and
+    last tiles) and every k-th row, about `target` in all, sorted and unique."""
     import numpy as np
 
-    import oracle
-    from paper_2211_00391_b200 import synthetic
+    if n <= target:
+        return np.arange(n, dtype=np.int64)
+    step = max(1, n // max(1, target - 2 * edge))
+    rows = np.concatenate([np.arange(min(edge, n)), np.arange(max(0, n - edge), n), np.arange(0, n, step)])
+    return np.unique(rows.astype(np.int64))
 
-    fm = flat_model(model)
+
+def verify_timed(x, out, fm, precision: int, rows, exact: bool) -> dict:
+    """The timed batch's outputs on `rows` against the CPU oracle on the same feature rows."""
+    import numpy as np
+    import torch
+
+    import oracle
+
+    idx = torch.from_numpy(rows).to(x.device)
+    xs = x.index_select(0, idx).cpu().numpy()
+    got = out.index_select(0, idx).cpu().numpy()
+    oracle.set_threads(oracle.host_cores())
+    want = oracle.evaluate_scalar(fm, xs, oracle.OBJECT_MAJOR, precision)
+    want = want.reshape(got.shape)
+    rel = np.abs(got - want) / np.maximum(np.maximum(np.abs(got), np.abs(want)), 1e-300)
+    rel = np.where(got == want, 0.0, rel)
+    return {"rows": int(rows.size), "bit_exact": bool(np.array_equal(got, want)),
+            "max_rel_dev": float(np.nanmax(rel)) if rel.size else 0.0, "expect_bit_exact": exact}
+
+
+def cpu_baseline_port(spec, fm, x, trees: int, seconds: float) -> dict:
+    """The C oracle port of the reference algorithm on all host cores, on a prefix of the
+    timed batch's rows (doubling until one pass takes >= seconds/4)."""
+    import oracle
+
     oracle.set_threads(oracle.host_cores())  # all host cores, whatever OMP_NUM_THREADS says
-    threads = oracle.max_threads()
-    n = 4096
-    best = None
+    prec = oracle.BINARY16 if spec.half_leaves else oracle.BINARY64
+    n_max = x.shape[0]
+    n = min(4096, n_max)
     while True:
-        x = synthetic.host_features(spec, n_objects=n, seed=spec.data_seed + 7)
+        xs = x[:n].cpu().numpy()
         t0 = time.perf_counter()
-        ref = oracle.evaluate_scalar(fm, x, oracle.OBJECT_MAJOR,
-                                     oracle.BINARY16 if spec.half_leaves else oracle.BINARY64)
+        oracle.evaluate_scalar(fm, xs, oracle.OBJECT_MAJOR, prec)
         dt = time.perf_counter() - t0
-        best = (n, dt, x, ref)
-        if dt >= seconds / 4 or n >= spec.n_objects or n >= 1 << 22:
+        if dt >= seconds / 4 or n >= n_max or n >= 1 << 22:
             break
-        n *= 2
-    n, dt, x, ref = best
+        n = min(n_max, 2 * n)
     reps = max(1, int(round(seconds * 0.75 / max(dt, 1e-6))))
     t0 = time.perf_counter()
     for _ in range(reps):
-        oracle.evaluate_scalar(fm, x, oracle.OBJECT_MAJOR, oracle.BINARY16 if spec.half_leaves else oracle.BINARY64)
+        oracle.evaluate_scalar(fm, xs, oracle.OBJECT_MAJOR, prec)
     dt = (time.perf_counter() - t0) / reps
-    out = {
-        "value": n * spec.n_trees / dt,
-        "unit": UNIT,
-        "cores": threads,
-        "host_cpus": os.cpu_count(),
+    return {
+        "value": n * trees / dt, "unit": UNIT, "cores": oracle.max_threads(), "host_cpus": os.cpu_count(),
         "kind": "port",
-        "sample": f"first {n} objects of the workload (full {spec.n_trees}-tree model), {reps} reps, "
+        "sample": f"the first {n} of the timed batch's {n_max} objects (full {trees}-tree model), {reps} reps; "
                   f"C restatement of evaluate_scalar (oracle/obtree_oracle.c), OpenMP over objects",
     }
-    if verify_fn is not None:
-        got = verify_fn(x)
-        out["gpu_verified_bit_exact"] = bool(np.array_equal(got, ref))
-        rel = np.abs(got - ref) / np.maximum(np.maximum(np.abs(got), np.abs(ref)), 1e-300)
-        out["gpu_max_rel_dev"] = float(rel.max()) if rel.size else 0.0
-    return out
 
 
-def load_ncu_mio(cfg: int):
-    """The dominant kernel's shared-memory wavefront rate as a fraction of peak (ncu), the
-    resource that binds this path on B200."""
-    path = ROOT / "profiles" / "ncu_apply_summary.json"
-    if not path.exists():
-        return None
+REF_PKG = ROOT / "baseline" / "_ref"
+
+
+def reference_model(model):
+    """The reference package's ObliviousModel for one of ours (same values)."""
+    import numpy as np
+
+    import obtree
+
+    ff = tuple(obtree.FloatFeatureBorders(f.feature_index, np.asarray(f.borders, np.float32))
+               for f in model.float_features)
+    trees = tuple(obtree.ObliviousTree(t.depth, tuple(obtree.SplitCondition(s.feature_index, s.border_ordinal)
+                                                      for s in t.splits), np.asarray(t.leaf_values))
+                  for t in model.trees)
+    return obtree.ObliviousModel(ff, trees, model.scale, model.bias)
+
+
+def refpkg_worker(path: str, core: int, offset: int, n: int, half: bool) -> None:
+    """One pinned process timing the reference package's Evaluator (its own _time_case)."""
+    import numpy as np
+
+    os.sched_setaffinity(0, {core})
+    sys.path.insert(0, str(REF_PKG))
+    import obtree
+    from obtree.bench import _time_case
+
+    from paper_2211_00391_b200 import synthetic
+
+    data = np.load(path, allow_pickle=False)
+    spec = synthetic.WorkloadSpec(**json.loads(str(data["spec"])))
+    model = reference_model(synthetic.build_model(spec))
+    x = np.ascontiguousarray(data["x"][offset: offset + n])
+    cfg = (obtree.EvalConfig(block_size=512, strategy=obtree.LeafStrategy.NAIVE16) if half else obtree.EvalConfig())
+    ev = obtree.Evaluator(model, cfg)
+    fm = obtree.FeatureMatrix(x, obtree.Layout.OBJECT_MAJOR)
+    ev.predict(fm)  # warm-up (the reference bench's verification run)
+    mean, std, inner = _time_case(ev, fm, 3)
+    print(json.dumps({"seconds": mean, "std": std, "inner": inner, "n": int(x.shape[0]), "core": core}), flush=True)
+
+
+def reference_pkg_baseline(spec, x, budget_s: float) -> dict:
+    """The reference package itself (pure Python + numpy, installed into baseline/_ref by
+    pip from /root/reference/pkg) on this host: 1 core, then one pinned process per core
+    each on its own slice of the timed batch (the reference is single-threaded by
+    contract), timed by the reference's own bench._time_case
+    (process_time, doubling inner loop, 3 repetitions)."""
+    import tempfile
+
+    import numpy as np
+
+    if not (REF_PKG / "obtree").exists():
+        return {"unavailable": "baseline/_ref/obtree not installed (pip install --target baseline/_ref)"}
+    if spec.n_outputs > 1 or spec.depth > 8:
+        return {"unavailable": "the reference stops at depth 8 and one output (model.py:22, SPEC.md:15)"}
+    cores = sorted(os.sched_getaffinity(0))
+    # ~35 us per object per 1000 depth-8 trees on one core (measured here): ~0.6 s slices
+    per_obj = 3.5e-5 * spec.n_trees / 1000.0
+    n = int(max(64, min(4096, 0.6 / per_obj)))
+    n_all = min(x.shape[0], n * len(cores))
+    xs = x[:n_all].cpu().numpy()
+    fd, path = tempfile.mkstemp(suffix=".npz")
+    os.close(fd)
+    fields = {k: getattr(spec, k) for k in spec.__dataclass_fields__}
+    np.savez(path, x=xs, spec=np.array(json.dumps(fields)))
+    env = {**os.environ, "OMP_NUM_THREADS": "1", "OPENBLAS_NUM_THREADS": "1", "MKL_NUM_THREADS": "1"}
+
+    def launch(core, offset):
+        return subprocess.Popen([sys.executable, str(Path(__file__).resolve()), "--refpkg-worker", path, str(core),
+                                 str(offset), str(n), "1" if spec.half_leaves else "0"],
+                                stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True, env=env)
+
+    def collect(procs):
+        res = []
+        for p in procs:
+            try:
+                o, e = p.communicate(timeout=budget_s)
+            except subprocess.TimeoutExpired:
+                p.kill()
+                continue
+            if p.returncode == 0 and o.strip():
+                res.append(json.loads(o.strip().splitlines()[-1]))
+        return res
+
     try:
-        v = json.loads(path.read_text()).get(f"cfg{cfg}", {}).get("smem_wavefront_pct_of_peak")
-        return None if v is None else v / 100.0
-    except Exception:
-        return None
+        one = collect([launch(cores[0], 0)])
+        if not one:
+            return {"unavailable": "reference worker failed"}
+        slots = [c for c in cores if (cores.index(c) + 1) * n <= n_all]
+        allr = collect([launch(c, i * n) for i, c in enumerate(slots)])
+    finally:
+        os.unlink(path)
+    v1 = one[0]["n"] * spec.n_trees / one[0]["seconds"]
+    vall = sum(r["n"] * spec.n_trees / r["seconds"] for r in allr)
+    cfg = "EvalConfig(block_size=512, strategy=NAIVE16)" if spec.half_leaves else "EvalConfig() (block 128, W512, NAIVE)"
+    return {"value_1core": v1, "value_all_cores": vall, "unit": UNIT, "cores": len(allr), "kind": "reference",
+            "impl": "obtree 0.1.0 Evaluator.predict (the reference package, pure Python + numpy) with " + cfg,
+            "timer": "obtree.bench._time_case (process CPU time, per pinned process)",
+            "sample": f"{n} objects of the timed batch per process (disjoint slices), full {spec.n_trees}-tree model"}
 
 
-def load_ncu_traffic(cfg: int):
-    path = ROOT / "profiles" / "ncu_apply_summary.json"
-    if not path.exists():
-        return None
-    try:
-        data = json.loads(path.read_text())
-        return data.get(f"cfg{cfg}", {}).get("dram_bytes_per_launch")
-    except Exception:
-        return None
+def fp16_report(model, x, p16, device: int) -> dict:
+    """Config 3: the fp16-leaf predictions of the timed batch against the fp32-leaf ones
+    (reference oracle.py:57-92 metrics, flips at threshold 0, and the reference's bound
+    |scale| * T * max|leaf| * 2^-10 of test_acceptance.py:156)."""
+    import paper_2211_00391_b200 as obt
+
+    ev32 = obt.Evaluator(model, obt.EvalConfig(strategy=obt.LeafStrategy.NAIVE), device=device)
+    p32 = ev32.predict_device(x).cpu().numpy()
+    p16 = p16.cpu().numpy()
+    m = obt.deviation_metrics(p32, p16)
+    bank = obt.build_leaf_bank(model, obt.LeafPrecision.BINARY16)
+    bound = abs(model.scale) * model.n_trees * bank.max_abs_leaf * 2.0 ** -10
+    return {"vs": "fp32-leaf (binary64-fold) predictions of the same timed batch", "objects": int(p16.size),
+            "max_abs": m.max_abs, "mean_abs": m.mean_abs, "median_abs": m.median_abs, "rms": m.rms,
+            "flips_at_0": obt.classification_flip_count(p32, p16, 0.0), "bound": bound,
+            "within_bound": bool(m.max_abs <= bound), "saturated_leaves": bank.saturation_count}
 
 
 def run_reference(args, world, rank):
     """--impl reference: the CPU port of the reference algorithm, all host threads."""
     if rank != 0:
         return
-    import numpy as np  # noqa: F401
-
     import oracle
     from paper_2211_00391_b200 import synthetic
 
@@ -305,7 +448,7 @@ def run_reference(args, world, rank):
     fm = flat_model(model)
     oracle.set_threads(oracle.host_cores())  # torchrun exports OMP_NUM_THREADS=1; use every core
     prec = oracle.BINARY16 if spec.half_leaves else oracle.BINARY64
-    n = args.ref_sample
+    n = min(args.ref_sample, spec.n_objects)
     x = synthetic.host_features(spec, n_objects=n, seed=spec.data_seed + 7)
     for _ in range(args.warmup):
         oracle.evaluate_scalar(fm, x, oracle.OBJECT_MAJOR, prec)
@@ -319,25 +462,79 @@ def run_reference(args, world, rank):
     line = {
         "impl": "reference",
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True,
+        "scaling": "weak" if args.config in (1, 2, 3) else "strong",
         "vs_baseline": None, "dtype": "f16/f32" if spec.half_leaves else "f64", "data": "synthetic",
         "config": {"workload": spec.name, "n_objects_per_step": n, "features": spec.n_features,
                    "borders": spec.borders, "trees": spec.n_trees, "depth": spec.depth},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.max_threads(), "host_cpus": os.cpu_count(),
                          "kind": "port",
-                         "sample": f"{n} objects per step of {spec.name}; the reference is pure Python/numpy and "
-                                   f"cannot travel, so its algorithm runs as the C oracle port"},
+                         "sample": f"{n} objects per step drawn with the workload's generator ({spec.name}); the C "
+                                   f"restatement of the reference algorithm (oracle/obtree_oracle.c), OpenMP over "
+                                   f"objects -- faster per core than the reference package (bench.py's "
+                                   f"cpu_baseline.reference_pkg times that one too)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+class Plan:
+    """What this rank evaluates: objects (n, data seed) and trees (model), and how the
+    step completes (a reduce group for tree / grid sharding)."""
+
+    def __init__(self, args, spec, world, rank):
+        from paper_2211_00391_b200 import sharding
+
+        self.multi = spec.n_outputs > 1
+        self.shard = args.shard or ("trees" if self.multi and world > 1 else "objects")
+        if self.shard == "objects" and not self.multi and args.config in (1, 2, 3) and args.scaling != "strong":
+            self.scaling = "weak"
+        elif self.shard == "objects" and args.scaling == "weak":
+            self.scaling = "weak"
+        else:
+            self.scaling = "strong"
+        go, gt = 1, 1
+        if self.shard == "objects":
+            go = world
+        elif self.shard == "trees":
+            gt = world
+        else:
+            go, gt = (int(v) for v in args.grid.split("x"))
+            if go * gt != world:
+                raise SystemExit(f"--grid {args.grid} needs {go * gt} ranks, got {world}")
+        self.grid = (go, gt)
+        self.object_index, self.tree_index = divmod(rank, gt)
+        if self.scaling == "weak":
+            self.n = spec.n_objects
+            self.total_objects = spec.n_objects * go
+        else:
+            b, e = sharding.balanced_ranges(spec.n_objects, go, quantum=256)[self.object_index]
+            self.n = e - b
+            self.total_objects = spec.n_objects
+        self.tree_range = sharding.tree_shard(spec.n_trees, self.tree_index, gt)
+        # ranks of one object shard see the same rows; different shards different rows
+        self.data_seed = spec.data_seed + 1000 * self.object_index
+        self.reduce = gt > 1
+
+    def parallelism(self, world) -> str:
+        go, gt = self.grid
+        if self.shard == "objects":
+            how = "objects sharded" if self.scaling == "strong" else "one batch per GPU (weak)"
+            return f"{how} over {world} GPU(s), no data-path collective"
+        if self.shard == "trees":
+            return (f"trees sharded over {world} GPU(s); NCCL all_reduce of fp64 partials + finalize inside every "
+                    "timed step")
+        return (f"{go} object shards x {gt} tree shards; all_reduce of fp64 partials within each object shard + "
+                "finalize inside every timed step")
 
 
 def run_ours(args, world, rank, local):
     import numpy as np
     import torch
 
+    import oracle
     import paper_2211_00391_b200 as obt
-    from paper_2211_00391_b200 import _native, synthetic
+    from paper_2211_00391_b200 import _native, sharding, synthetic
 
     spec = synthetic.CONFIGS[args.config]
     if args.objects:
@@ -346,43 +543,42 @@ def run_ours(args, world, rank, local):
         spec = synthetic.WorkloadSpec(**{**spec.__dict__, "n_trees": args.trees})
     device = local
     torch.cuda.set_device(device)
-    multi = spec.n_outputs > 1
+    plan = Plan(args, spec, world, rank)
+    multi = plan.multi
+    tb, te = plan.tree_range
     if multi:
-        # config 5: tree-sharded across ranks (each rank folds its trees for all objects,
-        # partial sums reduced after the timed region); at N=1 the whole model
-        from paper_2211_00391_b200 import multiclass, sharding
+        from paper_2211_00391_b200 import multiclass
 
         full_model = multiclass.from_arrays(synthetic.model_arrays(spec))
-        tb, te = sharding.tree_shard(full_model.n_trees, rank, world)
-        model = full_model.subset(tb, te, raw=world > 1) if world > 1 else full_model
-        ev = multiclass.MultiOutputEvaluator(model, device=device)
+        config = None
     else:
-        model = synthetic.build_model(spec)
-        strategy = obt.LeafStrategy.NAIVE16 if spec.half_leaves else obt.LeafStrategy.NAIVE
-        ev = obt.Evaluator(model, obt.EvalConfig(strategy=strategy), device=device)
-    data_seed = spec.data_seed + (0 if multi else 1000 * rank)  # tree sharding: same objects on every rank
-    x = synthetic.device_features(spec, seed=data_seed, device=f"cuda:{device}")
-    N = spec.n_objects
+        full_model = synthetic.build_model(spec)
+        config = obt.EvalConfig(strategy=obt.LeafStrategy.NAIVE16 if spec.half_leaves else obt.LeafStrategy.NAIVE)
+    sharded, group = None, None
+    if plan.reduce:
+        # tree / grid sharding through the public sharded evaluator (its inner GPU
+        # evaluator holds this rank's tree shard with scale 1 / bias 0)
+        sharded = sharding.GridShardedEvaluator(full_model, *plan.grid, config=config, device=device)
+        ev, group = sharded.trees.local_evaluator, sharded.trees.group
+    elif multi:
+        ev = multiclass.MultiOutputEvaluator(full_model, device=device)
+    else:
+        ev = obt.Evaluator(full_model, config, device=device)
+    x = synthetic.device_features(spec, n_objects=plan.n, seed=plan.data_seed, device=f"cuda:{device}")
+    N = plan.n
     out = torch.empty((N, spec.n_outputs) if multi else N, dtype=torch.float64, device=x.device)
     ws = torch.empty(ev.workspace_bytes(N), dtype=torch.uint8, device=x.device)
 
-    tree_sharded = multi and world > 1
-
-    def reduce_partials():
-        # tree sharding: a prediction is complete only after the NCCL sum of the ranks'
-        # binary64 partial sums and the affine finalize, so both are part of every step
-        import torch.distributed as dist
-
-        red = out if reduce_device() == "cuda" else out.cpu()
-        dist.all_reduce(red, op=dist.ReduceOp.SUM)
-        if red is not out:
-            out.copy_(red)
-        out.mul_(full_model.scale).add_(full_model.bias)
+    def complete():
+        # tree / grid sharding: a prediction is complete only after the sum of the ranks'
+        # binary64 partials and the affine finalize, so both are part of every step
+        if plan.reduce:
+            sharding._all_reduce_sum(out, group)
+            sharding._finalize_(out, full_model.scale, full_model.bias)
 
     for _ in range(args.warmup):
         ev.predict_device(x, out=out, workspace=ws)
-        if tree_sharded:
-            reduce_partials()
+        complete()
     torch.cuda.synchronize()
 
     stream = _native.current_stream_handle(device)
@@ -395,7 +591,7 @@ def run_ours(args, world, rank, local):
     t_end.record(stream)
     torch.cuda.synchronize()
     one_ms = t_start.elapsed_ms(t_end)
-    use_graph = not tree_sharded and (args.graph == "on" or (args.graph == "auto" and one_ms < 0.2))
+    use_graph = not plan.reduce and (args.graph == "on" or (args.graph == "auto" and one_ms < 0.2))
     graph, graph_launches = None, 0
     if use_graph:
         gs = torch.cuda.Stream(device)
@@ -425,14 +621,34 @@ def run_ours(args, world, rank, local):
             continue
         ev.predict_device_marked(x, marks[k], out=out, workspace=ws)
         launches += ev.last_launch_count()
-        if tree_sharded:
-            reduce_partials()
+        complete()
     t_end.record(stream)
     torch.cuda.synchronize()
     w1 = time.perf_counter()
     barrier(world)
     clk = clocks.stop(w0, w1)
     elapsed_ms = max_over_ranks(t_start.elapsed_ms(t_end), world)
+    step_s = elapsed_ms / K / 1e3
+    value = plan.total_objects * spec.n_trees / step_s
+
+    # --- the timed batch's outputs against the oracle (out holds the last timed step)
+    fm_full = flat_model(full_model)
+    prec = oracle.BINARY16 if spec.half_leaves else oracle.BINARY64
+    rows = sample_rows(N, max(1024, args.verify_rows // (8 if multi else 1)))
+    ver = verify_timed(x, out, fm_full, prec, rows, exact=not plan.reduce)
+    red = reduce_over_ranks([ver["rows"]], world, "sum")
+    mx = reduce_over_ranks([ver["max_rel_dev"]], world, "max")[0]
+    mn = reduce_over_ranks([1.0 if ver["bit_exact"] else 0.0], world, "min")[0]
+    verify = {"rows": int(red[0]), "ranks": world, "bit_exact": bool(mn == 1.0), "max_rel_dev": mx,
+              "tolerance": 0.0 if not plan.reduce else 1e-12,
+              "passed": bool(mn == 1.0) if not plan.reduce else bool(mx <= 1e-12),
+              "rows_spec": "per rank: first and last 1024 rows + every k-th row of its timed batch",
+              "oracle": "oracle/obtree_oracle.c evaluate_scalar (full model)"}
+
+    fp16 = None
+    if spec.half_leaves and rank == 0 and not plan.reduce:
+        fp16 = fp16_report(full_model, x, out, device)
+
     if graph is not None:
         # per-kernel split from marked stream launches after the timed region
         for m in marks:
@@ -440,60 +656,87 @@ def run_ours(args, world, rank, local):
         torch.cuda.synchronize()
     q_ms = sum(m[0].elapsed_ms(m[1]) for m in marks) / len(marks)
     a_ms = sum(m[1].elapsed_ms(m[2]) for m in marks) / len(marks)
-    step_s = elapsed_ms / K / 1e3
-    # object sharding: every rank folds all trees for its own N objects; tree sharding
-    # (config 5): every rank folds its share of the trees for the same N objects
-    value = (N * spec.n_trees if multi else world * N * spec.n_trees) / step_s
     reduce_ms = None
-    if tree_sharded:
+    if plan.reduce:
         # the reduce alone, for the report (it is already inside every timed step above)
         torch.cuda.synchronize()
-        r0 = time.perf_counter()
-        reduce_partials()
+        t_start.record(stream)
+        complete()
+        t_end.record(stream)
         torch.cuda.synchronize()
-        reduce_ms = (time.perf_counter() - r0) * 1e3
+        reduce_ms = t_start.elapsed_ms(t_end)
 
-    # end to end through the public API: pinned host features -> scores in pinned host memory
-    e2e = None
-    if not args.no_e2e and not multi:
-        xh = torch.empty((N, spec.n_features), dtype=torch.float32, pin_memory=True)
-        xh.copy_(x)
-        oh = torch.empty(N, dtype=torch.float64, pin_memory=True)
+    # --- end to end through the public API: pinned host features -> scores in pinned host memory
+    e2e, e2e_pageable = None, None
+    if not args.no_e2e:
+        n_e = N if not multi else min(N, args.e2e_multi_objects)
+        xh = torch.empty((n_e, spec.n_features), dtype=torch.float32, pin_memory=True)
+        xh.copy_(x[:n_e])
+        oh = torch.empty((n_e, spec.n_outputs) if multi else n_e, dtype=torch.float64, pin_memory=True)
         fmx = obt.FeatureMatrix(xh.numpy(), obt.Layout.OBJECT_MAJOR)
         ohn = oh.numpy()
-        ev.predict(fmx, out=ohn)
+        predict_host = sharded.trees.predict if sharded is not None else (lambda m: ev.predict(m, out=ohn))
+        predict_host(fmx)
         ke = max(1, min(K, args.e2e_steps))
         barrier(world)
         t0 = time.perf_counter()
         for _ in range(ke):
-            ev.predict(fmx, out=ohn)
+            predict_host(fmx)
         dt = max_over_ranks(time.perf_counter() - t0, world) / ke
-        e2e = {"value": world * N * spec.n_trees / dt, "unit": UNIT, "ms_per_step": dt * 1e3,
-               "h2d_bytes_per_step": N * spec.n_features * 4, "d2h_bytes_per_step": N * 8,
-               "api": "Evaluator.predict(FeatureMatrix, out=pinned) -> obt_predict_host", "steps": ke}
+        objs = reduce_over_ranks([n_e], world, "sum")[0] / plan.grid[1]
+        e2e = {"value": objs * spec.n_trees / dt, "unit": UNIT, "ms_per_step": dt * 1e3,
+               "h2d_bytes_per_step": n_e * spec.n_features * 4, "d2h_bytes_per_step": n_e * 8 * spec.n_outputs,
+               "api": ("TreeShardedEvaluator.predict(FeatureMatrix(pinned numpy)): partials -> NCCL all_reduce -> "
+                       "finalize -> host" if sharded is not None else
+                       "Evaluator.predict(FeatureMatrix(pinned numpy), out=pinned) -> obt_predict_host"),
+               "steps": ke, "objects_per_rank": n_e}
+        if n_e < N:
+            e2e["sample"] = f"the first {n_e} objects of each rank's batch (host memory bound)"
         del xh, oh
+        if world == 1 and not multi and args.e2e_pageable_steps > 0:
+            # the literal drop-in call: pageable numpy input, a fresh float64 result
+            xp = x.cpu().numpy()
+            fmp = obt.FeatureMatrix(xp, obt.Layout.OBJECT_MAJOR)
+            ev.predict(fmp)
+            kp = args.e2e_pageable_steps
+            t0 = time.perf_counter()
+            for _ in range(kp):
+                ev.predict(fmp)
+            dt = (time.perf_counter() - t0) / kp
+            e2e_pageable = {"value": N * spec.n_trees / dt, "unit": UNIT, "ms_per_step": dt * 1e3,
+                            "h2d_bytes_per_step": N * spec.n_features * 4, "d2h_bytes_per_step": N * 8,
+                            "api": "Evaluator.predict(FeatureMatrix(numpy)) -> fresh ndarray (pageable memory)",
+                            "steps": kp}
+            del xp, fmp
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_port(spec, fm_full, x, spec.n_trees, args.cpu_seconds)
+        if not args.no_reference_pkg:
+            cpu["reference_pkg"] = reference_pkg_baseline(spec, x, args.cpu_seconds * 4)
 
     if rank != 0:
         return
     pk = peaks()
-    import ctypes
-
-    sms = ctypes.c_int()
     props = torch.cuda.get_device_properties(device)
     n_sm = props.multi_processor_count
     p_int = n_sm * 128 * pk["sm_max_mhz"] * 1e6  # lane-ops/s
-    terms = roofline_terms(spec)
+    local_spec = synthetic.WorkloadSpec(**{**spec.__dict__, "n_objects": N, "n_trees": te - tb})
+    terms = roofline_terms(local_spec)
     apply_achieved = terms["apply_ops"] / (a_ms / 1e3)
     t_roof = max(terms["bytes"] / (pk["hbm_gbs"] * 1e9), terms["ops"] / p_int)
+    t_rank = step_s if not plan.reduce else step_s - (reduce_ms or 0) / 1e3
     quant_gbs = terms["quantize_bytes"] / (q_ms / 1e3) / 1e9
+    traffic, traffic_src = load_ncu_traffic(args.config)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
-        "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": plan.scaling, "vs_baseline": None,
         "dtype": "f16/f32" if spec.half_leaves else "f64",
         "data": "synthetic (seeded; BASELINE names no dataset)",
-        "config": {"workload": spec.name, "n_objects_per_gpu": N, "features": spec.n_features,
-                   "borders": spec.borders, "trees": spec.n_trees, "depth": spec.depth,
+        "config": {"workload": spec.name, "n_objects_total": plan.total_objects, "n_objects_per_gpu": N,
+                   "features": spec.n_features, "borders": spec.borders, "trees": spec.n_trees,
+                   "trees_per_gpu": te - tb, "depth": spec.depth, "outputs": spec.n_outputs,
                    "leaves": "fp16 (binary32 fold)" if spec.half_leaves else "fp32 values (binary64 fold)",
                    "leaf_storage_on_device": ev.leaf_storage,
                    "quantize_search": quantize_search(ev, spec.n_features),
@@ -501,66 +744,98 @@ def run_ours(args, world, rank, local):
                    "l2": ("inputs larger than L2 (features 4NF bytes, buckets NF bytes > 126 MB)"
                           if 4 * N * spec.n_features > 126e6 else
                           "inputs L2-resident between steps (features 4NF bytes < 126 MB; a launch-bound size)"),
-                   "parallelism": f"objects sharded over {world} GPU(s), no data-path collective",
+                   "parallelism": plan.parallelism(world), "shard": plan.shard,
                    "launch": "CUDA graph replay of one predict" if graph is not None else "stream launches"},
+        "verify": verify,
         "e2e": e2e,
+        "e2e_pageable": e2e_pageable,
         "gpu_launches": launches,
         "roofline": {
-            "bound": "issue", "kernel": "apply_kernel (leaf index + gather + fold)",
+            "bound": "issue", "kernel": "tree apply (leaf index + gather + fold)",
             "achieved": apply_achieved / 1e12, "peak": p_int / 1e12, "unit": "Tlane-op/s",
-            "frac": apply_achieved / p_int, "traffic": load_ncu_traffic(args.config),
-            "binding_resource": {"what": "shared-memory wavefronts (one 128-byte wavefront per SM per clock)",
-                                 "frac_of_peak_ncu": load_ncu_mio(args.config)},
+            "frac": apply_achieved / p_int, "traffic": traffic, "traffic_source": traffic_src,
             "algorithmic_ops_per_launch": terms["apply_ops"], "ms_per_launch": a_ms,
-            "ops_definition": "N*T*D split compares + N*T*C leaf gathers (SURVEY.md 8d)",
+            "ops_definition": "N*T*D split compares + N*T*C leaf gathers (SURVEY.md 8d), per predict",
             "peak_source": f"{n_sm} SMs x 128 lanes x {pk['sm_max_mhz']:.0f} MHz",
         },
-        "roofline_step": {"t_roof_ms": t_roof * 1e3, "t_step_ms": step_s * 1e3, "frac": t_roof / step_s,
+        "roofline_step": {"t_roof_ms": t_roof * 1e3, "t_step_ms": t_rank * 1e3, "frac": t_roof / t_rank,
                           "bytes": terms["bytes"], "ops": terms["ops"], "hbm_gbs_peak": pk["hbm_gbs"],
-                          "peak_source": pk["source"]},
+                          "peak_source": pk["source"],
+                          "definition": "max(bytes / HBM, ops / integer issue peak) of SURVEY.md 8d over this GPU's "
+                                        "share; t_step excludes the collective"},
         "kernels": {"quantize_ms": q_ms, "quantize_GBps": quant_gbs, "quantize_frac_hbm": quant_gbs / pk["hbm_gbs"],
                     "apply_ms": a_ms},
         "clocks": clk,
     }
     if not multi:
-        rs = roofline_smem(spec, n_sm, pk["sm_max_mhz"] * 1e6, pk["hbm_gbs"], 2 if spec.half_leaves else 4)
+        rs = roofline_smem(local_spec, n_sm, pk["sm_max_mhz"] * 1e6, pk["hbm_gbs"], 2 if spec.half_leaves else 4)
         t_floor = (rs["t_apply_floor_ms"] + rs["t_quantize_floor_ms"]) / 1e3
-        line["roofline_smem"] = {**rs, "t_floor_ms": t_floor * 1e3, "t_step_ms": step_s * 1e3, "frac": t_floor / step_s,
-                                 "apply_frac": rs["t_apply_floor_ms"] / a_ms}
-    if multi:
-        line["config"]["outputs"] = spec.n_outputs
-        line["config"]["parallelism"] = (f"trees sharded over {world} GPU(s); NCCL all_reduce of fp64 partials "
-                                         "+ finalize inside every timed step")
-        line["scaling"] = "strong"
+        line["roofline_smem"] = {**rs, "t_floor_ms": t_floor * 1e3, "t_step_ms": t_rank * 1e3,
+                                 "frac": t_floor / t_rank, "apply_frac": rs["t_apply_floor_ms"] / a_ms,
+                                 "note": "a B200 shared-memory model of this design, secondary to roofline"}
+    if plan.reduce:
         line["nccl_reduce_ms"] = reduce_ms
-    if world == 1 and not args.no_cpu_baseline:
-        def verify(xs):
-            return ev.predict(obt.FeatureMatrix(xs, obt.Layout.OBJECT_MAJOR))
-
-        line["cpu_baseline"] = cpu_baseline(spec, model, args.cpu_seconds, verify)
+    if fp16 is not None:
+        line["fp16_vs_fp32"] = fp16
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
+
+
+def load_ncu_traffic(cfg: int):
+    """DRAM bytes per apply launch from the committed ncu capture (not measured in this
+    run; the source file is named next to the number)."""
+    path = ROOT / "profiles" / "ncu_apply_summary.json"
+    if not path.exists():
+        return None, None
+    try:
+        data = json.loads(path.read_text()).get(f"cfg{cfg}", {})
+        v = data.get("dram_bytes_per_launch")
+        return v, (f"static: {data.get('source', 'profiles/ncu_apply_summary.json')} (committed ncu --set full "
+                   "capture, not measured in this run)") if v is not None else None
+    except Exception:
+        return None, None
 
 
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
-    ap.add_argument("--objects", type=int, default=0, help="override objects per GPU")
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--objects", type=int, default=0, help="override the configuration's object count")
     ap.add_argument("--trees", type=int, default=0, help="override the tree count (experiments)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
+                    help="objects: strong = the configuration's batch split over the GPUs (config 4's default), "
+                         "weak = one batch of that size per GPU (configs 1-3 default)")
+    ap.add_argument("--shard", choices=["objects", "trees", "grid"], default=None,
+                    help="config 5: trees (default at N>1), objects, or a 2-D grid (--grid GoxGt)")
+    ap.add_argument("--grid", default="1x1")
+    ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-reference-pkg", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-pageable-steps", type=int, default=2)
+    ap.add_argument("--e2e-multi-objects", type=int, default=2_000_000)
+    ap.add_argument("--verify-rows", type=int, default=65536)
     ap.add_argument("--ref-sample", type=int, default=65536)
     ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
                     help="replay a CUDA graph of one predict (auto: when a step is under 0.2 ms)")
+    ap.add_argument("--refpkg-worker", nargs=5, help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.refpkg_worker:
+        path, core, offset, n, half = args.refpkg_worker
+        refpkg_worker(path, int(core), int(offset), int(n), half == "1")
+        return
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(sys.argv[1:], args.gpus))
     world, rank, local = dist_setup()
+    if args.gpus > 1 and world != args.gpus and rank == 0:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}; running {world} rank(s)", file=sys.stderr)
     try:
         if args.impl == "reference":
             run_reference(args, world, rank)

@@ -87,7 +87,7 @@ int obt_model_info(const obt_model* model, int32_t* n_features, int32_t* n_trees
                    int32_t* leaf_storage, int32_t* compare_mode);
 
 /* Which quantize search the predict path runs for TMA-eligible inputs (object-major,
- * F % 4 == 0, 16-byte aligned): kind 1 / 2 = cell tables (K1L, 256 / 1024 cells per
+ * F % 4 == 0, 16-byte aligned): kind 1 / 2 / 3 = cell tables (K1L, 256 / 1024 / 512 cells per
  * feature) with `param` compares per value, kind 0 = Eytzinger search (K1t) with `param`
  * levels.  Diagnostics for tests
  * and tuning; no reference counterpart (the reference always counts every border,

@@ -116,8 +116,9 @@ void orc_leaf_indices(const uint8_t* q, int64_t n, int32_t n_trees, int32_t max_
 
 /* ---------------------------------------------------------------------------
  * binary16 helpers -- model.py:231-277 (build_leaf_bank): leaves.astype(float16)
- * is a direct binary64 -> binary16 round-to-nearest-even conversion; a finite
- * leaf that overflows to +/-inf is saturated to +/-65504 (model.py:262-268).
+ * is a direct binary64 -> binary16 round-to-nearest-even conversion; every
+ * +/-inf result (finite overflow or an infinite leaf) is saturated to +/-65504
+ * (model.py:262-268).
  */
 uint16_t orc_half_from_double(double x) {
   uint64_t bits;
@@ -155,7 +156,7 @@ uint16_t orc_half_from_double(double x) {
 
 uint16_t orc_half_saturated(double x) {
   uint16_t h = orc_half_from_double(x);
-  if (isfinite(x) && (h & 0x7FFFu) == 0x7C00u) h = (uint16_t)((h & 0x8000u) | 0x7BFFu);
+  if ((h & 0x7FFFu) == 0x7C00u) h = (uint16_t)((h & 0x8000u) | 0x7BFFu);
   return h;
 }
 
@@ -187,7 +188,7 @@ int64_t orc_half_bank(const double* leaves, int64_t count, uint16_t* out) {
   int64_t saturated = 0;
   for (int64_t i = 0; i < count; ++i) {
     const uint16_t raw = orc_half_from_double(leaves[i]);
-    if (isfinite(leaves[i]) && (raw & 0x7FFFu) == 0x7C00u) ++saturated;
+    if ((raw & 0x7FFFu) == 0x7C00u) ++saturated; /* inf leaves too (model.py:264) */
     out[i] = orc_half_saturated(leaves[i]);
   }
   return saturated;

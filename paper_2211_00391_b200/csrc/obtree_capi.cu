@@ -174,10 +174,11 @@ uint16_t half_rne(double x) {
   return (uint16_t)(sign | ((uint32_t)(he + 15) << 10) | (uint32_t)(q - 1024));
 }
 
-// saturation of finite overflow to +/-65504 (model.py:264-267)
+// saturation of every infinite result (finite overflow and infinite leaves) to
+// +/-65504 (model.py:262-268: the reference tests isinf on the cast values only)
 uint16_t half_bank_entry(double x) {
   uint16_t h = half_rne(x);
-  if (std::isfinite(x) && (h & 0x7FFFu) == 0x7C00u) h = (uint16_t)((h & 0x8000u) | 0x7BFFu);
+  if ((h & 0x7FFFu) == 0x7C00u) h = (uint16_t)((h & 0x8000u) | 0x7BFFu);
   return h;
 }
 
@@ -1354,7 +1355,7 @@ int obt_model_info(const obt_model* m, int32_t* n_features, int32_t* n_trees, in
 int obt_model_quantize_kernel(const obt_model* m, int32_t* kind, int32_t* param) {
   if (!m) return fail(OBT_E_INVALID, "null model");
   const bool lut = lut_preferred(m);
-  if (kind) *kind = lut ? (m->used_lut.cells == 1024 ? 2 : 1) : 0;
+  if (kind) *kind = lut ? (m->used_lut.cells == 1024 ? 2 : m->used_lut.cells == 512 ? 3 : 1) : 0;
   if (param) *param = lut ? m->used_lut.kmax : m->used.levels;
   return OBT_OK;
 }

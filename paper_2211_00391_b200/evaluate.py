@@ -16,7 +16,7 @@ from typing import Optional
 
 import numpy as np
 
-from . import _native
+from . import _checks, _native
 from .config import EvalConfig
 from .matrix import FeatureMatrix, Layout, layout_code
 from .model import LeafBank, LeafPrecision, ObliviousModel, build_leaf_bank, half_bank_values, require_valid
@@ -66,7 +66,7 @@ class DeviceModel:
         per value) for the cell-table kernel, ("eytzinger", levels) otherwise."""
         kind, param = ctypes.c_int32(), ctypes.c_int32()
         _native.check(self._lib.obt_model_quantize_kernel(self.handle, ctypes.byref(kind), ctypes.byref(param)))
-        return ({1: "cells", 2: "cells1024"}.get(kind.value, "eytzinger"), param.value)
+        return ({1: "cells", 2: "cells1024", 3: "cells512"}.get(kind.value, "eytzinger"), param.value)
 
     def close(self) -> None:
         if getattr(self, "handle", None) and self.handle.value:
@@ -145,8 +145,7 @@ class ModelTables:
 
 
 def _check_features(matrix_features: int, model: ObliviousModel) -> None:
-    if matrix_features != model.n_features:
-        raise ValueError(f"matrix has {matrix_features} features, model expects {model.n_features}")
+    _checks.check_features(matrix_features, model.n_features)
 
 
 class Evaluator:
@@ -190,10 +189,7 @@ class Evaluator:
             return self.predict_device(matrix)
         _check_features(matrix.n_features, self.model)
         n = matrix.n_objects
-        if out is None:
-            out = np.empty(n, dtype=np.float64)
-        elif out.dtype != np.float64 or out.shape != (n,) or not out.flags.c_contiguous:
-            raise ValueError("out must be a contiguous float64 array of one score per object")
+        out = _checks.host_out(out, n, 1)
         if n == 0:
             return out
         import torch
@@ -212,22 +208,10 @@ class Evaluator:
         """HBM-resident predict: ``x`` float32 CUDA tensor [n][F] (object-major) or
         [F][n] (feature-major) -> float64 CUDA tensor [n]; asynchronous on the
         current stream.  ``workspace`` (uint8 CUDA tensor) avoids pool allocation."""
-        import torch
-
-        if not (isinstance(x, torch.Tensor) and x.is_cuda):
-            raise TypeError("predict_device expects a CUDA tensor")
-        if x.dtype != torch.float32 or x.dim() != 2:
-            raise ValueError("feature tensor must be 2-D float32")
-        x = x.contiguous()
-        n, f = (x.shape[0], x.shape[1]) if layout is Layout.OBJECT_MAJOR else (x.shape[1], x.shape[0])
-        _check_features(f, self.model)
-        if out is None:
-            out = torch.empty(n, dtype=torch.float64, device=x.device)
+        x, n, out, ws_ptr, ws_bytes = _checks.device_inputs(x, layout, self.model.n_features, self.device, 1, out,
+                                                             workspace)
         if n == 0:
             return out
-        ws_ptr, ws_bytes = (0, 0)
-        if workspace is not None:
-            ws_ptr, ws_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
         lib = self._dev._lib
         stream = _native.current_stream_handle(x.device)
         _native.check(
@@ -239,14 +223,10 @@ class Evaluator:
 
     def predict_device_marked(self, x, events, layout: Layout = Layout.OBJECT_MAJOR, out=None, workspace=None):
         """``predict_device`` recording three ``_native.Event``s around the two kernels."""
-        import torch
-
-        n = x.shape[0] if layout is Layout.OBJECT_MAJOR else x.shape[1]
-        if out is None:
-            out = torch.empty(n, dtype=torch.float64, device=x.device)
-        ws_ptr, ws_bytes = (0, 0)
-        if workspace is not None:
-            ws_ptr, ws_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
+        x, n, out, ws_ptr, ws_bytes = _checks.device_inputs(x, layout, self.model.n_features, self.device, 1, out,
+                                                             workspace)
+        if n == 0:
+            return out
         stream = _native.current_stream_handle(x.device)
         ev = [e.handle if e is not None else None for e in events]
         _native.check(

@@ -200,12 +200,13 @@ def aligned_zeros(n: int, dtype, alignment: int = 64) -> np.ndarray:
 
 
 def half_bank_values(leaves: np.ndarray):
-    """binary64 leaves -> (binary16 values, saturation count): numpy's RNE cast,
-    finite overflow clamped to +/-65504 (reference model.py:262-268)."""
+    """binary64 leaves -> (binary16 values, saturation count): numpy's RNE cast, every
+    infinite result -- finite overflow and infinite leaves alike -- clamped to +/-65504
+    and counted (reference model.py:262-268 tests isinf on the cast values only)."""
     leaves = np.asarray(leaves, dtype=np.float64)
     with np.errstate(over="ignore"):
         halves = leaves.astype(np.float16)
-    overflow = np.isinf(halves) & np.isfinite(leaves)
+    overflow = np.isinf(halves)
     if overflow.any():
         halves[overflow] = np.where(leaves[overflow] > 0, np.float16(HALF_MAX), np.float16(-HALF_MAX))
     return halves, int(overflow.sum())

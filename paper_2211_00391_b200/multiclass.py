@@ -15,7 +15,7 @@ from typing import Optional
 
 import numpy as np
 
-from . import _native
+from . import _checks, _native
 from .matrix import FeatureMatrix, Layout, layout_code
 from .model import MAX_BORDERS
 
@@ -133,7 +133,7 @@ class MultiOutputEvaluator:
         """("cells", compares) or ("eytzinger", levels): the predict path's quantize search."""
         kind, param = ctypes.c_int32(), ctypes.c_int32()
         _native.check(self._lib.obt_model_quantize_kernel(self.handle, ctypes.byref(kind), ctypes.byref(param)))
-        return ({1: "cells", 2: "cells1024"}.get(kind.value, "eytzinger"), param.value)
+        return ({1: "cells", 2: "cells1024", 3: "cells512"}.get(kind.value, "eytzinger"), param.value)
 
     def apply_kernel(self) -> str:
         """The multi-output apply kernel this model runs: "staged" (K5), "sliced" (K4s) or "gather" (K4)."""
@@ -143,17 +143,8 @@ class MultiOutputEvaluator:
 
     def predict_device(self, x, layout: Layout = Layout.OBJECT_MAJOR, out=None, workspace=None):
         """float32 CUDA tensor [n][F] (or [F][n]) -> float64 CUDA tensor [n][C]."""
-        import torch
-
-        x = x.contiguous()
-        ws_ptr, ws_bytes = (0, 0)
-        if workspace is not None:
-            ws_ptr, ws_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
-        n, f = (x.shape[0], x.shape[1]) if layout is Layout.OBJECT_MAJOR else (x.shape[1], x.shape[0])
-        if f != self.model.n_features:
-            raise ValueError(f"matrix has {f} features, model expects {self.model.n_features}")
-        if out is None:
-            out = torch.empty((n, self.model.n_outputs), dtype=torch.float64, device=x.device)
+        x, n, out, ws_ptr, ws_bytes = _checks.device_inputs(x, layout, self.model.n_features, self.device,
+                                                             self.model.n_outputs, out, workspace)
         if n:
             _native.check(self._lib.obt_predict_dev(self.handle, x.data_ptr(), n, layout_code(layout), out.data_ptr(),
                                                     ws_ptr, ws_bytes, _native.current_stream_handle(x.device)))
@@ -161,14 +152,10 @@ class MultiOutputEvaluator:
 
     def predict_device_marked(self, x, events, layout: Layout = Layout.OBJECT_MAJOR, out=None, workspace=None):
         """predict_device recording three _native.Event's around the two kernels."""
-        import torch
-
-        n = x.shape[0] if layout is Layout.OBJECT_MAJOR else x.shape[1]
-        if out is None:
-            out = torch.empty((n, self.model.n_outputs), dtype=torch.float64, device=x.device)
-        ws_ptr, ws_bytes = (0, 0)
-        if workspace is not None:
-            ws_ptr, ws_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
+        x, n, out, ws_ptr, ws_bytes = _checks.device_inputs(x, layout, self.model.n_features, self.device,
+                                                             self.model.n_outputs, out, workspace)
+        if n == 0:
+            return out
         ev = [e.handle if e is not None else None for e in events]
         _native.check(self._lib.obt_predict_dev_marked(self.handle, x.data_ptr(), n, layout_code(layout), out.data_ptr(),
                                                        ws_ptr, ws_bytes, _native.current_stream_handle(x.device), *ev))
@@ -189,10 +176,10 @@ class MultiOutputEvaluator:
         return _native.LEAF_STORAGE_NAMES[info[5].value]
 
     def predict(self, matrix: FeatureMatrix, out: Optional[np.ndarray] = None) -> np.ndarray:
-        if matrix.n_features != self.model.n_features:
-            raise ValueError(f"matrix has {matrix.n_features} features, model expects {self.model.n_features}")
-        if out is None:
-            out = np.empty((matrix.n_objects, self.model.n_outputs), dtype=np.float64)
+        if not isinstance(matrix, FeatureMatrix):
+            return self.predict_device(matrix)
+        _checks.check_features(matrix.n_features, self.model.n_features)
+        out = _checks.host_out(out, matrix.n_objects, self.model.n_outputs)
         if matrix.n_objects:
             import torch
 

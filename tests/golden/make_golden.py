@@ -132,6 +132,19 @@ def known_answers() -> dict:
     bank = build_leaf_bank(sat, LeafPrecision.BINARY16)
     out["half_saturation"] = {"bits": [int(v) for v in bank.table(0)[:2].view(np.uint16)],
                               "count": int(bank.saturation_count)}
+    # infinite leaves are saturated and counted too (model.py:262-268 tests isinf on the
+    # cast values); the NAIVE16 pipeline then sums finite +/-65504 instead of +/-inf
+    inf_model = ObliviousModel(one_feature([0.5]),
+                               (ObliviousTree(2, (SplitCondition(0, 0), SplitCondition(0, 0)),
+                                              np.array([np.inf, -np.inf, 70000.0, 1.0])),
+                                ObliviousTree(1, (SplitCondition(0, 0),), np.array([-np.inf, 3.0]))), 1.0, 0.0)
+    bank = build_leaf_bank(inf_model, LeafPrecision.BINARY16)
+    xm = FeatureMatrix(np.array([[0.25], [0.75], [np.nan], [0.5]], np.float32), Layout.OBJECT_MAJOR)
+    out["half_saturation_inf"] = {
+        "bits": [int(v) for v in bank.table(0)[:4].view(np.uint16)] + [int(v) for v in bank.table(1)[:2].view(np.uint16)],
+        "count": int(bank.saturation_count), "x": [0.25, 0.75, None, 0.5],
+        "predictions_naive16": evaluate(inf_model, xm, EvalConfig(strategy=LeafStrategy.NAIVE16)).tolist(),
+        "predictions_scalar16": evaluate_scalar(inf_model, xm, LeafPrecision.BINARY16).tolist()}
     # xoshiro streams (seed expansion + update rule)
     streams = {}
     for seed in (0, 1, 99, 90125, 2**64 - 1):

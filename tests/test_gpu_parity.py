@@ -162,6 +162,59 @@ def test_depth3_known_answer():
     assert idx[0, 0] == 5
 
 
+def test_binary16_infinite_leaves_saturate_like_the_reference():
+    """Infinite leaves become +/-65504 in the binary16 bank (model.py:262-268), so the
+    NAIVE16 predictions are the reference's finite sums (golden from the reference)."""
+    import json
+    from pathlib import Path
+
+    g = json.loads((Path(__file__).parent / "golden" / "known_answers.json").read_text())["half_saturation_inf"]
+    from test_host_api import _inf_leaf_model
+
+    model = _inf_leaf_model()
+    x = np.array([[0.25], [0.75], [np.nan], [0.5]], np.float32)
+    ev = obt.Evaluator(model, obt.EvalConfig(strategy=obt.LeafStrategy.NAIVE16), device=0)
+    got = ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
+    assert got.tolist() == g["predictions_naive16"] == g["predictions_scalar16"]
+    want = oracle.evaluate_scalar(oracle.flatten(model), x, oracle.OBJECT_MAJOR, oracle.BINARY16)
+    assert np.array_equal(got, want)
+
+
+def test_device_entry_points_check_every_buffer():
+    """out / workspace / x are checked before a pointer reaches the kernels: wrong dtype,
+    short or non-contiguous outputs and foreign devices raise instead of writing."""
+    from paper_2211_00391_b200 import multiclass
+
+    model = _model(8, 16, 12, 4, seed=5)
+    ev = obt.Evaluator(model, device=0)
+    x = torch.from_numpy(_features(model, 300, seed=6)).cuda()
+    good = ev.predict_device(x)
+    bad_outs = [torch.empty(300, dtype=torch.float32, device="cuda"), torch.empty(299, dtype=torch.float64, device="cuda"),
+                torch.empty(600, dtype=torch.float64, device="cuda")[::2], torch.empty(300, dtype=torch.float64)]
+    for out in bad_outs:
+        with pytest.raises(ValueError):
+            ev.predict_device(x, out=out)
+        with pytest.raises(ValueError):
+            ev.predict_device_marked(x, [None, None, None], out=out)
+    with pytest.raises(ValueError):
+        ev.predict_device(x, workspace=torch.empty(1 << 20, dtype=torch.float32, device="cuda"))
+    with pytest.raises(ValueError):
+        ev.predict_device(x.double())
+    with pytest.raises(ValueError, match="features"):
+        ev.predict_device(x[:, :7])
+    with pytest.raises(ValueError):
+        ev.predict(obt.FeatureMatrix(x.cpu().numpy(), obt.Layout.OBJECT_MAJOR), out=np.empty(300, np.float32))
+    assert torch.equal(ev.predict_device(x[::1]), good)
+    mm = multiclass.from_arrays(synthetic.model_arrays(synthetic.WorkloadSpec("m", 1, 8, 16, 12, 4, 0.1, cfg=5,
+                                                                               n_outputs=3)))
+    mev = multiclass.MultiOutputEvaluator(mm, device=0)
+    with pytest.raises(ValueError):
+        mev.predict_device(x, out=torch.empty(300, dtype=torch.float64, device="cuda"))
+    with pytest.raises(ValueError):
+        mev.predict(obt.FeatureMatrix(x.cpu().numpy(), obt.Layout.OBJECT_MAJOR), out=np.empty(300, np.float64))
+    assert mev.predict_device(x).shape == (300, 3)
+
+
 def test_predict_device_matches_host_path():
     model = _model(40, 64, 200, 6, seed=5, affine=False)
     x = _features(model, 20000, seed=6, specials=False)

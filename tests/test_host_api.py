@@ -122,6 +122,24 @@ def test_binary16_bank_matches_reference_bits(known=None):
     assert bank.saturation_count == 2 and bank.table(0).size == 32 and bank.values.flags.writeable is False
 
 
+def test_binary16_bank_saturates_infinite_leaves():
+    import json
+
+    g = json.loads((GOLDEN / "known_answers.json").read_text())["half_saturation_inf"]
+    m = _inf_leaf_model()
+    bank = obt.build_leaf_bank(m, obt.LeafPrecision.BINARY16)
+    got = [int(v) for v in bank.table(0)[:4].view(np.uint16)] + [int(v) for v in bank.table(1)[:2].view(np.uint16)]
+    assert got == g["bits"] and bank.saturation_count == g["count"]
+
+
+def _inf_leaf_model():
+    return obt.ObliviousModel(
+        one_feature([0.5]),
+        (obt.ObliviousTree(2, (obt.SplitCondition(0, 0), obt.SplitCondition(0, 0)),
+                           np.array([np.inf, -np.inf, 70000.0, 1.0])),
+         obt.ObliviousTree(1, (obt.SplitCondition(0, 0),), np.array([-np.inf, 3.0]))), 1.0, 0.0)
+
+
 def test_model_tables_packing_for_the_c_abi():
     trees = (
         obt.ObliviousTree(2, (obt.SplitCondition(0, 1), obt.SplitCondition(1, 0)), np.array([1.0, 2.0, 3.0, 4.0])),

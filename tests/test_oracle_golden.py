@@ -74,6 +74,16 @@ def test_half_saturation(known):
     assert count == known["half_saturation"]["count"]
 
 
+def test_half_saturation_of_infinite_leaves(known):
+    """model.py:262-268: every +/-inf cast result is clamped and counted, infinite
+    leaves included; the binary16 oracle then sums the finite clamps."""
+    g = known["half_saturation_inf"]
+    bits0, c0 = oracle.half_bank(np.array([np.inf, -np.inf, 70000.0, 1.0]))
+    bits1, c1 = oracle.half_bank(np.array([-np.inf, 3.0]))
+    assert [int(b) for b in bits0] + [int(b) for b in bits1] == g["bits"]
+    assert c0 + c1 == g["count"]
+
+
 def test_xoshiro_streams(known):
     for seed, expect in known["xoshiro"].items():
         if seed == "state_1234":

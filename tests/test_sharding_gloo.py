@@ -78,6 +78,24 @@ def _worker(rank, world, port, case):
             assert got.shape == full_m.shape == (x.shape[0], 10)
             rel = np.abs(got - full_m) / np.maximum(np.maximum(np.abs(got), np.abs(full_m)), 1e-300)
             assert rel.max() <= 1e-12, rel.max()
+        elif case.startswith("grid"):
+            from paper_2211_00391_b200 import multiclass, synthetic
+
+            go, gt = (int(v) for v in case.split("_")[1].split("x"))
+            spec = synthetic.WorkloadSpec("m", 1, 9, 40, 101, 10, 0.01, n_outputs=10, cfg=5)
+            mm = multiclass.from_arrays(synthetic.model_arrays(spec, seed=3, affine=True))
+            full_m = oracle.evaluate_scalar(_flat(mm), x)
+            ev = sharding.GridShardedEvaluator(mm, go, gt, local_predict=_oracle_predict, reduce_device="cpu")
+            assert ev.tree_range == sharding.tree_shard(mm.n_trees, rank % gt, gt)
+            got = ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
+            assert got.shape == full_m.shape
+            rel = np.abs(got - full_m) / np.maximum(np.maximum(np.abs(got), np.abs(full_m)), 1e-300)
+            assert rel.max() <= 1e-12, rel.max()
+            if gt == 1:
+                assert np.array_equal(got, full_m), "a 1-tree-group grid is object sharding: bit-exact"
+            local = ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR), gather=False)
+            b, e = ev.object_range(x.shape[0])
+            assert np.allclose(local, full_m[b:e], rtol=1e-12, atol=0)
         else:
             ev = sharding.TreeShardedEvaluator(model, local_predict=_oracle_predict, reduce_device="cpu")
             got = ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
@@ -89,9 +107,14 @@ def _worker(rank, world, port, case):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case", ["objects", "objects_multi", "trees", "trees_multi"])
+@pytest.mark.parametrize("case", ["objects", "objects_multi", "trees", "trees_multi", "grid_1x2", "grid_2x1"])
 def test_two_rank_gloo(case):
     mp.spawn(_worker, args=(2, _free_port(), case), nprocs=2, join=True)
+
+
+def test_four_rank_grid_gloo():
+    """2 object shards x 2 tree shards: each object shard reduces within its own group."""
+    mp.spawn(_worker, args=(4, _free_port(), "grid_2x2"), nprocs=4, join=True)
 
 
 def test_balanced_ranges_cover_exactly():
