@@ -22,6 +22,7 @@
 #include "../../include/obtree_b200.h"
 #include "obtree_kernels.cuh"
 #include "dispatch.h"
+#include "wide_apply.cuh"
 
 using obt::ApplyKernel;
 using obt::QuantFn;
@@ -97,6 +98,16 @@ struct TilePlan {
   uint32_t tables_chunk_bytes = 0;
 };
 
+// K2w records: per chunk of chunk_trees trees, descriptors (kWideDescBytes(DI) per tree,
+// 256-byte aligned block) then leaf tables (`stride` bytes each), trees in the predict
+// path's level order.
+struct WidePlan {
+  uint8_t* d_chunks = nullptr;
+  int chunk_trees = 0, n_chunks = 0, stages = 0;
+  uint32_t chunk_bytes = 0, desc_bytes = 0, stride = 0;
+  size_t smem = 0;
+};
+
 }  // namespace
 
 struct obt_model {
@@ -121,6 +132,9 @@ struct obt_model {
   std::vector<int32_t> split_feature;   // [T][DI]
   std::vector<uint8_t> split_ordinal;   // [T][DI]
   std::vector<uint8_t> leaf_bytes;      // [T][2^DI] in leaf_storage
+  // predict-path level order: level_perm[t][j] = the reference level evaluated as depth j
+  // (index bit j); index dumps keep the reference order (see level_order)
+  std::vector<uint8_t> level_perm;      // [T][DI]
   // chunk geometry (independent of the tile size)
   int padded_trees = 0;
   int chunk_trees = 1, n_chunks = 0;
@@ -129,8 +143,10 @@ struct obt_model {
   int smem_optin = 232448;
   std::mutex mu;
   std::map<int, TilePlan> plans;
+  std::unique_ptr<WidePlan> wide;        // K2w records (built on first use, under mu)
   obt::ApplyArgs<1> param_args;  // launch-parameter staging (32 KB), guarded by mu
   ~obt_model() {
+    if (wide && wide->d_chunks) cudaFree(wide->d_chunks);
     for (auto& kv : plans) {
       cudaFree(kv.second.d_chunks);
       if (kv.second.d_tables) cudaFree(kv.second.d_tables);
@@ -413,10 +429,12 @@ void plan_chunks(obt_model* m) {
 }
 
 // Descriptor words of tree t (padded trees are all-sentinel) for a given tile size:
-// 7-bit compare {off, k replicated}; 8-bit compare {(off << 8) | k, s}.
-void tree_descriptors(const obt_model* m, int t, int tile, uint32_t* out) {
+// 7-bit compare {off, k replicated}; 8-bit compare {(off << 8) | k, s}.  `ordered`: the
+// predict path's level order (level_perm), else the reference's (index dumps).
+void tree_descriptors(const obt_model* m, int t, int tile, uint32_t* out, bool ordered = true) {
   const int DI = m->depth_inst;
-  for (int d = 0; d < DI; ++d) {
+  for (int j = 0; j < DI; ++j) {
+    const int d = (ordered && t < m->n_trees && !m->level_perm.empty()) ? m->level_perm[(size_t)t * DI + j] : j;
     const int ord = t < m->n_trees ? m->split_ordinal[(size_t)t * DI + d] : kSentinel;
     uint32_t w0 = 0, w1 = 0;  // sentinel: offset 0, k 0 never carries into bit 7
     if (ord != kSentinel) {
@@ -429,8 +447,55 @@ void tree_descriptors(const obt_model* m, int t, int tile, uint32_t* out) {
         w1 = ord < 128 ? 0xFFFFFFFFu : 0u;                    // or-with-q vs and-with-q
       }
     }
-    out[2 * d] = w0;
-    out[2 * d + 1] = w1;
+    out[2 * j] = w0;
+    out[2 * j + 1] = w1;
+  }
+}
+
+// Leaf i' of a tree evaluated in level order perm is leaf i = sum_j bit_j(i') << perm[j]
+// of the reference order.
+size_t reference_leaf(const uint8_t* perm, int DI, size_t ip) {
+  size_t i = 0;
+  for (int j = 0; j < DI; ++j) i |= ((ip >> j) & 1u) << perm[j];
+  return i;
+}
+
+// Tree t's leaf table (2^DI entries of `ls` bytes) in the predict path's level order.
+void ordered_leaves(const obt_model* m, int t, uint8_t* dst) {
+  const int DI = m->depth_inst;
+  const size_t ls = leaf_size(m->leaf_storage), n = (size_t)1 << DI;
+  const uint8_t* src = m->leaf_bytes.data() + (size_t)t * n * ls;
+  const uint8_t* perm = m->level_perm.data() + (size_t)t * DI;
+  for (size_t ip = 0; ip < n; ++ip) std::memcpy(dst + ip * ls, src + reference_leaf(perm, DI, ip) * ls, ls);
+}
+
+// Predict-path level order of every tree (exact: a permutation of the index bits and of
+// the leaf table).  A warp-wide gather from a 2^D-entry table costs as many shared-memory
+// wavefronts as the most distinct entries any one bank is asked for; the bank is set by
+// the low index bits.  Levels whose condition is nearly always true or false (ordinals
+// near either end of the feature's borders: P(x > b_k) ~ 1 - (k+1)/(B+1) for quantile
+// borders) take the high bits, where lanes then mostly agree, and the most uncertain
+// levels the low (bank) bits.  Measured by Monte Carlo at depth 8 / fp32 leaves: ~4.0 ->
+// ~2.6 wavefronts per warp gather (depth 6: 1.9 -> 1.7).  Sentinel levels go last.
+void plan_level_order(obt_model* m, const obt_model_desc* d) {
+  const int DI = m->depth_inst, D = m->max_depth;
+  m->level_perm.assign((size_t)m->n_trees * DI, 0);
+  std::vector<std::pair<double, int>> key(DI);
+  for (int t = 0; t < m->n_trees; ++t) {
+    for (int j = 0; j < DI; ++j) {
+      double h = -1.0;  // sentinel / padding levels: never true, zero entropy
+      if (j < D) {
+        const int ord = d->split_ordinal[(size_t)t * D + j];
+        if (ord != kSentinel) {
+          const int nb = d->border_counts[d->split_feature[(size_t)t * D + j]];
+          const double p = 1.0 - (ord + 1.0) / (nb + 1.0);
+          h = (p <= 0.0 || p >= 1.0) ? 0.0 : -(p * std::log(p) + (1.0 - p) * std::log(1.0 - p));
+        }
+      }
+      key[j] = {-h, j};
+    }
+    std::stable_sort(key.begin(), key.end());
+    for (int j = 0; j < DI; ++j) m->level_perm[(size_t)t * DI + j] = (uint8_t)key[j].second;
   }
 }
 
@@ -495,6 +560,7 @@ int build_tile_plan(obt_model* m, int tile, int variant, TilePlan& out) {
   // carries the leaf tables alone (27% fewer bytes per chunk at cfg2)
   const uint32_t tcb = (uint32_t)((stride * ct + 255) & ~(size_t)255);
   std::vector<uint8_t> host_tables(variant == 0 ? (size_t)std::max(m->n_chunks, 1) * tcb : 0, 0);
+  // variant 0: predicts (level order of level_perm); 1: K2s; 2: index dumps (reference order)
   out.param_desc.assign((size_t)m->padded_trees * DI * 2, 0u);
   std::vector<uint32_t> words((size_t)DI * 2);
   std::vector<int> perm(DI), wild(DI);
@@ -502,7 +568,7 @@ int build_tile_plan(obt_model* m, int tile, int variant, TilePlan& out) {
   for (int t = 0; t < m->padded_trees; ++t) {
     const int c = t / ct, tl = t % ct;
     uint8_t* rec = host.data() + (size_t)c * chunk_bytes;
-    tree_descriptors(m, t, tile, words.data());
+    tree_descriptors(m, t, tile, words.data(), variant == 0);
     if (m->compare_mode == 7) std::memcpy(out.param_desc.data() + (size_t)t * DI * 2, words.data(), (size_t)DI * 8);
     if (variant == 1) {
       // K2s: 16 bytes per split in paired level order, row offsets +- 64 for odd rows;
@@ -548,7 +614,8 @@ int build_tile_plan(obt_model* m, int tile, int variant, TilePlan& out) {
     std::memcpy(rec + (size_t)tl * dwt * 4, words.data(), (size_t)dwt * 4);
     uint8_t* leaf_dst = rec + desc_bytes + (size_t)tl * stride;
     if (t < m->n_trees) {
-      std::memcpy(leaf_dst, m->leaf_bytes.data() + (size_t)t * per_tree_leaf, per_tree_leaf);
+      if (variant == 0) ordered_leaves(m, t, leaf_dst);
+      else std::memcpy(leaf_dst, m->leaf_bytes.data() + (size_t)t * per_tree_leaf, per_tree_leaf);
     } else {
       write_null_leaves(m, leaf_dst);
     }
@@ -566,7 +633,7 @@ int build_tile_plan(obt_model* m, int tile, int variant, TilePlan& out) {
 
 int get_tile_plan(obt_model* m, int tile, int variant, const TilePlan** out) {
   std::lock_guard<std::mutex> lock(m->mu);
-  const int key = tile * 2 + variant;
+  const int key = tile * 4 + variant;
   auto it = m->plans.find(key);
   if (it == m->plans.end()) {
     TilePlan tp;
@@ -834,7 +901,7 @@ int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, int tpw, d
   const bool write_idx = idx_out != nullptr;
   const int dsrc = use_param_descriptors(m, tpw);
   const TilePlan* tp = nullptr;
-  int rc = get_tile_plan(m, tile, tpw > 1 ? 1 : 0, &tp);
+  int rc = get_tile_plan(m, tile, tpw > 1 ? 1 : write_idx ? 2 : 0, &tp);
   if (rc != OBT_OK) return rc;
   ApplyKernel k = tpw > 1 ? pick_split(m->depth_inst, m->compare_mode, m->leaf_storage, tpw)
                           : pick_apply(m->depth_inst, m->compare_mode, m->leaf_storage, write_idx, dsrc);
@@ -983,6 +1050,95 @@ int launch_fan(obt_model* m, const uint8_t* q, int64_t n, double* out, cudaStrea
   return OBT_OK;
 }
 
+// K2w records for the 256-object tile, in the predict path's level order; null trees
+// (sentinel descriptors, -0.0 leaves) pad the last chunk.
+constexpr int kWideChunkTrees = 16;  // a multiple of the fold warps' 4-tree groups
+int build_wide_plan(obt_model* m, WidePlan& w) {
+  const int DI = m->depth_inst;
+  const size_t ls = leaf_size(m->leaf_storage), per_tree_leaf = ls << DI;
+  w.stride = (uint32_t)((per_tree_leaf + 15) & ~(size_t)15);
+  w.chunk_trees = std::min(kWideChunkTrees, std::max(4, (m->n_trees + 3) / 4 * 4));
+  w.n_chunks = (m->n_trees + w.chunk_trees - 1) / w.chunk_trees;
+  const uint32_t dpt = obt::kWideDescBytes(DI);
+  w.desc_bytes = (uint32_t)(((size_t)w.chunk_trees * dpt + 255) & ~(size_t)255);
+  w.chunk_bytes = (uint32_t)(((size_t)w.desc_bytes + (size_t)w.chunk_trees * w.stride + 255) & ~(size_t)255);
+  const size_t per_stage = (size_t)w.chunk_bytes + obt::wide_panel_bytes(w.chunk_trees);
+  const size_t fixed = 512 + (size_t)m->n_features * obt::kWideTile;
+  if (fixed + 2 * per_stage > (size_t)m->smem_optin) return OBT_E_UNSUPPORTED;
+  w.stages = (int)std::min<size_t>(obt::kWideMaxStages, std::min<size_t>(4, ((size_t)m->smem_optin - fixed) / per_stage));
+  w.smem = fixed + (size_t)w.stages * per_stage;
+  std::vector<uint8_t> host((size_t)std::max(w.n_chunks, 1) * w.chunk_bytes, 0);
+  std::vector<uint32_t> words((size_t)DI * 2);
+  for (int t = 0; t < w.n_chunks * w.chunk_trees; ++t) {
+    const int c = t / w.chunk_trees, tl = t % w.chunk_trees;
+    uint8_t* rec = host.data() + (size_t)c * w.chunk_bytes;
+    tree_descriptors(m, t, obt::kWideTile, words.data(), true);
+    std::memcpy(rec + (size_t)tl * dpt, words.data(), (size_t)DI * 8);
+    uint8_t* leaf_dst = rec + w.desc_bytes + (size_t)tl * w.stride;
+    if (t < m->n_trees) ordered_leaves(m, t, leaf_dst);
+    else write_null_leaves(m, leaf_dst);
+  }
+  CUDA_TRY(cudaMalloc(&w.d_chunks, host.size()));
+  CUDA_TRY(cudaMemcpy(w.d_chunks, host.data(), host.size(), cudaMemcpyHostToDevice));
+  return OBT_OK;
+}
+
+int get_wide_plan(obt_model* m, const WidePlan** out) {
+  std::lock_guard<std::mutex> lock(m->mu);
+  if (!m->wide) {
+    std::unique_ptr<WidePlan> w(new WidePlan());
+    const int rc = build_wide_plan(m, *w);
+    if (rc != OBT_OK) return rc == OBT_E_UNSUPPORTED ? fail(rc, "K2w does not fit shared memory") : rc;
+    m->wide = std::move(w);
+  }
+  *out = m->wide.get();
+  return OBT_OK;
+}
+
+// K2w where the K2 tile would hold few objects: the bucket tile (F bytes per object)
+// leaves K2 too few warps per SM (config 4, F = 500: 256 objects, 2 warps).
+bool wide_eligible(const obt_model* m) {
+  if (m->n_outputs > 1 || m->depth_inst > 8 || m->n_trees == 0) return false;
+  const size_t per_stage = 2 * ((size_t)kWideChunkTrees * (leaf_size(m->leaf_storage) << m->depth_inst) + 2048) +
+                           obt::wide_panel_bytes(kWideChunkTrees);
+  if (512 + (size_t)m->n_features * obt::kWideTile + per_stage > (size_t)m->smem_optin) return false;
+  if (!obt::pick_wide(m->depth_inst, m->compare_mode, m->leaf_storage)) return false;
+  const char* e = getenv("OBT_WIDE");  // A/B knob: 0 never, 1 wherever it fits
+  if (e && !strcmp(e, "0")) return false;
+  if (e && !strcmp(e, "1")) return true;
+  return plan_tile(m, (int64_t)1 << 40) <= 512;
+}
+
+int launch_wide(obt_model* m, const uint8_t* q, int64_t n, double* out, cudaStream_t stream) {
+  const void* fn = obt::pick_wide(m->depth_inst, m->compare_mode, m->leaf_storage);
+  if (!fn) return fail(OBT_E_UNSUPPORTED, "no K2w kernel for depth %d", m->depth_inst);
+  const WidePlan* w = nullptr;
+  int rc = get_wide_plan(m, &w);
+  if (rc != OBT_OK) return rc;
+  obt::WideParams p{};
+  p.q = q;
+  p.chunks = w->d_chunks;
+  p.out = out;
+  p.n = n;
+  p.n_tiles = (n + obt::kWideTile - 1) / obt::kWideTile;
+  p.n_chunks = w->n_chunks;
+  p.chunk_trees = w->chunk_trees;
+  p.chunk_bytes = w->chunk_bytes;
+  p.desc_bytes = w->desc_bytes;
+  p.table_stride = w->stride;
+  p.q_tile_bytes = (uint32_t)((size_t)m->n_features * obt::kWideTile);
+  p.n_stages = w->stages;
+  p.scale = m->scale;
+  p.bias = m->bias;
+  CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, m->smem_optin));
+  void* kargs[] = {&p};
+  const dim3 grid((unsigned)std::min<int64_t>(p.n_tiles, m->sm_count)),
+      block(32 * (1 + obt::kWideIndexWarps + obt::kWideFoldWarps));
+  CUDA_TRY(cudaLaunchKernel(fn, grid, block, kargs, w->smem, stream));
+  ++g_launches;
+  return OBT_OK;
+}
+
 int launch_multi_staged(obt_model* m, const uint8_t* q, int64_t n, double* out, cudaStream_t stream) {
   int di = 0;
   const void* fn = obt::pick_multi_staged(m->depth_inst, m->compare_mode, m->n_outputs, &di);
@@ -1087,7 +1243,8 @@ struct Regions {
   int n_reg = 1;
   int64_t begin[2] = {0, 0}, count[2] = {0, 0};
   int tile[2] = {-1, -1};
-  bool fan = false;  // K2f: 128-object blocks, trees fanned out over the CTA's warps
+  bool fan = false;   // K2f: 128-object blocks, trees fanned out over the CTA's warps
+  bool wide = false;  // K2w: 256-object tiles, persistent warp-specialised CTAs
 };
 
 // K2f for small batches: the 128-object blocks fill no more than two waves, the model
@@ -1118,6 +1275,11 @@ Regions plan_regions(const obt_model* m, int64_t n, bool split_ok) {
   if (split_ok && fan_eligible(m, n)) {
     r.tile[0] = 128;
     r.fan = true;
+    return r;
+  }
+  if (split_ok && wide_eligible(m)) {
+    r.tile[0] = obt::kWideTile;
+    r.wide = true;
     return r;
   }
   r.tile[0] = plan_tile(m, n);
@@ -1248,6 +1410,8 @@ int obt_model_create(const obt_model_desc* d, int device, obt_model** out) {
       m->split_ordinal[(size_t)t * DI + s] = ord == kSentinel ? (uint8_t)kSentinel : (uint8_t)rank[f][ord];
     }
 
+  plan_level_order(m.get(), d);
+
   // leaf bank: binary16 bits, or binary64 stored as fp32 when that is exact
   const size_t per_tree_in = (size_t)1 << D, per_tree = (size_t)1 << DI;
   const int C = d->n_outputs;
@@ -1292,11 +1456,15 @@ int obt_model_create(const obt_model_desc* d, int device, obt_model** out) {
     m->multi_slot = m->multi_slice    ? obt::multi_slice_slot(m->leaf_storage, C)
                     : m->multi_staged ? obt::staged_record_values(C) * (int)ls
                                       : obt::multi_record_values(m->leaf_storage, C) * (int)ls;
+    // records in the predict path's level order (record j' holds reference leaf
+    // reference_leaf(perm, DI, j'); entries past 2^D belong to sentinel levels, never read)
     std::vector<uint8_t> rec((size_t)std::max(m->n_trees, 1) * per_tree * m->multi_slot, 0);
     for (int t = 0; t < m->n_trees; ++t)
       for (int c = 0; c < C; ++c)
-        for (size_t j = 0; j < per_tree_in; ++j) {
-          const double v = d->leaves[(((size_t)t * C + c) << D) + j];
+        for (size_t j = 0; j < per_tree; ++j) {
+          const size_t i = reference_leaf(m->level_perm.data() + (size_t)t * DI, DI, j);
+          if (i >= per_tree_in) continue;
+          const double v = d->leaves[(((size_t)t * C + c) << D) + i];
           uint8_t* dst = rec.data() + ((size_t)t * per_tree + j) * m->multi_slot + (size_t)c * ls;
           if (m->leaf_storage == 0) std::memcpy(dst, &v, 8);
           else { const float f = (float)v; std::memcpy(dst, &f, 4); }
@@ -1430,7 +1598,7 @@ static int predict_impl(obt_model* m, const float* x, int64_t n, int32_t layout,
   uint8_t* qr[2] = {q, q + workspace_bytes(m, reg.count[0], reg.tile[0])};
   uint32_t* flags = reinterpret_cast<uint32_t*>(q + regions_bucket_bytes(m, reg));
   int tpw[2] = {1, 1};
-  for (int i = 0; i < reg.n_reg; ++i) tpw[i] = reg.fan ? 1 : apply_lanes(m, reg.tile[i], idx_out != nullptr);
+  for (int i = 0; i < reg.n_reg; ++i) tpw[i] = (reg.fan || reg.wide) ? 1 : apply_lanes(m, reg.tile[i], idx_out != nullptr);
   if (ev_begin) CUDA_TRY(cudaEventRecord(ev_begin, stream));
   SecondRegion r2;
   int64_t n_slots = ((reg.count[0] + reg.tile[0] - 1) / reg.tile[0]) * (int64_t)reg.tile[0];
@@ -1450,6 +1618,8 @@ static int predict_impl(obt_model* m, const float* x, int64_t n, int32_t layout,
                    : launch_multi(m, qr[i], c, out + b * m->n_outputs, stream);
     } else if (reg.fan) {
       rc = launch_fan(m, qr[i], c, out + b, stream);
+    } else if (reg.wide) {
+      rc = launch_wide(m, qr[i], c, out + b, stream);
     } else {
       rc = launch_apply(m, qr[i], c, reg.tile[i], tpw[i], out ? out + b : nullptr, idx_out, tree_begin, tree_end, stream,
                         i == 0 && reg.n_reg == 1 ? flags : nullptr);

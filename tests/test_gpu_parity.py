@@ -795,3 +795,61 @@ def test_chained_parameter_bank_launches(monkeypatch):
         monkeypatch.setenv("OBT_PDL", pdl)
         got = ev.predict_device(xd).cpu().numpy()
         assert np.array_equal(got, want), (pdl, int(np.count_nonzero(got != want)))
+
+
+# ---------------------------------------------------------------------------
+# K2w (warp-specialised apply for wide feature sets), forced with OBT_WIDE=1 on small
+# models and chosen by default at config 4's shape.
+
+def _wide_cases():
+    for D in (1, 3, 6, 8):
+        for B in (16, 200):          # 7-bit and 8-bit compares (200 used borders -> 8-bit)
+            yield D, B
+
+
+@pytest.mark.parametrize("D,B", list(_wide_cases()))
+@pytest.mark.parametrize("n", [1, 255, 257, 256 * 148 + 77, 256 * 148 * 3 + 5])
+def test_wide_apply_bit_exact(monkeypatch, D, B, n):
+    monkeypatch.setenv("OBT_WIDE", "1")
+    monkeypatch.setenv("OBT_FAN", "0")
+    model = _model(37, B, 53, D, seed=D * 13 + B)
+    x = _features(model, n, seed=n % 1000 + D)
+    fm = oracle.flatten(model)
+    for strategy, prec in ((obt.LeafStrategy.NAIVE, oracle.BINARY64), (obt.LeafStrategy.NAIVE16, oracle.BINARY16)):
+        ev = obt.Evaluator(model, obt.EvalConfig(strategy=strategy), device=0)
+        got = ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
+        assert np.array_equal(got, oracle.evaluate_scalar(fm, x, oracle.OBJECT_MAJOR, prec)), (strategy, D, B, n)
+
+
+def test_wide_apply_mixed_depth_binary64_tables_and_layouts(monkeypatch):
+    monkeypatch.setenv("OBT_WIDE", "1")
+    monkeypatch.setenv("OBT_FAN", "0")
+    model = _mixed_depth_model(29, 60, 141, seed=5)
+    x = _features(model, 40_000, seed=6)
+    want = oracle.evaluate_scalar(oracle.flatten(model), x)
+    ev = obt.Evaluator(model, device=0)
+    assert ev.leaf_storage == "fp64"  # uniform(-1, 1) binary64 leaves are not fp32-exact
+    assert np.array_equal(ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR)), want)
+    assert np.array_equal(ev.predict(obt.FeatureMatrix(np.ascontiguousarray(x.T), obt.Layout.FEATURE_MAJOR)), want)
+    assert np.array_equal(ev.predict_device(torch.from_numpy(x).cuda()).cpu().numpy(), want)
+
+
+def test_wide_apply_zero_trees_and_empty(monkeypatch):
+    monkeypatch.setenv("OBT_WIDE", "1")
+    base = _model(9, 5, 1, 1, seed=2)
+    model = obt.ObliviousModel(base.float_features, (), scale=2.0, bias=-0.75)
+    x = _features(model, 1000, seed=3)
+    ev = obt.Evaluator(model, device=0)
+    assert np.array_equal(ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR)), np.full(1000, -0.75))
+    assert ev.predict(obt.FeatureMatrix(x[:0], obt.Layout.OBJECT_MAJOR)).shape == (0,)
+
+
+def test_wide_apply_is_the_default_at_config4_shape():
+    """Config 4's model (F = 500, 128 borders, depth 8) runs K2w by default; the first
+    60k objects of a config-4 batch equal the oracle bit for bit (60k objects: past the K2f small-batch range)."""
+    spec = synthetic.CONFIGS[4]
+    model = synthetic.build_model(synthetic.WorkloadSpec(**{**spec.__dict__, "n_trees": 512}))
+    x = synthetic.host_features(spec, n_objects=60_000, seed=9)
+    ev = obt.Evaluator(model, device=0)
+    got = ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
+    assert np.array_equal(got, oracle.evaluate_scalar(oracle.flatten(model), x))

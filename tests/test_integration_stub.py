@@ -39,7 +39,6 @@ def _real_obtree():
     if str(REF_PKG) not in sys.path:
         sys.path.insert(0, str(REF_PKG))
     import obtree
-    import obtree.evaluate  # noqa: F401
 
     return obtree
 
@@ -74,7 +73,7 @@ def test_integration_stub_with_the_real_reference_package():
         m = obtree.FeatureMatrix(x if layout is obtree.Layout.OBJECT_MAJOR else np.ascontiguousarray(x.T), layout)
         for strategy in (obtree.LeafStrategy.NAIVE, obtree.LeafStrategy.NAIVE16):
             cfg = obtree.EvalConfig(strategy=strategy)
-            got = ns["GpuEvaluator"](obtree.evaluate.ModelTables(model), cfg).predict(m)
+            got = ns["GpuEvaluator"](importlib.import_module("obtree.evaluate").ModelTables(model), cfg).predict(m)
             want = obtree.Evaluator(model, cfg).predict(m)
             assert np.array_equal(got, want), (layout, strategy)
 
