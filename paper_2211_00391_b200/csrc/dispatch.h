@@ -36,7 +36,10 @@ int multi_slice_slot(int leaf, int c);
 // K2f fanned-out small-batch apply (depths 1..8)
 const void* pick_fan(int di, int cmp, int leaf);
 // K2w warp-specialised apply for wide feature sets (depths 1..8)
-constexpr int kWideIndexWarps = 6;
+#ifndef OBT_WIDE_NIDX
+#define OBT_WIDE_NIDX 8
+#endif
+constexpr int kWideIndexWarps = OBT_WIDE_NIDX;
 const void* pick_wide(int di, int cmp, int leaf);
 // K5 staged multi-output (fp32 records; depths 4/6/8/10, outputs 2..10)
 const void* pick_multi_staged(int di, int cmp, int c, int* di_out);

@@ -98,13 +98,13 @@ struct TilePlan {
   uint32_t tables_chunk_bytes = 0;
 };
 
-// K2w records: per chunk of chunk_trees trees, descriptors (kWideDescBytes(DI) per tree,
-// 256-byte aligned block) then leaf tables (`stride` bytes each), trees in the predict
-// path's level order.
+// K2w records: per chunk of kWideChunkTrees trees, the descriptors (kWideDescBytes(DI)
+// per tree) and, in a second array, the leaf tables (`stride` bytes each), trees in the
+// predict path's level order.
 struct WidePlan {
-  uint8_t* d_chunks = nullptr;
-  int chunk_trees = 0, n_chunks = 0, stages = 0;
-  uint32_t chunk_bytes = 0, desc_bytes = 0, stride = 0;
+  uint8_t* d_desc = nullptr;
+  uint8_t* d_tables = nullptr;
+  int n_chunks = 0, tstages = 0, slots = 0;
   size_t smem = 0;
 };
 
@@ -146,7 +146,8 @@ struct obt_model {
   std::unique_ptr<WidePlan> wide;        // K2w records (built on first use, under mu)
   obt::ApplyArgs<1> param_args;  // launch-parameter staging (32 KB), guarded by mu
   ~obt_model() {
-    if (wide && wide->d_chunks) cudaFree(wide->d_chunks);
+    if (wide && wide->d_desc) cudaFree(wide->d_desc);
+    if (wide && wide->d_tables) cudaFree(wide->d_tables);
     for (auto& kv : plans) {
       cudaFree(kv.second.d_chunks);
       if (kv.second.d_tables) cudaFree(kv.second.d_tables);
@@ -1052,34 +1053,47 @@ int launch_fan(obt_model* m, const uint8_t* q, int64_t n, double* out, cudaStrea
 
 // K2w records for the 256-object tile, in the predict path's level order; null trees
 // (sentinel descriptors, -0.0 leaves) pad the last chunk.
-constexpr int kWideChunkTrees = 16;  // a multiple of the fold warps' 4-tree groups
+using obt::kWideChunkTrees;
+// Shared memory of K2w with ts table stages and ns descriptor/panel slots.
+size_t wide_smem(const obt_model* m, int ts, int ns) {
+  const int DI = m->depth_inst;
+  return obt::kWideSmemSlack + (size_t)ts * obt::wide_tables_bytes(DI, m->leaf_storage) +
+         (size_t)ns * (obt::wide_desc_bytes(DI) + obt::wide_panel_bytes(kWideChunkTrees)) +
+         (((size_t)m->n_features * obt::kWideTile + 15) & ~(size_t)15);
+}
+// Ring depths: 3 table stages (2 if that is all that fits) and as many descriptor /
+// panel slots as fit, up to 12 (the index warps' lead over the fold).
+bool wide_rings(const obt_model* m, int* ts, int* ns) {
+  for (int t = 3; t >= 2; --t) {
+    int n = 12;
+    while (n >= 4 && wide_smem(m, t, n) > (size_t)m->smem_optin) --n;
+    if (n >= 4) { *ts = t; *ns = n; return true; }
+  }
+  return false;
+}
 int build_wide_plan(obt_model* m, WidePlan& w) {
   const int DI = m->depth_inst;
-  const size_t ls = leaf_size(m->leaf_storage), per_tree_leaf = ls << DI;
-  w.stride = (uint32_t)((per_tree_leaf + 15) & ~(size_t)15);
-  w.chunk_trees = std::min(kWideChunkTrees, std::max(4, (m->n_trees + 3) / 4 * 4));
-  w.n_chunks = (m->n_trees + w.chunk_trees - 1) / w.chunk_trees;
-  const uint32_t dpt = obt::kWideDescBytes(DI);
-  w.desc_bytes = (uint32_t)(((size_t)w.chunk_trees * dpt + 255) & ~(size_t)255);
-  w.chunk_bytes = (uint32_t)(((size_t)w.desc_bytes + (size_t)w.chunk_trees * w.stride + 255) & ~(size_t)255);
-  const size_t per_stage = (size_t)w.chunk_bytes + obt::wide_panel_bytes(w.chunk_trees);
-  const size_t fixed = 512 + (size_t)m->n_features * obt::kWideTile;
-  if (fixed + 2 * per_stage > (size_t)m->smem_optin) return OBT_E_UNSUPPORTED;
-  w.stages = (int)std::min<size_t>(obt::kWideMaxStages, std::min<size_t>(4, ((size_t)m->smem_optin - fixed) / per_stage));
-  w.smem = fixed + (size_t)w.stages * per_stage;
-  std::vector<uint8_t> host((size_t)std::max(w.n_chunks, 1) * w.chunk_bytes, 0);
+  const uint32_t stride = obt::wide_table_stride(DI, m->leaf_storage);
+  if (!wide_rings(m, &w.tstages, &w.slots)) return OBT_E_UNSUPPORTED;
+  w.smem = wide_smem(m, w.tstages, w.slots);
+  w.n_chunks = (m->n_trees + kWideChunkTrees - 1) / kWideChunkTrees;
+  const uint32_t dpt = obt::kWideDescBytes(DI), db = obt::wide_desc_bytes(DI);
+  const uint32_t tb = obt::wide_tables_bytes(DI, m->leaf_storage);
+  const size_t nch = (size_t)std::max(w.n_chunks, 1);
+  std::vector<uint8_t> hd(nch * db, 0), ht(nch * tb, 0);
   std::vector<uint32_t> words((size_t)DI * 2);
-  for (int t = 0; t < w.n_chunks * w.chunk_trees; ++t) {
-    const int c = t / w.chunk_trees, tl = t % w.chunk_trees;
-    uint8_t* rec = host.data() + (size_t)c * w.chunk_bytes;
+  for (int t = 0; t < w.n_chunks * kWideChunkTrees; ++t) {
+    const int c = t / kWideChunkTrees, tl = t % kWideChunkTrees;
     tree_descriptors(m, t, obt::kWideTile, words.data(), true);
-    std::memcpy(rec + (size_t)tl * dpt, words.data(), (size_t)DI * 8);
-    uint8_t* leaf_dst = rec + w.desc_bytes + (size_t)tl * w.stride;
+    std::memcpy(hd.data() + (size_t)c * db + (size_t)tl * dpt, words.data(), (size_t)DI * 8);
+    uint8_t* leaf_dst = ht.data() + (size_t)c * tb + (size_t)tl * stride;
     if (t < m->n_trees) ordered_leaves(m, t, leaf_dst);
     else write_null_leaves(m, leaf_dst);
   }
-  CUDA_TRY(cudaMalloc(&w.d_chunks, host.size()));
-  CUDA_TRY(cudaMemcpy(w.d_chunks, host.data(), host.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMalloc(&w.d_desc, hd.size()));
+  CUDA_TRY(cudaMemcpy(w.d_desc, hd.data(), hd.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMalloc(&w.d_tables, ht.size()));
+  CUDA_TRY(cudaMemcpy(w.d_tables, ht.data(), ht.size(), cudaMemcpyHostToDevice));
   return OBT_OK;
 }
 
@@ -1099,9 +1113,8 @@ int get_wide_plan(obt_model* m, const WidePlan** out) {
 // leaves K2 too few warps per SM (config 4, F = 500: 256 objects, 2 warps).
 bool wide_eligible(const obt_model* m) {
   if (m->n_outputs > 1 || m->depth_inst > 8 || m->n_trees == 0) return false;
-  const size_t per_stage = 2 * ((size_t)kWideChunkTrees * (leaf_size(m->leaf_storage) << m->depth_inst) + 2048) +
-                           obt::wide_panel_bytes(kWideChunkTrees);
-  if (512 + (size_t)m->n_features * obt::kWideTile + per_stage > (size_t)m->smem_optin) return false;
+  int ts = 0, ns = 0;
+  if (!wide_rings(m, &ts, &ns)) return false;
   if (!obt::pick_wide(m->depth_inst, m->compare_mode, m->leaf_storage)) return false;
   const char* e = getenv("OBT_WIDE");  // A/B knob: 0 never, 1 wherever it fits
   if (e && !strcmp(e, "0")) return false;
@@ -1117,17 +1130,15 @@ int launch_wide(obt_model* m, const uint8_t* q, int64_t n, double* out, cudaStre
   if (rc != OBT_OK) return rc;
   obt::WideParams p{};
   p.q = q;
-  p.chunks = w->d_chunks;
+  p.desc = w->d_desc;
+  p.tables = w->d_tables;
   p.out = out;
   p.n = n;
   p.n_tiles = (n + obt::kWideTile - 1) / obt::kWideTile;
   p.n_chunks = w->n_chunks;
-  p.chunk_trees = w->chunk_trees;
-  p.chunk_bytes = w->chunk_bytes;
-  p.desc_bytes = w->desc_bytes;
-  p.table_stride = w->stride;
   p.q_tile_bytes = (uint32_t)((size_t)m->n_features * obt::kWideTile);
-  p.n_stages = w->stages;
+  p.n_tstages = w->tstages;
+  p.n_slots = w->slots;
   p.scale = m->scale;
   p.bias = m->bias;
   CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, m->smem_optin));

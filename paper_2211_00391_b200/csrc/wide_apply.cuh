@@ -10,19 +10,21 @@
 //   producer warp   lane 0 streams tree chunks (descriptors + leaf tables) into an
 //                   S-stage ring, lane 1 streams the CTA's bucket tiles (persistent
 //                   CTA: one per SM, looping over tiles)
-//   index warps     NIDX warps share each chunk's trees (tree j -> warp j mod NIDX);
-//                   a lane builds the packed leaf indices of bucket words l and l + 32
-//                   (8 objects, SWAR: per depth one LDS per word, one add carrying
-//                   [q > ordinal] into bit 7 of each byte, one shift-and-or) and
-//                   stores them to the chunk's index panel [tree][64 words]
-//   fold warps      2 warps, lane = bucket word (4 objects): per tree one panel load,
-//                   four leaf gathers and four adds in tree order -- the reference's
-//                   left fold, binary64 (binary32 for the binary16 family) -- then the
-//                   two-rounding finalize
+//   index warps     NIDX warps share each chunk's 4-tree groups; a lane builds the packed
+//                   leaf indices of bucket words l and l + 32 (8 objects, SWAR: per depth
+//                   one LDS per word, one add carrying [q > ordinal] into bit 7 of each
+//                   byte, one shift-and-or) for the group's 4 trees, transposes the 4 x 4
+//                   index bytes of each word (8 PRMT) so that one word holds one object's
+//                   indices of the 4 trees, and stores those words to the chunk's index
+//                   panel [group][object] (32 consecutive words per store: conflict-free)
+//   fold warps      kWideTile / 32 warps, lane = object: per 4-tree group one panel load,
+//                   four leaf gathers and four adds in tree order -- the reference's left
+//                   fold, binary64 (binary32 for the binary16 family) -- then the
+//                   two-rounding finalize and a coalesced store
 //
 // Shared-memory wavefronts per 128 object-trees at depth 8 (the resource that binds
 // this path on B200): 8 bucket words, ~10.5 leaf gathers (4 x ~2.6 with entropy-ordered
-// levels, see obtree_capi.cu level_order), 2 panel stores + loads, 2 descriptor
+// levels, see obtree_capi.cu level_order), 1 panel store + 1 panel load, 2 descriptor
 // broadcasts, ~4 of TMA ring fill (1 KB tables over 256 objects).
 #pragma once
 
@@ -30,24 +32,30 @@
 
 namespace obt {
 
-constexpr int kWideTile = 256;                 // objects per tile (64 bucket words)
+constexpr int kWideTile = 256;                   // objects per tile (64 bucket words)
 constexpr int kWideWords = kWideTile / 4;
-constexpr int kWideFoldWarps = kWideWords / 32;  // one lane per word
-constexpr int kWideMaxStages = 8;
+constexpr int kWideFoldWarps = kWideTile / 32;   // one lane per object
+constexpr int kWideMaxTStages = 8;
+constexpr int kWideMaxSlots = 16;
+constexpr int kWideChunkTrees = 16;              // trees per ring chunk (null trees pad the last)
+constexpr int kWideGroups = kWideChunkTrees / 4;  // 4-tree groups per chunk
+
+// bytes between consecutive leaf tables of a chunk
+__host__ __device__ constexpr uint32_t wide_table_stride(int di, int leaf) {
+  return (((leaf == 0 ? 8u : leaf == 1 ? 4u : 2u) << di) + 15u) & ~15u;
+}
 
 struct WideParams {
   const uint8_t* q;          // tiled buckets [n_tiles][F][kWideTile]
-  const uint8_t* chunks;     // [n_chunks][chunk_bytes]: descriptors (desc_bytes) + leaf tables
+  const uint8_t* desc;       // [n_chunks][wide_desc_bytes]: per tree DI {off, k} pairs
+  const uint8_t* tables;     // [n_chunks][wide_tables_bytes]: leaf tables, kStride apart
   double* out;               // [n]
   int64_t n;
   int64_t n_tiles;
   int32_t n_chunks;
-  int32_t chunk_trees;       // trees per chunk (the last chunk is padded with null trees)
-  uint32_t chunk_bytes;      // multiple of 256
-  uint32_t desc_bytes;       // descriptor part of a chunk (multiple of 256)
-  uint32_t table_stride;     // bytes between consecutive leaf tables
   uint32_t q_tile_bytes;     // F * kWideTile
-  int32_t n_stages;          // <= kWideMaxStages
+  int32_t n_tstages;         // table ring stages (<= kWideMaxTStages)
+  int32_t n_slots;           // descriptor + index-panel ring slots (<= kWideMaxSlots)
   double scale, bias;
 };
 
@@ -57,39 +65,79 @@ __device__ __forceinline__ void wide_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
-// Shared-memory layout (after the 256-byte aligned base):
-//   [0, 256)             barriers: full[S], idx_done[S], empty[S], tile_full, tile_free
-//   stages               S x chunk_bytes
-//   panels               S x chunk_trees x kWideWords x 4 bytes
-//   tile                 q_tile_bytes
-__host__ __device__ constexpr size_t wide_panel_bytes(int chunk_trees) { return (size_t)chunk_trees * kWideWords * 4; }
+// Shared-memory layout (2048-byte aligned base):
+//   table ring           TS x kWideChunkTrees tables (each stride-aligned, so a gather
+//                        address is one LOP3: (shifted index & mask) | table base, plus
+//                        the tree's compile-time offset)
+//   descriptor ring      NS x wide_desc_bytes
+//   index-panel ring     NS x kWideGroups x kWideTile x 4 bytes
+//   bucket tile          q_tile_bytes
+//   barriers
+// The descriptor / panel ring is deeper than the table ring: the index warps run up to
+// NS chunks ahead of the fold, so neither side waits on the other's latency.
+__host__ __device__ constexpr size_t wide_panel_bytes(int chunk_trees) { return (size_t)chunk_trees * kWideTile; }
 // descriptor bytes per tree: DI pairs of words, rounded to whole 16-byte loads
 __host__ __device__ constexpr uint32_t kWideDescBytes(int di) { return (uint32_t)((di + 1) / 2) * 16u; }
+__host__ __device__ constexpr uint32_t wide_desc_bytes(int di) { return (kWideChunkTrees * kWideDescBytes(di) + 127u) & ~127u; }
+__host__ __device__ constexpr uint32_t wide_tables_bytes(int di, int leaf) { return kWideChunkTrees * wide_table_stride(di, leaf); }
+constexpr uint32_t kWideSmemAlign = 2048;  // the largest table stride (binary64, depth 8)
+constexpr uint32_t kWideSmemSlack = kWideSmemAlign + 16 + 8 * (2 * kWideMaxTStages + 3 * kWideMaxSlots + 2);
+
+// 4 x 4 byte transpose: out[k] byte j = in[j] byte k.
+__device__ __forceinline__ void transpose4x4(const uint32_t (&in)[4], uint32_t (&out)[4]) {
+  const uint32_t ab_lo = __byte_perm(in[0], in[1], 0x5140u);  // a0 b0 a1 b1
+  const uint32_t ab_hi = __byte_perm(in[0], in[1], 0x7362u);  // a2 b2 a3 b3
+  const uint32_t cd_lo = __byte_perm(in[2], in[3], 0x5140u);  // c0 d0 c1 d1
+  const uint32_t cd_hi = __byte_perm(in[2], in[3], 0x7362u);  // c2 d2 c3 d3
+  out[0] = __byte_perm(ab_lo, cd_lo, 0x5410u);                // a0 b0 c0 d0
+  out[1] = __byte_perm(ab_lo, cd_lo, 0x7632u);                // a1 b1 c1 d1
+  out[2] = __byte_perm(ab_hi, cd_hi, 0x5410u);
+  out[3] = __byte_perm(ab_hi, cd_hi, 0x7632u);
+}
+
+// Ring position: slot and phase parity, advanced without divisions.
+struct RingPos {
+  int slot = 0;
+  uint32_t phase = 0;
+  __device__ __forceinline__ void next(int n) {
+    if (++slot == n) { slot = 0; phase ^= 1u; }
+  }
+};
 
 template <int DI, int CMP, int LEAF, int NIDX>
 __global__ void __launch_bounds__(32 * (1 + NIDX + kWideFoldWarps), 1) apply_wide_kernel(const __grid_constant__ WideParams p) {
   static_assert(DI >= 1 && DI <= 8, "K2w: one index byte per object");
   using LT = LeafT<LEAF>;
   using acc_t = typename LT::Acc;
+  constexpr uint32_t kTablesBytes = wide_tables_bytes(DI, LEAF), kDescBytes = wide_desc_bytes(DI);
+  constexpr uint32_t kPanelBytes = (uint32_t)wide_panel_bytes(kWideChunkTrees);
+  constexpr uint32_t kStride = wide_table_stride(DI, LEAF);
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  unsigned char* smem = smem_raw + ((256u - (smem_u32(smem_raw) & 255u)) & 255u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* idx_done = full + kWideMaxStages;
-  uint64_t* empty = idx_done + kWideMaxStages;
-  uint64_t* tile_full = empty + kWideMaxStages;
+  unsigned char* smem = smem_raw + ((kWideSmemAlign - (smem_u32(smem_raw) & (kWideSmemAlign - 1u))) & (kWideSmemAlign - 1u));
+  const int TS = p.n_tstages, NS = p.n_slots;
+  unsigned char* tstages = smem;                                      // TS x kTablesBytes (stride-aligned)
+  unsigned char* descs = tstages + (size_t)TS * kTablesBytes;         // NS x kDescBytes
+  unsigned char* panels = descs + (size_t)NS * kDescBytes;            // NS x kPanelBytes
+  unsigned char* qtile = panels + (size_t)NS * kPanelBytes;           // q_tile_bytes
+  uint64_t* bars = reinterpret_cast<uint64_t*>(qtile + ((p.q_tile_bytes + 15u) & ~15u));
+  uint64_t* tfull = bars;                          // [TS] tables landed
+  uint64_t* tfree = tfull + kWideMaxTStages;       // [TS] fold done with the tables
+  uint64_t* dfull = tfree + kWideMaxTStages;       // [NS] descriptors landed (slot free)
+  uint64_t* pfull = dfull + kWideMaxSlots;         // [NS] index panel written
+  uint64_t* sfree = pfull + kWideMaxSlots;         // [NS] fold done with the panel
+  uint64_t* tile_full = sfree + kWideMaxSlots;
   uint64_t* tile_free = tile_full + 1;
-  const int S = p.n_stages;
-  unsigned char* stages = smem + 256;
-  unsigned char* panels = stages + (size_t)S * p.chunk_bytes;
-  const size_t panel_bytes = wide_panel_bytes(p.chunk_trees);
-  unsigned char* qtile = panels + (size_t)S * panel_bytes;
 
   const int tid = threadIdx.x;
   if (tid == 0) {
-    for (int i = 0; i < S; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&idx_done[i], NIDX * 32);
-      mbar_init(&empty[i], kWideFoldWarps * 32);
+    for (int i = 0; i < TS; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tfree[i], kWideFoldWarps * 32);
+    }
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&dfull[i], 1);
+      mbar_init(&pfull[i], NIDX * 32);
+      mbar_init(&sfree[i], kWideFoldWarps * 32);
     }
     mbar_init(tile_full, 1);
     mbar_init(tile_free, NIDX * 32);
@@ -104,15 +152,15 @@ __global__ void __launch_bounds__(32 * (1 + NIDX + kWideFoldWarps), 1) apply_wid
 
   if (warp == 0) {
     if (lane == 0) {
-      // tree chunks, continuously across this CTA's tiles
+      // descriptors, NS chunks ahead of the fold: index warps run ahead of the fold by
+      // up to NS chunks, decoupled from the (larger) table ring
+      RingPos r;
       for (int64_t i = 0; i < n_my_tiles; ++i) {
         for (int c = 0; c < nc; ++c) {
-          const int64_t seq = i * nc + c;
-          const int s = (int)(seq % S);
-          if (seq >= S) mbar_wait(&empty[s], (uint32_t)((seq / S - 1) & 1));
-          mbar_expect_tx(&full[s], p.chunk_bytes);
-          bulk_g2s_split(stages + (size_t)s * p.chunk_bytes, p.chunks + (size_t)c * p.chunk_bytes, p.chunk_bytes,
-                         &full[s]);
+          if (i > 0 || c >= NS) mbar_wait(&sfree[r.slot], r.phase ^ 1u);
+          mbar_expect_tx(&dfull[r.slot], kDescBytes);
+          bulk_g2s(descs + (size_t)r.slot * kDescBytes, p.desc + (size_t)c * kDescBytes, kDescBytes, &dfull[r.slot]);
+          r.next(NS);
         }
       }
     } else if (lane == 1) {
@@ -124,6 +172,18 @@ __global__ void __launch_bounds__(32 * (1 + NIDX + kWideFoldWarps), 1) apply_wid
         bulk_g2s_split(qtile, p.q + tile * (int64_t)p.q_tile_bytes, p.q_tile_bytes, tile_full);
         if (i + 1 < n_my_tiles) bulk_prefetch_l2(p.q + (tile + gridDim.x) * (int64_t)p.q_tile_bytes, p.q_tile_bytes);
       }
+    } else if (lane == 2) {
+      // leaf tables, TS chunks ahead of the fold
+      RingPos r;
+      for (int64_t i = 0; i < n_my_tiles; ++i) {
+        for (int c = 0; c < nc; ++c) {
+          if (i > 0 || c >= TS) mbar_wait(&tfree[r.slot], r.phase ^ 1u);
+          mbar_expect_tx(&tfull[r.slot], kTablesBytes);
+          bulk_g2s_split(tstages + (size_t)r.slot * kTablesBytes, p.tables + (size_t)c * kTablesBytes, kTablesBytes,
+                         &tfull[r.slot]);
+          r.next(TS);
+        }
+      }
     }
     return;
   }
@@ -131,112 +191,119 @@ __global__ void __launch_bounds__(32 * (1 + NIDX + kWideFoldWarps), 1) apply_wid
   if (warp <= NIDX) {
     // ---------------- index warps
     const int iw = warp - 1;
-    const uint32_t q0 = smem_u32(qtile) + 4u * lane;  // bucket word `lane` of every row; + 128: word lane + 32
+    // lane l owns bucket words 2l and 2l + 1 (one LDS.64 per depth): objects
+    // blk * 128 + p + 32k and blk * 128 + p + 1 + 32k, blk = l / 16, p = 2l mod 32
+    const uint32_t q0 = smem_u32(qtile) + 8u * lane;
+    const int obj0 = (lane >> 4) * 128 + ((2 * lane) & 31);
+    int rr = iw;  // round-robin position of this warp's next group across chunks
+    RingPos r;
     for (int64_t i = 0; i < n_my_tiles; ++i) {
       wide_wait(tile_full, (uint32_t)(i & 1));
       for (int c = 0; c < nc; ++c) {
-        const int64_t seq = i * nc + c;
-        const int s = (int)(seq % S);
-        wide_wait(&full[s], (uint32_t)((seq / S) & 1));
-        const unsigned char* st = stages + (size_t)s * p.chunk_bytes;
-        uint32_t* panel = reinterpret_cast<uint32_t*>(panels + (size_t)s * panel_bytes);
-        for (int t = iw; t < p.chunk_trees; t += NIDX) {
-          // descriptors: DI pairs {off, k replicated} (7-bit) or {(off << 8) | k, s} (8-bit),
-          // two pairs per broadcast LDS.128
-          uint32_t dw[2 * DI + 2];
-          const uint4* dsrc = reinterpret_cast<const uint4*>(st + (size_t)t * kWideDescBytes(DI));
+        wide_wait(&dfull[r.slot], r.phase);
+        const unsigned char* st = descs + (size_t)r.slot * kDescBytes;
+        const uint32_t panel = smem_u32(panels + (size_t)r.slot * kPanelBytes) + 4u * obj0;
+        for (; rr < kWideGroups; rr += NIDX) {
+          const int g = rr;
+          uint32_t i0[4], i1[4];  // packed indices of trees 4g..4g+3, words 2l and 2l + 1
 #pragma unroll
-          for (int v = 0; v < (DI + 1) / 2; ++v) {
-            const uint4 q4 = dsrc[v];
-            dw[4 * v + 0] = q4.x; dw[4 * v + 1] = q4.y; dw[4 * v + 2] = q4.z; dw[4 * v + 3] = q4.w;
-          }
-          uint32_t w0[DI], w1[DI];
+          for (int j = 0; j < 4; ++j) {
+            const int t = 4 * g + j;
+            // descriptors: DI pairs {off, k replicated} (7-bit) or {(off << 8) | k, s}
+            // (8-bit), two pairs per broadcast LDS.128
+            uint32_t dw[2 * DI + 2];
+            const uint4* dsrc = reinterpret_cast<const uint4*>(st + (size_t)t * kWideDescBytes(DI));
 #pragma unroll
-          for (int d = 0; d < DI; ++d) {
-            const uint32_t off = CMP == 7 ? dw[2 * d] : (dw[2 * d] >> 8);
-            w0[d] = lds_u32<false>(q0 + off);
-            w1[d] = lds_u32<false>(q0 + off + 128u);
-          }
-          uint32_t i0 = 0, i1 = 0;
-#pragma unroll
-          for (int d = 0; d < DI; ++d) {
-            uint32_t b0, b1;
-            if constexpr (CMP == 7) {
-              b0 = w0[d] + dw[2 * d + 1];
-              b1 = w1[d] + dw[2 * d + 1];
-            } else {
-              const uint32_t k = __byte_perm(dw[2 * d], 0u, 0x0000u) & 0x7f7f7f7fu;
-              b0 = maj3((w0[d] & 0x7f7f7f7fu) + k, w0[d], dw[2 * d + 1]);
-              b1 = maj3((w1[d] & 0x7f7f7f7fu) + k, w1[d], dw[2 * d + 1]);
+            for (int v = 0; v < (DI + 1) / 2; ++v) {
+              const uint4 q4 = dsrc[v];
+              dw[4 * v + 0] = q4.x; dw[4 * v + 1] = q4.y; dw[4 * v + 2] = q4.z; dw[4 * v + 3] = q4.w;
             }
-            const uint32_t mask = 0x01010101u << d;
-            i0 |= (d == 7 ? b0 : (b0 >> (7 - d))) & mask;
-            i1 |= (d == 7 ? b1 : (b1 >> (7 - d))) & mask;
+            uint32_t w0[DI], w1[DI];
+#pragma unroll
+            for (int d = 0; d < DI; ++d) {
+              const uint32_t off = CMP == 7 ? dw[2 * d] : (dw[2 * d] >> 8);
+              asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w0[d]), "=r"(w1[d]) : "r"(q0 + off));
+            }
+            // LSB-first: acc = (acc >> 1) | (bit 7 of each byte of b); after DI steps depth
+            // d sits at bit 8 - DI + d of each byte (no bit crosses a byte: a bit reaches
+            // position 0 only at the last step of a depth-8 tree)
+            uint32_t a0 = 0, a1 = 0;
+#pragma unroll
+            for (int d = 0; d < DI; ++d) {
+              uint32_t b0, b1;
+              if constexpr (CMP == 7) {
+                b0 = w0[d] + dw[2 * d + 1];
+                b1 = w1[d] + dw[2 * d + 1];
+              } else {
+                const uint32_t k = __byte_perm(dw[2 * d], 0u, 0x0000u) & 0x7f7f7f7fu;
+                b0 = maj3((w0[d] & 0x7f7f7f7fu) + k, w0[d], dw[2 * d + 1]);
+                b1 = maj3((w1[d] & 0x7f7f7f7fu) + k, w1[d], dw[2 * d + 1]);
+              }
+              a0 = (a0 >> 1) | (b0 & 0x80808080u);
+              a1 = (a1 >> 1) | (b1 & 0x80808080u);
+            }
+            if constexpr (DI < 8) {
+              a0 >>= 8 - DI;
+              a1 >>= 8 - DI;
+            }
+            i0[j] = a0;
+            i1[j] = a1;
           }
-          panel[t * kWideWords + lane] = i0;
-          panel[t * kWideWords + 32 + lane] = i1;
+          uint32_t o0[4], o1[4];
+          transpose4x4(i0, o0);
+          transpose4x4(i1, o1);
+          // objects obj0 + 32k and obj0 + 1 + 32k are adjacent panel words: one STS.64
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(panel + (uint32_t)g * (kWideTile * 4) + 128u * k),
+                         "r"(o0[k]), "r"(o1[k]) : "memory");
         }
-        mbar_arrive(&idx_done[s]);
+        rr -= kWideGroups;
+        mbar_arrive(&pfull[r.slot]);
+        r.next(NS);
       }
       mbar_arrive(tile_free);
     }
     return;
   }
 
-  // ---------------- fold warps: lane = bucket word fw * 32 + lane
+  // ---------------- fold warps: lane = object fw * 32 + lane of the tile
   const int fw = warp - 1 - NIDX;
-  const int wi = fw * 32 + lane;
+  const int ol = fw * 32 + lane;
+  RingPos r, rt;
   for (int64_t i = 0; i < n_my_tiles; ++i) {
     const int64_t tile = blockIdx.x + i * gridDim.x;
-    const int64_t tile_base = tile * kWideTile;
-    acc_t acc[4] = {(acc_t)0, (acc_t)0, (acc_t)0, (acc_t)0};
+    acc_t acc = (acc_t)0;
     for (int c = 0; c < nc; ++c) {
-      const int64_t seq = i * nc + c;
-      const int s = (int)(seq % S);
-      wide_wait(&idx_done[s], (uint32_t)((seq / S) & 1));
-      wide_wait(&full[s], (uint32_t)((seq / S) & 1));  // (already complete: makes the TMA writes visible here)
-      const uint32_t panel = smem_u32(panels + (size_t)s * panel_bytes) + 4u * wi;
-      const uint32_t tables = smem_u32(stages + (size_t)s * p.chunk_bytes + p.desc_bytes);
-      // groups of 4 trees, software-pipelined: the panel words of group g + 1 are
-      // requested before group g's 16 gathers, whose adds then run in tree order
-      uint32_t nxt[4];
+      wide_wait(&pfull[r.slot], r.phase);
+      wide_wait(&tfull[rt.slot], rt.phase);
+      const uint32_t panel = smem_u32(panels + (size_t)r.slot * kPanelBytes) + 4u * ol;
+      const uint32_t tables = smem_u32(tstages + (size_t)rt.slot * kTablesBytes);  // kStride-aligned
+      // the chunk's panel words, then its 4 x kWideGroups gathers (gather address: one
+      // LOP3 of the shifted index byte into the aligned table base, plus the tree's
+      // compile-time offset), then the adds in tree order
+      uint32_t iwd[kWideGroups];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) nxt[j] = lds_u32<true>(panel + (uint32_t)j * (kWideWords * 4));
-      for (int t0 = 0; t0 < p.chunk_trees; t0 += 4) {
-        uint32_t iw[4];
+      for (int g = 0; g < kWideGroups; ++g) iwd[g] = lds_u32<false>(panel + (uint32_t)g * (kWideTile * 4));
+      typename LT::T v[kWideGroups][4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) iw[j] = nxt[j];
-        if (t0 + 4 < p.chunk_trees) {
+      for (int g = 0; g < kWideGroups; ++g)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) nxt[j] = lds_u32<true>(panel + (uint32_t)(t0 + 4 + j) * (kWideWords * 4));
-        }
-        typename LT::T v[4][4];
+        for (int j = 0; j < 4; ++j)
+          v[g][j] = lds_leaf<LEAF, false>((((iwd[g] >> (8 * j)) << LT::kShift) & (0xffu << LT::kShift) | tables) +
+                                          (uint32_t)(4 * g + j) * kStride);
+      mbar_arrive(&sfree[r.slot]);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint32_t tab = tables + (uint32_t)(t0 + j) * p.table_stride;
+      for (int g = 0; g < kWideGroups; ++g)
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            v[j][k] = lds_leaf<LEAF, true>(tab + (((iw[j] >> (8 * k)) & 0xffu) << LT::kShift));
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if constexpr (LEAF == 2 && OBT_FADD2) {
-            fadd2(acc[0], acc[1], LT::widen(v[j][0]), LT::widen(v[j][1]));
-            fadd2(acc[2], acc[3], LT::widen(v[j][2]), LT::widen(v[j][3]));
-          } else {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) acc[k] += LT::widen(v[j][k]);
-          }
-        }
-      }
-      mbar_arrive(&empty[s]);
+        for (int j = 0; j < 4; ++j) acc += LT::widen(v[g][j]);
+      mbar_arrive(&tfree[rt.slot]);
+      r.next(NS);
+      rt.next(TS);
     }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int64_t o = word_object(tile_base, wi, k);
-      // finalize: f64(acc) * scale + bias, two roundings (evaluate.py:298-299)
-      if (o < p.n) p.out[o] = __dadd_rn(__dmul_rn((double)acc[k], p.scale), p.bias);
-    }
+    const int64_t o = tile * kWideTile + ol;
+    // finalize: f64(acc) * scale + bias, two roundings (evaluate.py:298-299)
+    if (o < p.n) p.out[o] = __dadd_rn(__dmul_rn((double)acc, p.scale), p.bias);
   }
 }
 

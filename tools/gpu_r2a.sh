@@ -1,0 +1,7 @@
+mkdir -p gpurun_out/r2a
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/r2a/smi.txt
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/r2a/pytest.log 2>&1; echo "pytest rc=$?"
+tail -30 gpurun_out/r2a/pytest.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2a/smoke.log 2>&1; echo "smoke rc=$?"; tail -3 gpurun_out/r2a/smoke.log
+timeout 1500 python bench.py > gpurun_out/r2a/bench_default.json 2> gpurun_out/r2a/bench_default.err; echo "bench rc=$?"
+tail -c 3000 gpurun_out/r2a/bench_default.json; tail -20 gpurun_out/r2a/bench_default.err
