@@ -59,9 +59,10 @@ struct WideParams {
   double scale, bias;
 };
 
-// Warp-wide wait with a suspend hint: waiting warps leave the issue slots to the others.
+// Warp-wide wait on the plain (potentially blocking) try_wait.  A suspend-time hint
+// (TRYWAIT / NANOSLEEP.SYNCS / PHASECHK loop) measured slower at config 4: 48.9 vs 48.2 ms.
 __device__ __forceinline__ void wide_wait(uint64_t* bar, uint32_t parity) {
-  while (!__all_sync(0xffffffffu, mbar_try_suspend(bar, parity, 20000u))) {
+  while (!__all_sync(0xffffffffu, mbar_try(bar, parity))) {
   }
 }
 
