@@ -7,6 +7,9 @@
 //           (s + lane) % 4 (row 3, the padding, predicated off), four LDS.128 per record
 //   MODE 2: 256-entry fp32 table, one LDS.32 per lane (the single-output fold), uniform
 //   MODE 3: 64-byte slots, plain order (rows 0..2), three LDS.128
+//   MODE 5: as MODE 4, rows 0-1 LDS.128 and row 2 LDS.64 (only the 40 bytes of C = 10)
+//   MODE 4: 48-byte records, indices of a depth-10 oblivious tree with random splits:
+//           bit d set with probability p_d, p_d uniform per "tree" (shared by the warp)
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/microbench_gather tools/microbench_gather.cu
 #include <cstdint>
 #include <cstdio>
@@ -56,6 +59,28 @@ __global__ void __launch_bounds__(512, 1) k_gather(int n_instr_out) {
             acc0 += v.x; acc1 += v.y; acc2 += v.z; acc3 += v.w;
           }
         }
+      } else if constexpr (MODE == 4 || MODE == 5) {
+        // per-tree level biases (warp-uniform), per-lane bits
+        uint32_t tr = mix((uint32_t)(it * 4 + u) * 2654435761u + blockIdx.x);
+        uint32_t id = 0;
+#pragma unroll
+        for (int d = 0; d < 10; ++d) {
+          tr = tr * 1664525u + 1013904223u;
+          const uint32_t pd = tr >> 22;         // bias in 1/1024 units
+          h = h * 1664525u + 1013904223u;
+          id |= ((h >> 22) < pd ? 1u : 0u) << d;
+        }
+        const uint32_t rec = base + id * 48u;
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          if (MODE == 5 && r == 2) {
+            asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(rec + 16u * r));
+            acc0 += v.x; acc1 += v.y;
+          } else {
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(rec + 16u * r));
+            acc0 += v.x; acc1 += v.y; acc2 += v.z; acc3 += v.w;
+          }
+        }
       } else if constexpr (MODE == 2) {
         const uint32_t a = base + (idx & 255u) * 4u;
         float x;
@@ -101,5 +126,7 @@ int main() {
   run<1>("64-B slots, rotated rows, 4 x LDS.128 (3 active)", sms, 4);
   run<3>("64-B slots, plain rows, 3 x LDS.128", sms, 3);
   run<2>("256 x fp32 table, LDS.32", sms, 1);
+  run<4>("48-B records, depth-10 random-split indices", sms, 3);
+  run<5>("  same, third row as LDS.64 (40 bytes)", sms, 3);
   return 0;
 }
