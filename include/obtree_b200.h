@@ -95,9 +95,27 @@ int obt_model_info(const obt_model* model, int32_t* n_features, int32_t* n_trees
 int obt_model_quantize_kernel(const obt_model* model, int32_t* kind, int32_t* param);
 
 /* Which multi-output apply kernel a model with n_outputs > 1 runs: 0 = K4 (records
- * gathered from L2), 1 = K4s (sliced records), 2 = K5 (tables and bucket rows staged in
- * shared memory); -1 for single-output models.  Diagnostics, like the above. */
+ * gathered from L2), 2 = K5 (tables and bucket rows staged in shared memory); -1 for
+ * single-output models.  Diagnostics, like the above. */
 int obt_model_multi_kernel(const obt_model* model, int32_t* kind);
+
+/* Path options: force one of the planner's automatic choices, process-wide, so parity
+ * tests can cover every kernel path and A/B runs can compare them.  value -1 restores the
+ * automatic choice (the default; production callers never set these).  Names:
+ *   "desc_source"  0 shared-memory ring, 1 kernel-parameter bank (K2 descriptors)
+ *   "tpw"          lanes per bucket word in K2 / K2s (1, 2, 4)
+ *   "wide"         0 / 1 forbid / force K2w (where it fits)
+ *   "fan"          0 / 1 forbid / force K2f (small batches)
+ *   "pdl"          0: no chained (programmatic dependent) parameter-bank launches
+ *   "tail_split"   0 / 1 forbid / force the tail-wave region
+ *   "quant_lut"    0 / 1 Eytzinger (K1t) / cell-table (K1L) quantize
+ *   "lut_cells"    256, 512, 1024 cells per feature table (read by obt_model_create)
+ *   "leaf_storage" 0: binary64 tables even when binary32 is exact (obt_model_create)
+ *   "multi_staged" 0 / 1 K4 / K5 for multi-output models (obt_model_create)
+ * Not synchronised with concurrent predict calls: set them between calls.  No
+ * reference counterpart (the reference has one CPU path). */
+int obt_set_path_option(const char* name, int value);
+int obt_get_path_option(const char* name, int* value);
 
 /* Bytes of scratch obt_predict_dev needs for n objects (the blocked bucket matrix). */
 int obt_workspace_size(const obt_model* model, int64_t n_objects, size_t* bytes);

@@ -48,7 +48,13 @@ EXPORTED_SYMBOLS = (
     "obt_last_launch_count",
     "obt_last_error",
     "obt_abi_version",
+    "obt_set_path_option",
+    "obt_get_path_option",
 )
+
+# Planner choices a caller may force (obt_set_path_option; -1 = automatic).
+PATH_OPTIONS = ("desc_source", "tpw", "wide", "fan", "pdl", "tail_split", "quant_lut", "lut_cells",
+                "leaf_storage", "multi_staged")
 
 
 class NativeUnavailable(RuntimeError):
@@ -122,6 +128,8 @@ def load_library() -> ctypes.CDLL:
         "obt_last_launch_count": (ctypes.c_int, []),
         "obt_last_error": (ctypes.c_char_p, []),
         "obt_abi_version": (ctypes.c_int, []),
+        "obt_set_path_option": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int]),
+        "obt_get_path_option": (ctypes.c_int, [ctypes.c_char_p, p_i32]),
     }
     for name, (restype, argtypes) in sig.items():
         fn = getattr(lib, name)
@@ -146,6 +154,37 @@ def require_gpu() -> ctypes.CDLL:
     if not torch.cuda.is_available():
         raise NativeUnavailable("no CUDA device is visible; the B200 kernels have no CPU fallback")
     return lib
+
+
+def set_path_option(name: str, value: int) -> None:
+    """Force one planner choice process-wide (see include/obtree_b200.h); -1 = automatic."""
+    check(load_library().obt_set_path_option(name.encode(), int(value)))
+
+
+def get_path_option(name: str) -> int:
+    v = ctypes.c_int32()
+    check(load_library().obt_get_path_option(name.encode(), ctypes.byref(v)))
+    return int(v.value)
+
+
+class path_options:
+    """Context manager forcing planner choices for the duration of a block, then
+    restoring the previous values: ``with path_options(wide=1, fan=0): ...``."""
+
+    def __init__(self, **opts):
+        self.opts = opts
+        self.saved = {}
+
+    def __enter__(self):
+        for k, v in self.opts.items():
+            self.saved[k] = get_path_option(k)
+            set_path_option(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k, v in self.saved.items():
+            set_path_option(k, v)
+        return False
 
 
 class Event:

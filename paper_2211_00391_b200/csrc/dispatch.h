@@ -30,9 +30,6 @@ ApplyKernel pick_split(int di, int cmp, int leaf, int tpw);
 // capacity it was instantiated for through *di_out / *c_out
 const void* pick_multi(int di, int cmp, int leaf, int c, int* di_out);
 int multi_depth(int d);
-// K4s sliced multi-output (same depths / outputs); record slot bytes for leaf storage
-const void* pick_multi_slice(int di, int cmp, int leaf, int c, int* di_out);
-int multi_slice_slot(int leaf, int c);
 // K2f fanned-out small-batch apply (depths 1..8)
 const void* pick_fan(int di, int cmp, int leaf);
 // K2w warp-specialised apply for wide feature sets (depths 1..8)

@@ -1,40 +1,18 @@
 // k_apply_lo.cu -- instantiations of K2 (apply_kernel) for depths {1, 2, 3, 4, 5}.
-#include <cstdlib>
-
 #include "dispatch.h"
 
 namespace obt {
 
-// bucket words (4 objects each) per apply thread: 1, or 2 (8 objects per thread: half
-// the threads, each with twice the independent work); OBT_WORDS_PER_THREAD overrides
-static int words_per_thread() {
-  static const int w = [] {
-    const char* e = getenv("OBT_WORDS_PER_THREAD");
-    return (e && atoi(e) == 2) ? 2 : 1;
-  }();
-  return w;
-}
-
-template <int DI, int CMP, int DSRC, int W>
-static ApplyKernel apply_leaf_w(int leaf, bool write_idx) {
-  ApplyKernel k;
-  k.dsrc = DSRC;
-  k.words = W;
-  if (write_idx) k.fn = (const void*)apply_kernel<DI, CMP, 1, true, W, DSRC>;
-  else if (leaf == 0) k.fn = (const void*)apply_kernel<DI, CMP, 0, false, W, DSRC>;
-  else if (leaf == 1) k.fn = (const void*)apply_kernel<DI, CMP, 1, false, W, DSRC>;
-  else k.fn = (const void*)apply_kernel<DI, CMP, 2, false, W, DSRC>;
-  return k;
-}
-
 template <int DI, int CMP, int DSRC>
 static ApplyKernel apply_leaf(int leaf, bool write_idx) {
-  if constexpr (DSRC == 1) {
-    return apply_leaf_w<DI, CMP, 1, 1>(leaf, write_idx);
-  } else {
-    return words_per_thread() == 2 && !write_idx ? apply_leaf_w<DI, CMP, DSRC, 2>(leaf, write_idx)
-                                                 : apply_leaf_w<DI, CMP, DSRC, 1>(leaf, write_idx);
-  }
+  ApplyKernel k;
+  k.dsrc = DSRC;
+  k.words = 1;
+  if (write_idx) k.fn = (const void*)apply_kernel<DI, CMP, 1, true, 1, DSRC>;
+  else if (leaf == 0) k.fn = (const void*)apply_kernel<DI, CMP, 0, false, 1, DSRC>;
+  else if (leaf == 1) k.fn = (const void*)apply_kernel<DI, CMP, 1, false, 1, DSRC>;
+  else k.fn = (const void*)apply_kernel<DI, CMP, 2, false, 1, DSRC>;
+  return k;
 }
 
 template <int DI>

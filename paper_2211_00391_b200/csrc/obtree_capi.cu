@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -36,6 +37,28 @@ namespace {
 
 thread_local std::string g_error;
 thread_local int g_launches = 0;
+
+// Path options (obt_set_path_option): each forces one automatic choice of the dispatch,
+// for parity tests that cover every kernel path and for A/B measurements.  -1 (the
+// default) leaves the choice to the planner; production callers never set them.
+enum PathOption {
+  OPT_DESC_SOURCE,   // 0: descriptors from the shared-memory ring, 1: kernel-parameter bank
+  OPT_TPW,           // lanes per bucket word in K2 / K2s: 1, 2 or 4
+  OPT_WIDE,          // 0 / 1: forbid / force K2w (where it fits)
+  OPT_FAN,           // 0 / 1: forbid / force K2f (small batches)
+  OPT_PDL,           // 0: no chained (programmatic dependent) parameter-bank launches
+  OPT_TAIL_SPLIT,    // 0 / 1: forbid / force the tail-wave region
+  OPT_QUANT_LUT,     // 0 / 1: Eytzinger (K1t) / cell-table (K1L) quantize
+  OPT_LUT_CELLS,     // 256, 512 or 1024 cells per feature table (read at model creation)
+  OPT_LEAF_STORAGE,  // 0: binary64 leaf tables even when binary32 is exact (model creation)
+  OPT_MULTI_STAGED,  // 0 / 1: K4 / K5 for multi-output models (model creation)
+  OPT_COUNT
+};
+const char* const kPathOptionNames[OPT_COUNT] = {"desc_source", "tpw", "wide", "fan", "pdl",
+                                                 "tail_split", "quant_lut", "lut_cells", "leaf_storage",
+                                                 "multi_staged"};
+std::atomic<int> g_opt[OPT_COUNT] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
+int opt(PathOption o) { return g_opt[o].load(std::memory_order_relaxed); }
 
 
 int fail(int code, const char* fmt, ...) {
@@ -121,7 +144,6 @@ struct obt_model {
   BorderTable used;          // borders referenced by splits: the predict path
   LutTable used_lut;         // cell tables of `used` (K1L), kmax 0 if not applicable
   void* d_multi_leaves = nullptr;   // multi-output records [T][2^DI][CP] (K4) or [T][2^DI] slots (K4s)
-  int multi_slice = 0;              // 1: sliced kernel K4s with multi_slot-byte record slots
   int multi_staged = 0;             // 1: K5 (tree tables + bucket rows staged in shared memory)
   int staged_stages = 0;
   uint32_t staged_table_bytes = 0, staged_stage_bytes = 0;
@@ -319,8 +341,7 @@ int build_lut_table(const float* borders, const int32_t* counts, int F, int stri
   out.kmax = 0;
   out.cells = 256;
   int k = plan_lut_table(borders, counts, F, stride, 256, lut, rec, rs);
-  const char* e = getenv("OBT_LUT_CELLS");  // tuning override: 256, 512 or 1024
-  const int forced = e ? atoi(e) : 0;
+  const int forced = std::max(0, opt(OPT_LUT_CELLS));
   const int big = (forced == 512 || forced == 1024) ? forced : 1024;
   if ((k != 1 && forced != 256) || forced == 512 || forced == 1024) {
     std::vector<uint8_t> lut2;
@@ -416,10 +437,6 @@ void plan_chunks(obt_model* m) {
   const int64_t ring = std::max<int64_t>((int64_t)kStages * per_tree * group, avail - tile_objs * m->n_features);
   int ct = (int)std::max<int64_t>(group, (ring / kStages - 512) / (int64_t)per_tree / group * group);
   ct = std::min(ct, 64);
-  if (const char* e = getenv("OBT_CHUNK_TREES")) {  // tuning override (a multiple of the group)
-    const int v = atoi(e);
-    if (v >= group && v % group == 0) ct = std::min(ct, v);
-  }
   const int groups = (m->n_trees + group - 1) / group;
   if (groups > 0) ct = std::min(ct, groups * group);
   m->chunk_trees = ct;
@@ -660,10 +677,6 @@ int plan_tile(const obt_model* m, int64_t n) {
   int64_t tmax = (m->smem_optin - fixed) / m->n_features;
   tmax = std::min<int64_t>(tmax / kTileQuantum * kTileQuantum, 4 * (obt::kApplyMaxThreads - obt::kApplyProducerThreads) / kTileQuantum * kTileQuantum);
   if (tmax < kTileQuantum) return -1;
-  if (const char* e = getenv("OBT_TILE")) {  // tuning override (multiple of 128, within the cap)
-    const int64_t t = atoll(e);
-    if (t >= kTileQuantum && t % kTileQuantum == 0 && t <= tmax) return (int)t;
-  }
   int64_t want = (n + m->sm_count - 1) / m->sm_count;
   want = std::max<int64_t>(kTileQuantum, (want + kTileQuantum - 1) / kTileQuantum * kTileQuantum);
   return (int)std::min(tmax, want);
@@ -680,12 +693,12 @@ int param_chunks_per_launch(const obt_model* m) {
 // (cfg2): 13% faster per tree in one launch, still 4% faster split over 4 launches, so
 // they are the default up to kMaxParamLaunches launches.
 int use_param_descriptors(const obt_model* m, int tpw) {
-  const char* e = getenv("OBT_DESC_SOURCE");  // tuning override: "smem" or "param"
-  if (e && !strcmp(e, "smem")) return 0;
+  const int forced = opt(OPT_DESC_SOURCE);
+  if (forced == 0) return 0;
   if (m->compare_mode != 7 || tpw != 1) return 0;
   const int per = param_chunks_per_launch(m);
   if (per < 1) return 0;
-  if (e && !strcmp(e, "param")) return 1;
+  if (forced == 1) return 1;
   return (m->n_chunks + per - 1) / per <= kMaxParamLaunches ? 1 : 0;
 }
 
@@ -698,9 +711,7 @@ int choose_tpw(const obt_model* m, int tile, bool write_idx) {
   if (write_idx || m->depth_inst > 8) return 1;
   const int words = tile / 4;
   const int cap = obt::kApplyMaxThreads - obt::kApplyProducerThreads;
-  const char* e = getenv("OBT_TPW");
-  if (e) {
-    const int t = atoi(e);
+  if (const int t = opt(OPT_TPW); t > 0) {
     if ((t == 2 || t == 4) && m->depth_inst % t == 0 && words * t <= cap) return t;
     return 1;
   }
@@ -713,8 +724,7 @@ int choose_tpw(const obt_model* m, int tile, bool write_idx) {
 // buckets out for it).
 int apply_lanes(const obt_model* m, int tile, bool write_idx) {
   if (m->n_outputs > 1) return 1;
-  const char* e = getenv("OBT_DESC_SOURCE");
-  if (e && !strcmp(e, "param")) return 1;  // the parameter-bank kernels have one lane per word
+  if (opt(OPT_DESC_SOURCE) == 1) return 1;  // the parameter-bank kernels have one lane per word
   return choose_tpw(m, tile, write_idx);
 }
 
@@ -733,8 +743,7 @@ int quantize_chunk_bytes(const obt_model* m, size_t per_feature, int64_t n_slots
   // Chunks that start on 32-feature (128-byte) boundaries of the object-major rows: the
   // TMA reads of neighbouring chunks then never share an L2 line (balanced chunks of
   // 100 features read 0.99 GB for cfg2's 0.8 GB of features)
-  const char* al = getenv("OBT_QUANT_ALIGN");  // A/B knob: 0 = balanced chunks
-  if (chunks > 1 && per_feature && !(al && !strcmp(al, "0"))) {
+  if (chunks > 1 && per_feature) {
     const int fit = (int)(budget / per_feature) / 32 * 32;
     if (fit >= 32) fc = std::min(fit, (F + 7) / 8 * 8);
   }
@@ -782,18 +791,12 @@ CUtensorMapL2promotion tma_l2_promotion() {
 // OBT_QUANT_LUT=1 forces K1L wherever its tables exist, 0 disables it.
 bool lut_preferred(const obt_model* m) {
   if (m->used_lut.kmax <= 0) return false;
-  const char* e = getenv("OBT_QUANT_LUT");
-  if (e && !strcmp(e, "0")) return false;
-  if (e && !strcmp(e, "1")) return true;
+  if (opt(OPT_QUANT_LUT) == 0) return false;
+  if (opt(OPT_QUANT_LUT) == 1) return true;
   // 1024-cell tables (1 KB per feature) pay off only against deep searches: cfg4 (7
   // levels) 4.49 vs 4.95 ms, cfg5 (6 levels) 17.1 vs 16.5 ms
   if (m->used_lut.cells > 256 && m->used.levels < 7) return false;
   return 1 + m->used_lut.kmax < m->used.levels - 2;
-}
-
-bool quantize_tma_enabled() {
-  const char* e = getenv("OBT_QUANT_TMA");  // A/B knob: 0 = always the LDG kernel
-  return !(e && !strcmp(e, "0"));
 }
 
 // Tiled output may have a second region (objects >= split, tiles of tile2 into out2):
@@ -833,13 +836,10 @@ int launch_quantize(const obt_model* m, const float* x, int64_t n, int layout, u
   const bool use_lut = tiled && lut_preferred(m);
   obt::QuantTmaFn tfn = use_lut ? pick_quant_lut(lt.kmax, lt.cells) : pick_quant_tma(bt.levels);
   if (tiled && layout == OBT_LAYOUT_OBJECT_MAJOR && F % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
-      tfn && encode_tiled() && quantize_tma_enabled()) {
+      tfn && encode_tiled()) {
     // two CTAs per SM: each gets half the SM's shared memory less the per-CTA reserve
-    // two CTAs per SM: each gets half the SM's shared memory (OBT_QUANT_ONE_CTA=1: one CTA
-    // per SM with every feature of its rows, so no L2 line is shared between CTAs)
-    const char* oc = getenv("OBT_QUANT_ONE_CTA");
-    const size_t half = (oc && !strcmp(oc, "1")) ? (size_t)m->smem_optin - 1024
-                                                 : (size_t)(m->smem_optin + 1024) / 2 - 1024;
+    // (one CTA per SM with every feature of its rows measured slower: cfg2 0.239 vs 0.198 ms)
+    const size_t half = (size_t)(m->smem_optin + 1024) / 2 - 1024;
     const size_t lut_fixed = use_lut ? 256 + 32 : 0;  // 256-byte alignment of the tables
     const int fc = use_lut ? quantize_chunk_bytes(m, (size_t)lt.cells + lt.rec_stride, n_slots,
                                                   half - obt::kQTSmemFixed - lut_fixed)
@@ -870,8 +870,7 @@ int launch_quantize(const obt_model* m, const float* x, int64_t n, int layout, u
   }
 
   // K1 (rows loaded by each lane): the cell-table search where K1L would run, else Eytzinger
-  const char* le = getenv("OBT_LDG_LUT");  // A/B knob: 0 = Eytzinger in the LDG kernel
-  const bool ldg_lut = use_lut && !(le && !strcmp(le, "0"));
+  const bool ldg_lut = use_lut;
   QuantFn fn = ldg_lut ? obt::pick_quant_ldg_lut(lt.kmax, lt.cells, layout) : pick_quant(bt.levels, layout, tiled);
   if (!fn) return fail(OBT_E_UNSUPPORTED, "no quantize kernel for %d levels", bt.levels);
   const int fc = ldg_lut ? quantize_chunk_bytes(m, (size_t)lt.cells + lt.rec_stride, n_slots, obt::kQuantSmem - 256)
@@ -908,17 +907,11 @@ int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, int tpw, d
                           : pick_apply(m->depth_inst, m->compare_mode, m->leaf_storage, write_idx, dsrc);
   if (!k.fn) return fail(OBT_E_UNSUPPORTED, "no apply kernel for depth %d", m->depth_inst);
   const int64_t n_tiles = (n + tile - 1) / tile;
-  const char* te = getenv("OBT_PARAM_TABLES");  // A/B knob: 0 = parameter launches stream full records
-  const bool tables_only = dsrc && tp->d_tables && !(te && !strcmp(te, "0"));
+  // parameter-bank launches stream tables-only ring chunks (their descriptors travel in
+  // the kernel parameters)
+  const bool tables_only = dsrc && tp->d_tables;
   const uint32_t ring_chunk = tables_only ? tp->tables_chunk_bytes : m->chunk_bytes;
-  // the smaller tables-only chunks may leave room for more ring stages (OBT_PARAM_STAGES)
-  int stages = kStages;
-  if (tables_only) {
-    const char* ps = getenv("OBT_PARAM_STAGES");
-    const int want = ps ? std::max(2, std::min(8, atoi(ps))) : kStages;
-    while (stages < want && 512 + (size_t)(stages + 1) * ring_chunk + (size_t)m->n_features * tile <= (size_t)m->smem_optin)
-      ++stages;
-  }
+  const int stages = kStages;
   const size_t smem = 512 + (size_t)stages * ring_chunk + (size_t)m->n_features * tile;
   if (smem > (size_t)m->smem_optin)
     return fail(OBT_E_UNSUPPORTED, "tile of %d objects needs %zu bytes of shared memory", tile, smem);
@@ -947,30 +940,19 @@ int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, int tpw, d
   // Bucket tiles of one region are re-read by every launch.  Launches alternate the tile
   // order (the first runs last-to-first: the quantize launch wrote the high tiles last),
   // so each launch's first wave finds the previous pass's last tiles still in L2
-  // (OBT_TILE_ORDER=fwd disables it; cfg2 apply 1.035 -> 1.024 ms).  OBT_L2_NEXT=1 also
-  // has every CTA prefetch the next wave's tile into L2 (measured 1.029 ms: no gain).
+  // (cfg2 apply 1.035 -> 1.024 ms; an L2 prefetch of the next wave's tile measured no gain).
   // Launch chaining (parameter-bank folds of several launches): launch k > 0 goes out
   // as a programmatic dependent launch, so its CTAs start on the SMs launch k - 1's
   // partial last wave leaves idle; a CTA waits only for its own tile's carry (per-tile
-  // flags).  Not under stream capture.  OBT_PDL=0 disables it.
+  // flags).  Not under stream capture.  Path option "pdl" = 0 disables it.
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   CUDA_TRY(cudaStreamIsCapturing(stream, &cap));
-  const char* pe = getenv("OBT_PDL");  // read per call
   const bool chain = flags && dsrc && !write_idx && n_launch > 1 && k.words == 1 && cap == cudaStreamCaptureStatusNone &&
-                     !(pe && !strcmp(pe, "0"));
+                     opt(OPT_PDL) != 0;
   if (chain) CUDA_TRY(cudaMemsetAsync(flags, 0, (size_t)n_tiles * 4, stream));
   p.tile_flags = flags;
-  const char* to = getenv("OBT_TILE_ORDER");
-  const bool alternate = !chain && !(to && !strcmp(to, "fwd"));  // chained launches keep one order
-  const char* co = getenv("OBT_CHAIN_ORDER");  // "fwd": chained launches first-to-last
-  const bool chain_rev = !(co && !strcmp(co, "fwd"));
-  const char* ln = getenv("OBT_L2_NEXT");
+  const bool alternate = !chain;  // chained launches keep one order
   p.l2_wave = 0;
-  if (ln && !strcmp(ln, "1")) {
-    int per_sm = 1;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, (int)block.x, smem));
-    p.l2_wave = std::max(per_sm, 1) * m->sm_count;
-  }
   for (int l = 0; l < n_launch; ++l) {
     p.chunk_begin = l * per;
     p.chunk_end = std::min(m->n_chunks, (l + 1) * per);
@@ -978,7 +960,7 @@ int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, int tpw, d
     p.last = l == n_launch - 1;
     // chained launches share one order; last-to-first by default, so the first launch's
     // first waves read the tiles the quantize wrote last (still in L2)
-    p.reverse = chain ? (chain_rev ? 1 : 0) : (alternate && (l % 2 == 0) ? 1 : 0);
+    p.reverse = chain ? 1 : (alternate && (l % 2 == 0) ? 1 : 0);
     p.flag_wait = chain ? l : 0;
     p.flag_set = chain && l < n_launch - 1 ? l + 1 : 0;
     if (dsrc) {
@@ -1116,9 +1098,8 @@ bool wide_eligible(const obt_model* m) {
   int ts = 0, ns = 0;
   if (!wide_rings(m, &ts, &ns)) return false;
   if (!obt::pick_wide(m->depth_inst, m->compare_mode, m->leaf_storage)) return false;
-  const char* e = getenv("OBT_WIDE");  // A/B knob: 0 never, 1 wherever it fits
-  if (e && !strcmp(e, "0")) return false;
-  if (e && !strcmp(e, "1")) return true;
+  if (opt(OPT_WIDE) == 0) return false;
+  if (opt(OPT_WIDE) == 1) return true;
   return plan_tile(m, (int64_t)1 << 40) <= 512;
 }
 
@@ -1182,8 +1163,7 @@ int launch_multi_staged(obt_model* m, const uint8_t* q, int64_t n, double* out, 
 int launch_multi(obt_model* m, const uint8_t* q, int64_t n, double* out, cudaStream_t stream) {
   if (m->multi_staged) return launch_multi_staged(m, q, n, out, stream);
   int di = 0;
-  const void* fn = m->multi_slice ? obt::pick_multi_slice(m->depth_inst, m->compare_mode, m->leaf_storage, m->n_outputs, &di)
-                                  : obt::pick_multi(m->depth_inst, m->compare_mode, m->leaf_storage, m->n_outputs, &di);
+  const void* fn = obt::pick_multi(m->depth_inst, m->compare_mode, m->leaf_storage, m->n_outputs, &di);
   if (!fn || di != m->depth_inst) return fail(OBT_E_UNSUPPORTED, "no multi-output kernel for depth %d, %d outputs",
                                              m->depth_inst, m->n_outputs);
   obt::MultiParams p{};
@@ -1202,27 +1182,14 @@ int launch_multi(obt_model* m, const uint8_t* q, int64_t n, double* out, cudaStr
   p.scale = m->scale;
   p.bias = m->bias;
   void* kargs[] = {&p};
-  const int threads = m->multi_slice ? kMultiTile / 4 : obt::kMultiThreads;
+  const int threads = obt::kMultiThreads;
   const int64_t n_tiles = (n + kMultiTile - 1) / kMultiTile;
-  // persistent grid: the resident CTAs loop over the tiles (OBT_MULTI_PERSIST=0: one CTA per tile)
+  // persistent grid: the resident CTAs loop over the tiles
   int per_sm = 0;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0));
-  const char* pe = getenv("OBT_MULTI_PERSIST");
   const int64_t resident = (int64_t)std::max(per_sm, 1) * m->sm_count;
-  const int64_t blocks = (pe && !strcmp(pe, "0")) ? n_tiles : std::min<int64_t>(n_tiles, resident);
-  const dim3 grid((unsigned)blocks), block(threads);
-  // residency cap (experiment knob): reserving shared memory limits the CTAs per SM, so
-  // fewer objects' bucket rows (F bytes each) compete for L2
-  size_t smem = 0;
-  if (const char* e = getenv("OBT_MULTI_CTAS_PER_SM")) {
-    const int k = atoi(e);
-    if (k > 0) {
-      smem = (size_t)(m->smem_optin + 1024) / (size_t)k - 1024;
-      if (smem > (size_t)m->smem_optin) smem = (size_t)m->smem_optin;
-      CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, m->smem_optin));
-    }
-  }
-  CUDA_TRY(cudaLaunchKernel(fn, grid, block, kargs, smem, stream));
+  const dim3 grid((unsigned)std::min<int64_t>(n_tiles, resident)), block(threads);
+  CUDA_TRY(cudaLaunchKernel(fn, grid, block, kargs, 0, stream));
   ++g_launches;
   return OBT_OK;
 }
@@ -1273,9 +1240,8 @@ bool fan_eligible(const obt_model* m, int64_t n) {
   if (m->n_outputs > 1 || m->depth_inst > 8 || m->n_trees == 0 || n <= 0) return false;
   if (fan_stages(m) < 2 || fan_smem(m) > (size_t)m->smem_optin) return false;
   if (!obt::pick_fan(m->depth_inst, m->compare_mode, m->leaf_storage)) return false;
-  const char* e = getenv("OBT_FAN");
-  if (e && !strcmp(e, "0")) return false;
-  if (e && !strcmp(e, "1")) return true;
+  if (opt(OPT_FAN) == 0) return false;
+  if (opt(OPT_FAN) == 1) return true;
   const int64_t blocks = (n + 127) / 128;
   return blocks <= 2 * (int64_t)m->sm_count && m->n_trees >= 4 * obt::kFanComputeWarps;
 }
@@ -1294,12 +1260,12 @@ Regions plan_regions(const obt_model* m, int64_t n, bool split_ok) {
     return r;
   }
   r.tile[0] = plan_tile(m, n);
-  const char* e = getenv("OBT_TAIL_SPLIT");  // "0" never, "1" whenever a tail exists
-  if (!split_ok || r.tile[0] < 0 || m->n_outputs > 1 || (e && !strcmp(e, "0"))) return r;
+  const int split = opt(OPT_TAIL_SPLIT);  // 0 never, 1 whenever a tail exists
+  if (!split_ok || r.tile[0] < 0 || m->n_outputs > 1 || split == 0) return r;
   // Not behind a parameter-bank main region: the tail then runs with shared-memory
   // descriptors at ~60% of the main region's rate, and one more launch; measured at
   // cfg2 (3 parameter-bank launches): apply 1.045 ms without the split, 1.081 with it.
-  if (!(e && !strcmp(e, "1")) && use_param_descriptors(m, apply_lanes(m, r.tile[0], false))) return r;
+  if (split != 1 && use_param_descriptors(m, apply_lanes(m, r.tile[0], false))) return r;
   const int64_t wave = (int64_t)m->sm_count * r.tile[0];
   const int64_t full = n / wave * wave, rest = n - full;
   if (full == 0 || rest == 0) return r;
@@ -1337,6 +1303,26 @@ int check_layout(int layout) {
 extern "C" {
 
 int obt_abi_version(void) { return OBT_ABI_VERSION; }
+
+int obt_set_path_option(const char* name, int value) {
+  if (!name) return fail(OBT_E_INVALID, "null option name");
+  for (int i = 0; i < OPT_COUNT; ++i)
+    if (!strcmp(name, kPathOptionNames[i])) {
+      g_opt[i].store(value < 0 ? -1 : value, std::memory_order_relaxed);
+      return OBT_OK;
+    }
+  return fail(OBT_E_INVALID, "unknown path option '%s'", name);
+}
+
+int obt_get_path_option(const char* name, int* value) {
+  if (!name || !value) return fail(OBT_E_INVALID, "null argument");
+  for (int i = 0; i < OPT_COUNT; ++i)
+    if (!strcmp(name, kPathOptionNames[i])) {
+      *value = opt((PathOption)i);
+      return OBT_OK;
+    }
+  return fail(OBT_E_INVALID, "unknown path option '%s'", name);
+}
 
 const char* obt_last_error(void) { return g_error.c_str(); }
 
@@ -1380,16 +1366,11 @@ int obt_model_create(const obt_model_desc* d, int device, obt_model** out) {
       const int ord = d->split_ordinal[(size_t)t * D + s];
       if (ord != kSentinel) used[d->split_feature[(size_t)t * D + s]].push_back(ord);
     }
-  const char* no_remap = getenv("OBT_NO_REMAP");  // A/B knob: quantize against every border
   std::vector<std::vector<int>> rank(d->n_features);  // ordinal -> rank in R_f
   std::vector<float> used_borders((size_t)d->n_features * std::max(1, d->border_stride), INFINITY);
   std::vector<int32_t> used_counts(d->n_features, 0);
   for (int f = 0; f < d->n_features; ++f) {
     auto& u = used[f];
-    if (no_remap && atoi(no_remap)) {
-      u.resize(d->border_counts[f]);
-      for (int k = 0; k < d->border_counts[f]; ++k) u[k] = k;
-    }
     std::sort(u.begin(), u.end());
     u.erase(std::unique(u.begin(), u.end()), u.end());
     rank[f].assign(256, -1);
@@ -1435,38 +1416,30 @@ int obt_model_create(const obt_model_desc* d, int device, obt_model** out) {
       const float f = (float)v;
       exact32 = std::isfinite(f) && (double)f == v && !(v == 0.0 && std::signbit(v) != std::signbit(f));
     }
-    const char* force64 = getenv("OBT_LEAF_STORAGE");  // A/B knob: "64" keeps binary64 tables
-    m->leaf_storage = (exact32 && !(force64 && !strcmp(force64, "64"))) ? 1 : 0;
+    m->leaf_storage = (exact32 && opt(OPT_LEAF_STORAGE) != 0) ? 1 : 0;
   }
   const size_t ls = leaf_size(m->leaf_storage);
   if (C > 1) {
-    // multi-output records, one leaf's C values contiguous: K4s slots of multi_slot bytes
-    // (a power of two, so a record never straddles a 128-byte line), or K4 [CP] rows
-    // K4s measured slower than K4 at config 5 (668 vs 575 ms: 168 registers, 12 warps per
-    // SM); kept as the OBT_MULTI_SLICE=1 knob
-    const char* ms = getenv("OBT_MULTI_SLICE");
-    m->multi_slice = (ms && !strcmp(ms, "1")) ? 1 : 0;
+    // multi-output records, one leaf's C values contiguous in 16-byte rows (K4, K5)
     // K5 (staged tables and rows) for fp32 records, C <= 10, depth <= 10, when at least
     // two stages (one tree's table + its bucket rows each) fit shared memory
     {
-      const char* mst = getenv("OBT_MULTI_STAGED");  // A/B knob: 0 = K4
       const int CPs = obt::staged_record_values(C);
       const uint32_t table = (uint32_t)((per_tree * CPs * 4 + 15) / 16 * 16);
       const uint32_t stage = (table + (uint32_t)DI * obt::kStagedTile + 127u) & ~127u;
       const int stages = std::min(8, (int)(((size_t)m->smem_optin - 512) / stage));
       int sdi = 0;
-      const bool ok = !m->multi_slice && m->leaf_storage == 1 && C <= 10 && stages >= 2 &&
+      const bool ok = m->leaf_storage == 1 && C <= 10 && stages >= 2 &&
                       obt::pick_multi_staged(DI, m->compare_mode, C, &sdi) != nullptr && sdi == DI;
-      if (ok && !(mst && !strcmp(mst, "0"))) {
+      if (ok && opt(OPT_MULTI_STAGED) != 0) {
         m->multi_staged = 1;
         m->staged_stages = stages;
         m->staged_table_bytes = table;
         m->staged_stage_bytes = stage;
       }
     }
-    m->multi_slot = m->multi_slice    ? obt::multi_slice_slot(m->leaf_storage, C)
-                    : m->multi_staged ? obt::staged_record_values(C) * (int)ls
-                                      : obt::multi_record_values(m->leaf_storage, C) * (int)ls;
+    m->multi_slot = m->multi_staged ? obt::staged_record_values(C) * (int)ls
+                                    : obt::multi_record_values(m->leaf_storage, C) * (int)ls;
     // records in the predict path's level order (record j' holds reference leaf
     // reference_leaf(perm, DI, j'); entries past 2^D belong to sentinel levels, never read)
     std::vector<uint8_t> rec((size_t)std::max(m->n_trees, 1) * per_tree * m->multi_slot, 0);
@@ -1541,7 +1514,7 @@ int obt_model_quantize_kernel(const obt_model* m, int32_t* kind, int32_t* param)
 
 int obt_model_multi_kernel(const obt_model* m, int32_t* kind) {
   if (!m || !kind) return fail(OBT_E_INVALID, "null argument");
-  *kind = m->n_outputs <= 1 ? -1 : m->multi_staged ? 2 : m->multi_slice ? 1 : 0;
+  *kind = m->n_outputs <= 1 ? -1 : m->multi_staged ? 2 : 0;
   return OBT_OK;
 }
 

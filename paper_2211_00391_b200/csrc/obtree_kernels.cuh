@@ -26,7 +26,6 @@
 //                                 fold by 4 fold warps
 //   K2s  apply_split_kernel       depth-split lanes (wide feature sets)
 //   K4   apply_multi_kernel       multi-output, records gathered from L2
-//   K4s  apply_multi_slice_kernel multi-output, sliced records (knob)
 //   K5   apply_multi_staged_kernel multi-output, per-tree tables + bucket rows staged by TMA
 #pragma once
 
@@ -1681,119 +1680,6 @@ __global__ void __launch_bounds__(kMultiThreads, multi_min_blocks(LEAF, C)) appl
       for (int c = 0; c < C; ++c)
         p.out[obj_of(k) * C + c] = p.last ? __dadd_rn(__dmul_rn(acc[k][c], p.scale), p.bias) : acc[k][c];
     }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// K4s: sliced multi-output apply.  K4 gathers each object's C-value record with
-// 16-byte loads from one lane, so every warp load touches 32 random L2 lines and a
-// record costs 3 line lookups (the L1 takes about one line per clock: config 5 ran at
-// ~3 lookups per object-tree).  Here the record lives in one aligned slot (64 bytes at
-// C = 10 fp32, never straddling a 128-byte line) and S = ceil(C / V) lanes fetch it
-// together, V values (8 bytes) each: a warp load covers ~32 / S objects with one line
-// each.  Index work stays SWAR (lane = 4 objects of a bucket word, as K4); the leaf
-// index of the lane-word's byte k is then shuffled to the lanes gathering that object:
-// for byte k the warp's 32 objects x S pairs are exactly S loads of 32 lanes, lane l of
-// load s handling object (32 s + l) / S, pair (32 s + l) % S -- so the shuffled word is
-// the same byte k for every lane of a load.  Accumulators: 4 x S x V binary64 per lane
-// (80 registers at C = 10), folded in tree order per (object, output) as K4.
-template <int LEAF, int C> struct MultiSlice {
-  static constexpr int kLS = LEAF == 0 ? 8 : 4;                 // bytes per value
-  static constexpr int V = 8 / kLS;                             // values per lane load
-  static constexpr int S = (C + V - 1) / V;                     // lanes per object
-  static constexpr int kRec = S * 8;                            // used bytes of a slot
-  static constexpr int kSlot = kRec <= 16 ? 16 : kRec <= 32 ? 32 : kRec <= 64 ? 64 : 128;
-};
-
-template <int DI, int CMP, int LEAF, int C>
-__global__ void __launch_bounds__(128) apply_multi_slice_kernel(const __grid_constant__ MultiParams p) {
-  using MS = MultiSlice<LEAF, C>;
-  constexpr int S = MS::S, V = MS::V;
-  static_assert(S <= 32, "slices per object");
-  using leaf_t = typename LeafT<LEAF>::T;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int word = threadIdx.x;  // bucket word of this lane within the 512-object tile
-  // persistent CTAs (grid = resident CTAs): every CTA starts its next tile when the
-  // previous one ends, so all CTAs walk the trees nearly in step and the active window of
-  // leaf records stays L2-resident (one launch of 31250 CTAs kept CTAs at every tree
-  // position at once: all 4000 trees' records, 197 MB, competed for L2 at config 5)
-  const int64_t n_tiles = (p.n + p.tile - 1) / p.tile;
-  for (int64_t tile_idx = blockIdx.x; tile_idx < n_tiles; tile_idx += gridDim.x) {
-    const uint8_t* qrow0 = p.q + tile_idx * (int64_t)p.n_features * p.tile + 4 * word;
-    const int64_t blk = tile_idx * p.tile + warp * 128;  // the warp's 128-object block
-    // gather slots: load s of byte k -> object 32 k + j_s, pair q_s
-    int src[S];
-    uint32_t qoff[S];
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
-      const int g = 32 * s + lane;
-      src[s] = g / S;
-      qoff[s] = (uint32_t)(g % S) * 8u;
-    }
-    auto out_index = [&](int k, int s, int v) -> int64_t {  // -1: padding
-      const int g = 32 * s + lane;
-      const int c = (g % S) * V + v;
-      const int64_t o = blk + 32 * k + g / S;
-      return (c < C && o < p.n) ? o * C + c : -1;
-    };
-    double acc[4][S][V];
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-#pragma unroll
-      for (int s = 0; s < S; ++s)
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-          const int64_t i = out_index(k, s, v);
-          acc[k][s][v] = (p.first || i < 0) ? 0.0 : p.out[i];
-        }
-    for (int t = p.tree_begin; t < p.tree_end; ++t) {
-      const uint2* ds = reinterpret_cast<const uint2*>(p.desc) + (size_t)t * DI;
-      uint32_t lo = 0, hi = 0;
-#pragma unroll
-      for (int d = 0; d < DI; ++d) {
-        const uint2 dd = __ldg(ds + d);  // warp-uniform address: one broadcast
-        uint32_t b7;
-        if constexpr (CMP == 7) {
-          b7 = __ldg(reinterpret_cast<const uint32_t*>(qrow0 + dd.x)) + dd.y;
-        } else {
-          const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(qrow0 + (dd.x >> 8)));
-          b7 = maj3((w & 0x7f7f7f7fu) + (__byte_perm(dd.x, 0u, 0x0000u) & 0x7f7f7f7fu), w, dd.y);
-        }
-        if (d < 8) lo |= (b7 >> (7 - d)) & (0x01010101u << d);
-        else hi |= (b7 >> (15 - d)) & (0x01010101u << (d - 8));
-      }
-      const unsigned char* tab = reinterpret_cast<const unsigned char*>(p.leaves) + ((size_t)t << DI) * MS::kSlot;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        // leaf index of byte k (object 32 k + lane): low 8 bits from lo, the rest from hi
-        const uint32_t mine = DI > 8 ? (__byte_perm(lo, hi, (uint32_t)(k | ((4 + k) << 4))) & 0xffffu)
-                                     : __byte_perm(lo, 0u, 0x4440u | k);
-        uint2 rv[S];
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-          const uint32_t idx = __shfl_sync(0xffffffffu, mine, src[s]);
-          rv[s] = __ldg(reinterpret_cast<const uint2*>(tab + (size_t)idx * MS::kSlot + qoff[s]));
-        }
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-          if constexpr (LEAF == 0) {
-            acc[k][s][0] += __hiloint2double((int)rv[s].y, (int)rv[s].x);
-          } else {
-            acc[k][s][0] += (double)__uint_as_float(rv[s].x);
-            acc[k][s][V - 1] += (double)__uint_as_float(rv[s].y);
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-#pragma unroll
-      for (int s = 0; s < S; ++s)
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-          const int64_t i = out_index(k, s, v);
-          if (i >= 0) p.out[i] = p.last ? __dadd_rn(__dmul_rn(acc[k][s][v], p.scale), p.bias) : acc[k][s][v];
-        }
   }
 }
 

@@ -136,10 +136,10 @@ class MultiOutputEvaluator:
         return ({1: "cells", 2: "cells1024", 3: "cells512"}.get(kind.value, "eytzinger"), param.value)
 
     def apply_kernel(self) -> str:
-        """The multi-output apply kernel this model runs: "staged" (K5), "sliced" (K4s) or "gather" (K4)."""
+        """The multi-output apply kernel this model runs: "staged" (K5) or "gather" (K4)."""
         kind = ctypes.c_int32()
         _native.check(self._lib.obt_model_multi_kernel(self.handle, ctypes.byref(kind)))
-        return {2: "staged", 1: "sliced", 0: "gather"}.get(kind.value, "none")
+        return {2: "staged", 0: "gather"}.get(kind.value, "none")
 
     def predict_device(self, x, layout: Layout = Layout.OBJECT_MAJOR, out=None, workspace=None):
         """float32 CUDA tensor [n][F] (or [F][n]) -> float64 CUDA tensor [n][C]."""

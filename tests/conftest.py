@@ -41,3 +41,22 @@ def _built_artifacts():
         # the CPU suite only needs the library for the symbol checks, which report it
         pass
     yield
+
+
+@pytest.fixture
+def paths():
+    """Force planner choices (obt_set_path_option) for one test: ``paths(wide=1, fan=0)``;
+    the previous values are restored afterwards."""
+    from paper_2211_00391_b200 import _native
+
+    saved = {}
+
+    def force(**opts):
+        for k, v in opts.items():
+            if k not in saved:
+                saved[k] = _native.get_path_option(k)
+            _native.set_path_option(k, v)
+
+    yield force
+    for k, v in saved.items():
+        _native.set_path_option(k, v)

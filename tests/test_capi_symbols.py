@@ -50,3 +50,24 @@ def test_sm100a_code_present():
     """The library carries sm_100a SASS (not only PTX for another target)."""
     out = subprocess.run(["cuobjdump", "--list-elf", str(_native.library_path())], capture_output=True, text=True)
     assert "sm_100a" in out.stdout, out.stdout[:500]
+
+
+def test_path_options_roundtrip_without_gpu():
+    """Every planner choice a test forces is a named path option: automatic (-1) by
+    default, settable, restorable; unknown names are refused with the name in the error."""
+    for name in _native.PATH_OPTIONS:
+        assert _native.get_path_option(name) == -1, name
+    with _native.path_options(wide=1, tpw=2):
+        assert _native.get_path_option("wide") == 1 and _native.get_path_option("tpw") == 2
+    assert _native.get_path_option("wide") == -1 and _native.get_path_option("tpw") == -1
+    with pytest.raises(_native.NativeError, match="no_such_path"):
+        _native.set_path_option("no_such_path", 1)
+
+
+def test_no_environment_switches_in_the_library():
+    """Kernel selection never reads the environment per call (the path options above are
+    the one, explicit way to force a path)."""
+    import glob
+
+    for src in glob.glob(str(ROOT / "paper_2211_00391_b200" / "csrc" / "*")):
+        assert "getenv(" not in Path(src).read_text(), src

@@ -278,12 +278,12 @@ def test_predict_deeper_than_reference(D):
 
 @pytest.mark.parametrize("source", ["param", "smem"])
 @pytest.mark.parametrize("strategy", [obt.LeafStrategy.NAIVE, obt.LeafStrategy.NAIVE16])
-def test_descriptor_sources_and_multi_launch_fold(monkeypatch, source, strategy):
+def test_descriptor_sources_and_multi_launch_fold(paths, source, strategy):
     """3,000 depth-6 trees exceed one launch's parameter bank (about 1,300 trees), so the
     parameter path folds across 3 launches through the carried accumulators; the
     shared-memory path streams all descriptors in one launch.  Both are bit-exact."""
-    monkeypatch.setenv("OBT_DESC_SOURCE", source)
-    monkeypatch.setenv("OBT_FAN", "0")  # the K2 / K2s paths, not the small-batch K2f
+    paths(desc_source=1 if source == "param" else 0)
+    paths(fan=0)  # the K2 / K2s paths, not the small-batch K2f
     model = _model(12, 50, 3001, 6, seed=77)
     x = _features(model, 2500, seed=78)
     prec = oracle.BINARY64 if strategy is obt.LeafStrategy.NAIVE else oracle.BINARY16
@@ -296,18 +296,17 @@ def test_descriptor_sources_and_multi_launch_fold(monkeypatch, source, strategy)
     assert np.array_equal(idx, oracle.leaf_indices(fm, oracle.quantize(fm, x))[1290:1400])
 
 
-@pytest.mark.parametrize("kernel", ["staged", "k4", "slice"])
+@pytest.mark.parametrize("kernel", ["staged", "k4"])
 @pytest.mark.parametrize("D,C,F,B", [(10, 10, 40, 254), (6, 3, 17, 64), (8, 16, 9, 128), (3, 2, 5, 7), (12, 7, 13, 30),
                                      (10, 9, 33, 100), (4, 5, 8, 200), (10, 4, 2, 254)])  # last: 8-bit compare
-def test_multi_output_bit_exact(monkeypatch, kernel, D, C, F, B):
+def test_multi_output_bit_exact(paths, kernel, D, C, F, B):
     """Multi-output (config 5 shape family): K5 (staged tables, default where it applies:
-    fp32 records, C <= 10, depth <= 10), K4 (OBT_MULTI_STAGED=0) and K4s (sliced records,
-    OBT_MULTI_SLICE=1) against the oracle restatement, both layouts, with the binary64
-    leaf tables too (OBT_LEAF_STORAGE=64, which K5 leaves to K4)."""
+    fp32 records, C <= 10, depth <= 10) and K4 (path option multi_staged=0) against the
+    oracle restatement, both layouts, with the binary64 leaf tables too (leaf_storage=0,
+    which K5 leaves to K4)."""
     from paper_2211_00391_b200 import multiclass
 
-    monkeypatch.setenv("OBT_MULTI_SLICE", "1" if kernel == "slice" else "0")
-    monkeypatch.setenv("OBT_MULTI_STAGED", "1" if kernel == "staged" else "0")
+    paths(multi_staged=1 if kernel == "staged" else 0)
 
     spec = synthetic.WorkloadSpec("m", 1, F, B, 57, D, 0.01, n_outputs=C, cfg=5)
     arrays = synthetic.model_arrays(spec, seed=D * 100 + C, affine=True)
@@ -325,7 +324,7 @@ def test_multi_output_bit_exact(monkeypatch, kernel, D, C, F, B):
     assert np.array_equal(got, want)
     dev = ev.predict_device(torch.from_numpy(np.ascontiguousarray(x.T)).cuda(), obt.Layout.FEATURE_MAJOR).cpu().numpy()
     assert np.array_equal(dev, want)
-    monkeypatch.setenv("OBT_LEAF_STORAGE", "64")
+    paths(leaf_storage=0)
     ev64 = multiclass.MultiOutputEvaluator(model)
     assert np.array_equal(ev64.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR)), want)
 
@@ -349,12 +348,12 @@ def test_multi_output_tree_shard_partials_sum_to_prediction():
 
 @pytest.mark.parametrize("n", [1, 129, 1000, 4097])
 @pytest.mark.parametrize("tpw", ["1", "2"])
-def test_no_writes_outside_outputs_and_workspace(monkeypatch, n, tpw):
+def test_no_writes_outside_outputs_and_workspace(paths, n, tpw):
     """compute-sanitizer is unavailable on this pool: guard regions around the score
     vector and the bucket workspace must be untouched after a predict (ragged n, both
     apply kernels), and results must still match the oracle."""
-    monkeypatch.setenv("OBT_TPW", tpw)
-    monkeypatch.setenv("OBT_FAN", "0")  # the K2 / K2s paths, not the small-batch K2f
+    paths(tpw=int(tpw))
+    paths(fan=0)  # the K2 / K2s paths, not the small-batch K2f
     model = _model(24, 60, 75, 6, seed=n)
     x = _features(model, n, seed=n)
     ev = obt.Evaluator(model)
@@ -416,10 +415,10 @@ def test_reference_corpus_on_gpu():
 @pytest.mark.parametrize("tpw", ["2", "4"])
 @pytest.mark.parametrize("D", [4, 8])
 @pytest.mark.parametrize("F,B,T", [(29, 100, 70), (3, 254, 200)])  # 7-bit / 8-bit compare after remap
-def test_depth_split_lanes_bit_exact(monkeypatch, tpw, D, F, B, T):
-    """K2s: TPW lanes per bucket word (OBT_TPW forces it) keep the tree-order fold exact."""
-    monkeypatch.setenv("OBT_TPW", tpw)
-    monkeypatch.setenv("OBT_FAN", "0")  # the K2 / K2s paths, not the small-batch K2f
+def test_depth_split_lanes_bit_exact(paths, tpw, D, F, B, T):
+    """K2s: TPW lanes per bucket word (path option tpw forces it) keep the tree-order fold exact."""
+    paths(tpw=int(tpw))
+    paths(fan=0)  # the K2 / K2s paths, not the small-batch K2f
     model = _model(F, B, T, D, seed=D * 100 + F)
     x = _features(model, 3001, seed=D + F)
     fm = oracle.flatten(model)
@@ -528,7 +527,7 @@ def test_misaligned_workspace_and_output_rejected():
 
 @pytest.mark.parametrize("D", [6, 8])
 @pytest.mark.parametrize("layout", [obt.Layout.OBJECT_MAJOR, obt.Layout.FEATURE_MAJOR])
-def test_tail_wave_split_bit_exact(monkeypatch, D, layout):
+def test_tail_wave_split_bit_exact(paths, D, layout):
     """Batches past one full wave run the partial last wave as a second region of
     smaller tiles (F = 500: 384-object tiles, 148 per wave): bit-exact against the oracle
     and against the single-region path, in both input layouts."""
@@ -541,7 +540,7 @@ def test_tail_wave_split_bit_exact(monkeypatch, D, layout):
     xd = torch.from_numpy(xin).cuda()
     got = ev.predict_device(xd, layout=layout).cpu().numpy()
     assert np.array_equal(got, want)
-    monkeypatch.setenv("OBT_TAIL_SPLIT", "0")
+    paths(tail_split=0)
     assert np.array_equal(ev.predict_device(xd, layout=layout).cpu().numpy(), want)
 
 
@@ -693,13 +692,13 @@ _LUT_SETS = {
 @pytest.mark.parametrize("name,expect,cells", [("mixed", "cells", "256"), ("mixed", "cells1024", "1024"),
                                               ("fallback", "eytzinger", ""), ("crowded256", "cells1024", ""),
                                               ("crowded", "eytzinger", "")])
-def test_cell_table_quantize_edges(monkeypatch, name, expect, cells):
+def test_cell_table_quantize_edges(paths, name, expect, cells):
     """K1L (cell-table quantize) against the oracle on values at, next to and far from
     every border, NaN, +-inf, signed zeros and denormals; and equal to the Eytzinger
-    search (OBT_QUANT_LUT=0) bucket for bucket through the predictions and leaf indices."""
-    monkeypatch.setenv("OBT_QUANT_LUT", "1")  # K1L wherever its tables exist (not only where it is faster)
+    search (path option quant_lut=0) bucket for bucket through the predictions and leaf indices."""
+    paths(quant_lut=1)  # K1L wherever its tables exist (not only where it is faster)
     if cells:
-        monkeypatch.setenv("OBT_LUT_CELLS", cells)
+        paths(lut_cells=int(cells))
     sets = [np.asarray(b, np.float32) for b in _LUT_SETS[name]]
     pad = (-len(sets)) % 4  # F % 4 == 0: the TMA-staged path
     sets += [np.array([0.25 * (i + 1)], np.float32) for i in range(pad)]
@@ -715,17 +714,17 @@ def test_cell_table_quantize_edges(monkeypatch, name, expect, cells):
     # the LDG-loaded kernel (feature-major rows) runs the same cell-table search
     xt = torch.from_numpy(np.ascontiguousarray(x.T)).cuda()
     assert np.array_equal(ev.predict_device(xt, layout=obt.Layout.FEATURE_MAJOR).cpu().numpy(), want)
-    monkeypatch.setenv("OBT_QUANT_LUT", "0")
+    paths(quant_lut=0)
     assert np.array_equal(ev.predict_device(torch.from_numpy(x).cuda()).cpu().numpy(), want)
     assert np.array_equal(ev.predict_device(xt, layout=obt.Layout.FEATURE_MAJOR).cpu().numpy(), want)
 
 
 @pytest.mark.parametrize("split", ["1", "0", "auto"])
-def test_tail_split_behind_parameter_bank(monkeypatch, split):
+def test_tail_split_behind_parameter_bank(paths, split):
     """A parameter-bank main region (7-bit compare, one lane per word) skips the tail
-    split by default; forced on (OBT_TAIL_SPLIT=1) or off, predictions stay bit-exact."""
+    split by default; forced on (tail_split=1) or off, predictions stay bit-exact."""
     if split != "auto":
-        monkeypatch.setenv("OBT_TAIL_SPLIT", split)
+        paths(tail_split=int(split))
     model = _model(48, 64, 40, 6, seed=77)
     n = 400001  # past one wave of the largest tile at F = 48
     x = _features(model, n, seed=78, specials=False)
@@ -737,27 +736,27 @@ def test_tail_split_behind_parameter_bank(monkeypatch, split):
 @pytest.mark.parametrize("D", [1, 3, 6, 8])
 @pytest.mark.parametrize("B", [16, 200])
 @pytest.mark.parametrize("n", [1, 127, 129, 5000])
-def test_fanned_out_small_batch_apply(monkeypatch, D, B, n):
+def test_fanned_out_small_batch_apply(paths, D, B, n):
     """K2f (small batches: trees fanned out over a CTA's compute warps, the fold in tree
     order by the fold warps) bit-exact against the oracle in both precision families, and
-    equal to the K2 / K2s path (OBT_FAN=0)."""
+    equal to the K2 / K2s path (fan=0)."""
     model = _model(21, B, 131, D, seed=D * 31 + B)  # 131 trees: a ragged last chunk
     x = _features(model, n, seed=n + D)
     fm = oracle.flatten(model)
     for strategy, prec in ((obt.LeafStrategy.NAIVE, oracle.BINARY64), (obt.LeafStrategy.NAIVE16, oracle.BINARY16)):
-        monkeypatch.setenv("OBT_FAN", "1")
+        paths(fan=1)
         ev = obt.Evaluator(model, obt.EvalConfig(strategy=strategy))
         got = ev.predict_device(torch.from_numpy(x).cuda()).cpu().numpy()
         want = oracle.evaluate_scalar(fm, x, oracle.OBJECT_MAJOR, prec)
         assert np.array_equal(got, want), (strategy, int(np.count_nonzero(got != want)))
-        monkeypatch.setenv("OBT_FAN", "0")
+        paths(fan=0)
         assert np.array_equal(ev.predict_device(torch.from_numpy(x).cuda()).cpu().numpy(), want)
 
 
 @pytest.mark.parametrize("D", [4, 8])
-def test_fanned_out_eight_bit_compare(monkeypatch, D):
+def test_fanned_out_eight_bit_compare(paths, D):
     """K2f with the 8-bit compare (more than 127 used borders on a feature)."""
-    monkeypatch.setenv("OBT_FAN", "1")
+    paths(fan=1)
     model = _model(2, 254, 160, D, seed=D)  # 320+ splits on each of 2 features: > 127 used borders
     x = _features(model, 2000, seed=D + 1)
     ev = obt.Evaluator(model)
@@ -766,9 +765,9 @@ def test_fanned_out_eight_bit_compare(monkeypatch, D):
     assert np.array_equal(got, oracle.evaluate_scalar(oracle.flatten(model), x))
 
 
-def test_fanned_out_binary64_leaf_tables(monkeypatch):
+def test_fanned_out_binary64_leaf_tables(paths):
     """K2f with binary64 leaf tables (leaves not exactly binary32)."""
-    monkeypatch.setenv("OBT_FAN", "1")
+    paths(fan=1)
     rng = np.random.default_rng(5)
     base = _model(13, 40, 97, 5, seed=5)
     trees = tuple(obt.ObliviousTree(depth=t.depth, splits=t.splits, leaf_values=rng.normal(0, 1, 1 << t.depth))
@@ -781,7 +780,7 @@ def test_fanned_out_binary64_leaf_tables(monkeypatch):
     assert np.array_equal(got, oracle.evaluate_scalar(oracle.flatten(model), x))
 
 
-def test_chained_parameter_bank_launches(monkeypatch):
+def test_chained_parameter_bank_launches(paths):
     """Launch chaining (programmatic dependent launches with per-tile carry flags): a
     2000-tree depth-6 model folds over 3 parameter-bank launches of 2 waves each; the
     chained and the plainly serialised launches equal the oracle bit for bit."""
@@ -792,13 +791,13 @@ def test_chained_parameter_bank_launches(monkeypatch):
     ev = obt.Evaluator(model)
     xd = torch.from_numpy(x).cuda()
     for pdl in ("1", "0", "1"):
-        monkeypatch.setenv("OBT_PDL", pdl)
+        paths(pdl=int(pdl))
         got = ev.predict_device(xd).cpu().numpy()
         assert np.array_equal(got, want), (pdl, int(np.count_nonzero(got != want)))
 
 
 # ---------------------------------------------------------------------------
-# K2w (warp-specialised apply for wide feature sets), forced with OBT_WIDE=1 on small
+# K2w (warp-specialised apply for wide feature sets), forced with the path option wide=1 on small
 # models and chosen by default at config 4's shape.
 
 def _wide_cases():
@@ -809,9 +808,9 @@ def _wide_cases():
 
 @pytest.mark.parametrize("D,B", list(_wide_cases()))
 @pytest.mark.parametrize("n", [1, 255, 257, 256 * 148 + 77, 256 * 148 * 3 + 5])
-def test_wide_apply_bit_exact(monkeypatch, D, B, n):
-    monkeypatch.setenv("OBT_WIDE", "1")
-    monkeypatch.setenv("OBT_FAN", "0")
+def test_wide_apply_bit_exact(paths, D, B, n):
+    paths(wide=1)
+    paths(fan=0)
     model = _model(37, B, 53, D, seed=D * 13 + B)
     x = _features(model, n, seed=n % 1000 + D)
     fm = oracle.flatten(model)
@@ -821,9 +820,9 @@ def test_wide_apply_bit_exact(monkeypatch, D, B, n):
         assert np.array_equal(got, oracle.evaluate_scalar(fm, x, oracle.OBJECT_MAJOR, prec)), (strategy, D, B, n)
 
 
-def test_wide_apply_mixed_depth_binary64_tables_and_layouts(monkeypatch):
-    monkeypatch.setenv("OBT_WIDE", "1")
-    monkeypatch.setenv("OBT_FAN", "0")
+def test_wide_apply_mixed_depth_binary64_tables_and_layouts(paths):
+    paths(wide=1)
+    paths(fan=0)
     model = _mixed_depth_model(29, 60, 141, seed=5)
     x = _features(model, 40_000, seed=6)
     want = oracle.evaluate_scalar(oracle.flatten(model), x)
@@ -834,8 +833,8 @@ def test_wide_apply_mixed_depth_binary64_tables_and_layouts(monkeypatch):
     assert np.array_equal(ev.predict_device(torch.from_numpy(x).cuda()).cpu().numpy(), want)
 
 
-def test_wide_apply_zero_trees_and_empty(monkeypatch):
-    monkeypatch.setenv("OBT_WIDE", "1")
+def test_wide_apply_zero_trees_and_empty(paths):
+    paths(wide=1)
     base = _model(9, 5, 1, 1, seed=2)
     model = obt.ObliviousModel(base.float_features, (), scale=2.0, bias=-0.75)
     x = _features(model, 1000, seed=3)

@@ -7,7 +7,8 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import paper_2211_00391_b200 as obt  # noqa: E402
+import paper_2211_00391_b200 as obt
+from paper_2211_00391_b200 import _native  # noqa: E402
 from paper_2211_00391_b200 import multiclass, stages, synthetic  # noqa: E402
 
 spec = synthetic.WorkloadSpec("s", 3000, 40, 64, 96, 6, 0.05, cfg=2)
@@ -20,7 +21,7 @@ b = ev.predict_device(xd).cpu().numpy()
 assert np.array_equal(a, b)
 stages.quantize(model, xd)
 stages.leaf_indices(model, xd)
-os.environ["OBT_TPW"] = "2"
+_native.set_path_option("tpw", 2)
 ev2 = obt.Evaluator(obt.ModelTables(model))
 assert np.array_equal(ev2.predict_device(xd).cpu().numpy(), a)
 ev16 = obt.Evaluator(model, obt.EvalConfig(strategy=obt.LeafStrategy.NAIVE16))
