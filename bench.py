@@ -475,6 +475,12 @@ def run_reference(args, world, rank):
                                    f"cpu_baseline.reference_pkg times that one too)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not args.no_reference_pkg:
+        # the reference package itself (pure Python + numpy from baseline/_ref), 1 core and
+        # one pinned process per core, beside the C port this line's value times
+        import torch
+
+        line["cpu_baseline"]["reference_pkg"] = reference_pkg_baseline(spec, torch.from_numpy(x), args.cpu_seconds * 4)
     print(json.dumps(line), flush=True)
 
 
