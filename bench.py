@@ -543,6 +543,9 @@ def run_ours(args, world, rank, local):
     from paper_2211_00391_b200 import _native, sharding, synthetic
 
     spec = synthetic.CONFIGS[args.config]
+    for kv in args.path:
+        name, value = kv.split("=", 1)
+        _native.set_path_option(name, int(value))
     if args.objects:
         spec = synthetic.WorkloadSpec(**{**spec.__dict__, "n_objects": args.objects})
     if args.trees:
@@ -751,7 +754,8 @@ def run_ours(args, world, rank, local):
                           if 4 * N * spec.n_features > 126e6 else
                           "inputs L2-resident between steps (features 4NF bytes < 126 MB; a launch-bound size)"),
                    "parallelism": plan.parallelism(world), "shard": plan.shard,
-                   "launch": "CUDA graph replay of one predict" if graph is not None else "stream launches"},
+                   "launch": "CUDA graph replay of one predict" if graph is not None else "stream launches",
+                   **({"path_options": dict(kv.split("=", 1) for kv in args.path)} if args.path else {})},
         "verify": verify,
         "e2e": e2e,
         "e2e_pageable": e2e_pageable,
@@ -829,6 +833,8 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=65536)
     ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
                     help="replay a CUDA graph of one predict (auto: when a step is under 0.2 ms)")
+    ap.add_argument("--path", action="append", default=[], metavar="NAME=VALUE",
+                    help="force a planner choice (obt_set_path_option; A/B runs), e.g. --path desc_source=0")
     ap.add_argument("--refpkg-worker", nargs=5, help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.refpkg_worker:

@@ -37,7 +37,7 @@ const void* pick_fan(int di, int cmp, int leaf);
 #define OBT_WIDE_NIDX 8
 #endif
 constexpr int kWideIndexWarps = OBT_WIDE_NIDX;
-const void* pick_wide(int di, int cmp, int leaf);
+const void* pick_wide(int di, int cmp, int leaf, int dsrc);
 // K5 staged multi-output (fp32 records; depths 4/6/8/10, outputs 2..10)
 const void* pick_multi_staged(int di, int cmp, int c, int* di_out);
 

@@ -127,8 +127,10 @@ struct TilePlan {
 struct WidePlan {
   uint8_t* d_desc = nullptr;
   uint8_t* d_tables = nullptr;
-  int n_chunks = 0, tstages = 0, slots = 0;
-  size_t smem = 0;
+  std::vector<uint32_t> bank;  // [n_chunks][kWideChunkTrees][2 DI] descriptors for the parameter bank
+  int n_chunks = 0;
+  int tstages[2] = {0, 0}, slots[2] = {0, 0};  // per descriptor source (0 ring, 1 bank)
+  size_t smem[2] = {0, 0};
 };
 
 }  // namespace
@@ -1036,38 +1038,45 @@ int launch_fan(obt_model* m, const uint8_t* q, int64_t n, double* out, cudaStrea
 // K2w records for the 256-object tile, in the predict path's level order; null trees
 // (sentinel descriptors, -0.0 leaves) pad the last chunk.
 using obt::kWideChunkTrees;
-// Shared memory of K2w with ts table stages and ns descriptor/panel slots.
-size_t wide_smem(const obt_model* m, int ts, int ns) {
+// Shared memory of K2w with ts table stages and ns descriptor/panel slots (dsrc 1: the
+// descriptors travel in the kernel parameters, no descriptor ring).
+size_t wide_smem(const obt_model* m, int ts, int ns, int dsrc) {
   const int DI = m->depth_inst;
   return obt::kWideSmemSlack + (size_t)ts * obt::wide_tables_bytes(DI, m->leaf_storage) +
-         (size_t)ns * (obt::wide_desc_bytes(DI) + obt::wide_panel_bytes(kWideChunkTrees)) +
+         (size_t)ns * ((dsrc ? 0 : obt::wide_desc_bytes(DI)) + obt::wide_panel_bytes(kWideChunkTrees)) +
          (((size_t)m->n_features * obt::kWideTile + 15) & ~(size_t)15);
 }
 // Ring depths: 3 table stages (2 if that is all that fits) and as many descriptor /
 // panel slots as fit, up to 12 (the index warps' lead over the fold).
-bool wide_rings(const obt_model* m, int* ts, int* ns) {
+bool wide_rings(const obt_model* m, int dsrc, int* ts, int* ns) {
   for (int t = 3; t >= 2; --t) {
     int n = 12;
-    while (n >= 4 && wide_smem(m, t, n) > (size_t)m->smem_optin) --n;
+    while (n >= 4 && wide_smem(m, t, n, dsrc) > (size_t)m->smem_optin) --n;
     if (n >= 4) { *ts = t; *ns = n; return true; }
   }
   return false;
 }
+// Descriptor source of K2w: the parameter bank unless the path option asks for the ring.
+int wide_dsrc() { return opt(OPT_DESC_SOURCE) == 0 ? 0 : 1; }
 int build_wide_plan(obt_model* m, WidePlan& w) {
   const int DI = m->depth_inst;
   const uint32_t stride = obt::wide_table_stride(DI, m->leaf_storage);
-  if (!wide_rings(m, &w.tstages, &w.slots)) return OBT_E_UNSUPPORTED;
-  w.smem = wide_smem(m, w.tstages, w.slots);
+  for (int ds = 0; ds < 2; ++ds) {
+    if (!wide_rings(m, ds, &w.tstages[ds], &w.slots[ds])) return OBT_E_UNSUPPORTED;
+    w.smem[ds] = wide_smem(m, w.tstages[ds], w.slots[ds], ds);
+  }
   w.n_chunks = (m->n_trees + kWideChunkTrees - 1) / kWideChunkTrees;
   const uint32_t dpt = obt::kWideDescBytes(DI), db = obt::wide_desc_bytes(DI);
   const uint32_t tb = obt::wide_tables_bytes(DI, m->leaf_storage);
   const size_t nch = (size_t)std::max(w.n_chunks, 1);
   std::vector<uint8_t> hd(nch * db, 0), ht(nch * tb, 0);
   std::vector<uint32_t> words((size_t)DI * 2);
+  w.bank.assign(nch * kWideChunkTrees * 2 * DI, 0);
   for (int t = 0; t < w.n_chunks * kWideChunkTrees; ++t) {
     const int c = t / kWideChunkTrees, tl = t % kWideChunkTrees;
     tree_descriptors(m, t, obt::kWideTile, words.data(), true);
     std::memcpy(hd.data() + (size_t)c * db + (size_t)tl * dpt, words.data(), (size_t)DI * 8);
+    std::memcpy(w.bank.data() + (size_t)t * 2 * DI, words.data(), (size_t)DI * 8);
     uint8_t* leaf_dst = ht.data() + (size_t)c * tb + (size_t)tl * stride;
     if (t < m->n_trees) ordered_leaves(m, t, leaf_dst);
     else write_null_leaves(m, leaf_dst);
@@ -1096,38 +1105,52 @@ int get_wide_plan(obt_model* m, const WidePlan** out) {
 bool wide_eligible(const obt_model* m) {
   if (m->n_outputs > 1 || m->depth_inst > 8 || m->n_trees == 0) return false;
   int ts = 0, ns = 0;
-  if (!wide_rings(m, &ts, &ns)) return false;
-  if (!obt::pick_wide(m->depth_inst, m->compare_mode, m->leaf_storage)) return false;
+  if (!wide_rings(m, wide_dsrc(), &ts, &ns)) return false;
+  if (!obt::pick_wide(m->depth_inst, m->compare_mode, m->leaf_storage, wide_dsrc())) return false;
   if (opt(OPT_WIDE) == 0) return false;
   if (opt(OPT_WIDE) == 1) return true;
   return plan_tile(m, (int64_t)1 << 40) <= 512;
 }
 
 int launch_wide(obt_model* m, const uint8_t* q, int64_t n, double* out, cudaStream_t stream) {
-  const void* fn = obt::pick_wide(m->depth_inst, m->compare_mode, m->leaf_storage);
+  const int ds = wide_dsrc();
+  const void* fn = obt::pick_wide(m->depth_inst, m->compare_mode, m->leaf_storage, ds);
   if (!fn) return fail(OBT_E_UNSUPPORTED, "no K2w kernel for depth %d", m->depth_inst);
   const WidePlan* w = nullptr;
   int rc = get_wide_plan(m, &w);
   if (rc != OBT_OK) return rc;
-  obt::WideParams p{};
+  static thread_local obt::WideArgs<1> args;  // the driver copies the parameters at launch
+  obt::WideParams& p = args.p;
+  p = obt::WideParams{};
   p.q = q;
   p.desc = w->d_desc;
   p.tables = w->d_tables;
   p.out = out;
   p.n = n;
   p.n_tiles = (n + obt::kWideTile - 1) / obt::kWideTile;
-  p.n_chunks = w->n_chunks;
   p.q_tile_bytes = (uint32_t)((size_t)m->n_features * obt::kWideTile);
-  p.n_tstages = w->tstages;
-  p.n_slots = w->slots;
+  p.n_tstages = w->tstages[ds];
+  p.n_slots = w->slots[ds];
   p.scale = m->scale;
   p.bias = m->bias;
   CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, m->smem_optin));
-  void* kargs[] = {&p};
   const dim3 grid((unsigned)std::min<int64_t>(p.n_tiles, m->sm_count)),
       block(32 * (1 + obt::kWideIndexWarps + obt::kWideFoldWarps));
-  CUDA_TRY(cudaLaunchKernel(fn, grid, block, kargs, w->smem, stream));
-  ++g_launches;
+  // one launch (descriptor ring), or one per parameter bank of descriptors, the fold
+  // carried through `out` between launches
+  const int per = ds ? obt::wide_bank_chunks(m->depth_inst) : std::max(w->n_chunks, 1);
+  const int n_launch = std::max(1, (w->n_chunks + per - 1) / per);
+  const size_t per_chunk = (size_t)kWideChunkTrees * 2 * m->depth_inst;
+  for (int l = 0; l < n_launch; ++l) {
+    p.chunk_begin = l * per;
+    p.n_chunks = std::min(w->n_chunks, (l + 1) * per) - p.chunk_begin;
+    p.first = l == 0;
+    p.last = l == n_launch - 1;
+    if (ds) std::memcpy(args.desc, w->bank.data() + (size_t)p.chunk_begin * per_chunk, (size_t)p.n_chunks * per_chunk * 4);
+    void* kargs[] = {&args};
+    CUDA_TRY(cudaLaunchKernel(fn, grid, block, kargs, w->smem[ds], stream));
+    ++g_launches;
+  }
   return OBT_OK;
 }
 

@@ -56,16 +56,29 @@ struct WideParams {
   uint32_t q_tile_bytes;     // F * kWideTile
   int32_t n_tstages;         // table ring stages (<= kWideMaxTStages)
   int32_t n_slots;           // descriptor + index-panel ring slots (<= kWideMaxSlots)
+  int32_t chunk_begin;       // this launch folds chunks [chunk_begin, chunk_begin + n_chunks)
+  int32_t first, last;       // start the fold at 0 / finalize into predictions (else carry in out)
   double scale, bias;
 };
 
-// Warp-wide wait on the plain (potentially blocking) try_wait.  A suspend-time hint
-// (TRYWAIT / NANOSLEEP.SYNCS / PHASECHK loop) measured slower at config 4: 48.9 vs 48.2 ms.
+// Kernel arguments: DSRC 0 streams the descriptors through a shared-memory ring; DSRC 1
+// carries this launch's descriptors in the kernel-parameter bank (uniform LDCU loads:
+// no shared-memory wavefronts, and the bucket-word address takes the offset from a
+// uniform register), one launch per kWideBankChunks chunks, the fold carried in `out`.
+constexpr int kWideBankWords = (32760 - (int)sizeof(WideParams)) / 8 * 2;  // keeps the struct a multiple of 8 bytes
+__host__ __device__ constexpr int wide_bank_chunks(int di) { return kWideBankWords / (kWideChunkTrees * 2 * di); }
+template <int DSRC> struct WideArgs;
+template <> struct WideArgs<0> { WideParams p; };
+template <> struct WideArgs<1> { WideParams p; uint32_t desc[kWideBankWords]; };
+static_assert(sizeof(WideArgs<1>) <= 32764, "kernel parameter space");
+
+// Warp-wide wait on the plain (potentially blocking) try_wait.  A suspend-time hint (a
+// TRYWAIT / NANOSLEEP.SYNCS / PHASECHK loop) measured slower at config 4 (48.9 vs 48.2
+// ms), and so did a nanosleep back-off in the fold warps' waits (200 ns: 47.74 vs 47.28).
 __device__ __forceinline__ void wide_wait(uint64_t* bar, uint32_t parity) {
   while (!__all_sync(0xffffffffu, mbar_try(bar, parity))) {
   }
 }
-
 // Shared-memory layout (2048-byte aligned base):
 //   table ring           TS x kWideChunkTrees tables (each stride-aligned, so a gather
 //                        address is one LOP3: (shifted index & mask) | table base, plus
@@ -105,8 +118,9 @@ struct RingPos {
   }
 };
 
-template <int DI, int CMP, int LEAF, int NIDX>
-__global__ void __launch_bounds__(32 * (1 + NIDX + kWideFoldWarps), 1) apply_wide_kernel(const __grid_constant__ WideParams p) {
+template <int DI, int CMP, int LEAF, int NIDX, int DSRC>
+__global__ void __launch_bounds__(32 * (1 + NIDX + kWideFoldWarps), 1) apply_wide_kernel(const __grid_constant__ WideArgs<DSRC> args) {
+  const WideParams& p = args.p;
   static_assert(DI >= 1 && DI <= 8, "K2w: one index byte per object");
   using LT = LeafT<LEAF>;
   using acc_t = typename LT::Acc;
@@ -117,8 +131,8 @@ __global__ void __launch_bounds__(32 * (1 + NIDX + kWideFoldWarps), 1) apply_wid
   unsigned char* smem = smem_raw + ((kWideSmemAlign - (smem_u32(smem_raw) & (kWideSmemAlign - 1u))) & (kWideSmemAlign - 1u));
   const int TS = p.n_tstages, NS = p.n_slots;
   unsigned char* tstages = smem;                                      // TS x kTablesBytes (stride-aligned)
-  unsigned char* descs = tstages + (size_t)TS * kTablesBytes;         // NS x kDescBytes
-  unsigned char* panels = descs + (size_t)NS * kDescBytes;            // NS x kPanelBytes
+  unsigned char* descs = tstages + (size_t)TS * kTablesBytes;         // NS x kDescBytes (DSRC 0)
+  unsigned char* panels = descs + (DSRC == 0 ? (size_t)NS * kDescBytes : 0);  // NS x kPanelBytes
   unsigned char* qtile = panels + (size_t)NS * kPanelBytes;           // q_tile_bytes
   uint64_t* bars = reinterpret_cast<uint64_t*>(qtile + ((p.q_tile_bytes + 15u) & ~15u));
   uint64_t* tfull = bars;                          // [TS] tables landed
@@ -152,7 +166,7 @@ __global__ void __launch_bounds__(32 * (1 + NIDX + kWideFoldWarps), 1) apply_wid
   const int nc = p.n_chunks;
 
   if (warp == 0) {
-    if (lane == 0) {
+    if (lane == 0 && DSRC == 0) {
       // descriptors, NS chunks ahead of the fold: index warps run ahead of the fold by
       // up to NS chunks, decoupled from the (larger) table ring
       RingPos r;
@@ -160,7 +174,8 @@ __global__ void __launch_bounds__(32 * (1 + NIDX + kWideFoldWarps), 1) apply_wid
         for (int c = 0; c < nc; ++c) {
           if (i > 0 || c >= NS) mbar_wait(&sfree[r.slot], r.phase ^ 1u);
           mbar_expect_tx(&dfull[r.slot], kDescBytes);
-          bulk_g2s(descs + (size_t)r.slot * kDescBytes, p.desc + (size_t)c * kDescBytes, kDescBytes, &dfull[r.slot]);
+          bulk_g2s(descs + (size_t)r.slot * kDescBytes, p.desc + (size_t)(p.chunk_begin + c) * kDescBytes, kDescBytes,
+                   &dfull[r.slot]);
           r.next(NS);
         }
       }
@@ -180,8 +195,8 @@ __global__ void __launch_bounds__(32 * (1 + NIDX + kWideFoldWarps), 1) apply_wid
         for (int c = 0; c < nc; ++c) {
           if (i > 0 || c >= TS) mbar_wait(&tfree[r.slot], r.phase ^ 1u);
           mbar_expect_tx(&tfull[r.slot], kTablesBytes);
-          bulk_g2s_split(tstages + (size_t)r.slot * kTablesBytes, p.tables + (size_t)c * kTablesBytes, kTablesBytes,
-                         &tfull[r.slot]);
+          bulk_g2s_split(tstages + (size_t)r.slot * kTablesBytes, p.tables + (size_t)(p.chunk_begin + c) * kTablesBytes,
+                         kTablesBytes, &tfull[r.slot]);
           r.next(TS);
         }
       }
@@ -201,7 +216,11 @@ __global__ void __launch_bounds__(32 * (1 + NIDX + kWideFoldWarps), 1) apply_wid
     for (int64_t i = 0; i < n_my_tiles; ++i) {
       wide_wait(tile_full, (uint32_t)(i & 1));
       for (int c = 0; c < nc; ++c) {
-        wide_wait(&dfull[r.slot], r.phase);
+        if constexpr (DSRC == 0) {
+          wide_wait(&dfull[r.slot], r.phase);
+        } else if (i > 0 || c >= NS) {
+          wide_wait(&sfree[r.slot], r.phase ^ 1u);  // the fold is done with this panel slot
+        }
         const unsigned char* st = descs + (size_t)r.slot * kDescBytes;
         const uint32_t panel = smem_u32(panels + (size_t)r.slot * kPanelBytes) + 4u * obj0;
         for (; rr < kWideGroups; rr += NIDX) {
@@ -213,11 +232,17 @@ __global__ void __launch_bounds__(32 * (1 + NIDX + kWideFoldWarps), 1) apply_wid
             // descriptors: DI pairs {off, k replicated} (7-bit) or {(off << 8) | k, s}
             // (8-bit), two pairs per broadcast LDS.128
             uint32_t dw[2 * DI + 2];
-            const uint4* dsrc = reinterpret_cast<const uint4*>(st + (size_t)t * kWideDescBytes(DI));
+            if constexpr (DSRC == 0) {
+              const uint4* dsrc = reinterpret_cast<const uint4*>(st + (size_t)t * kWideDescBytes(DI));
 #pragma unroll
-            for (int v = 0; v < (DI + 1) / 2; ++v) {
-              const uint4 q4 = dsrc[v];
-              dw[4 * v + 0] = q4.x; dw[4 * v + 1] = q4.y; dw[4 * v + 2] = q4.z; dw[4 * v + 3] = q4.w;
+              for (int v = 0; v < (DI + 1) / 2; ++v) {
+                const uint4 q4 = dsrc[v];
+                dw[4 * v + 0] = q4.x; dw[4 * v + 1] = q4.y; dw[4 * v + 2] = q4.z; dw[4 * v + 3] = q4.w;
+              }
+            } else {
+              const uint32_t* bank = args.desc + ((size_t)c * kWideChunkTrees + t) * (2 * DI);
+#pragma unroll
+              for (int v = 0; v < 2 * DI; ++v) dw[v] = bank[v];
             }
             uint32_t w0[DI], w1[DI];
 #pragma unroll
@@ -274,7 +299,9 @@ __global__ void __launch_bounds__(32 * (1 + NIDX + kWideFoldWarps), 1) apply_wid
   RingPos r, rt;
   for (int64_t i = 0; i < n_my_tiles; ++i) {
     const int64_t tile = blockIdx.x + i * gridDim.x;
-    acc_t acc = (acc_t)0;
+    const int64_t o = tile * kWideTile + ol;
+    // continue the fold of the previous launch (exact: the carry holds acc_t values)
+    acc_t acc = (p.first || o >= p.n) ? (acc_t)0 : (acc_t)p.out[o];
     for (int c = 0; c < nc; ++c) {
       wide_wait(&pfull[r.slot], r.phase);
       wide_wait(&tfull[rt.slot], rt.phase);
@@ -302,9 +329,8 @@ __global__ void __launch_bounds__(32 * (1 + NIDX + kWideFoldWarps), 1) apply_wid
       r.next(NS);
       rt.next(TS);
     }
-    const int64_t o = tile * kWideTile + ol;
     // finalize: f64(acc) * scale + bias, two roundings (evaluate.py:298-299)
-    if (o < p.n) p.out[o] = __dadd_rn(__dmul_rn((double)acc, p.scale), p.bias);
+    if (o < p.n) p.out[o] = p.last ? __dadd_rn(__dmul_rn((double)acc, p.scale), p.bias) : (double)acc;
   }
 }
 
