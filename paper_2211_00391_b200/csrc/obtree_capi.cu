@@ -1056,8 +1056,11 @@ bool wide_rings(const obt_model* m, int dsrc, int* ts, int* ns) {
   }
   return false;
 }
-// Descriptor source of K2w: the parameter bank unless the path option asks for the ring.
-int wide_dsrc() { return opt(OPT_DESC_SOURCE) == 0 ? 0 : 1; }
+// Descriptor source of K2w: the shared-memory ring (one launch) unless the path option
+// asks for the parameter bank.  The bank (16 launches at config 4, each re-reading the
+// 4 GB bucket matrix: 64 GB of DRAM reads per predict instead of 4) measured only 1.4%
+// faster (47.29 vs 47.95 ms), not worth 16x the HBM traffic.
+int wide_dsrc() { return opt(OPT_DESC_SOURCE) == 1 ? 1 : 0; }
 int build_wide_plan(obt_model* m, WidePlan& w) {
   const int DI = m->depth_inst;
   const uint32_t stride = obt::wide_table_stride(DI, m->leaf_storage);
