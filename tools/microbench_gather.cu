@@ -8,6 +8,11 @@
 //   MODE 2: 256-entry fp32 table, one LDS.32 per lane (the single-output fold), uniform
 //   MODE 3: 64-byte slots, plain order (rows 0..2), three LDS.128
 //   MODE 5: as MODE 4, rows 0-1 LDS.128 and row 2 LDS.64 (only the 40 bytes of C = 10)
+//   MODE 6: 48-byte records, entropy-ordered depth-10 indices (the most uncertain level
+//           in the lowest bit), three LDS.128
+//   MODE 7: entropy-ordered indices, ten SoA planes of 1024 fp32 (one LDS.32 per output)
+//   MODE 8: entropy-ordered indices, lane = (object j of 3, output c of 10): 30 lanes load
+//           word c of record j (48-byte stride), one LDS.32 per 3 objects
 //   MODE 4: 48-byte records, indices of a depth-10 oblivious tree with random splits:
 //           bit d set with probability p_d, p_d uniform per "tree" (shared by the warp)
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/microbench_gather tools/microbench_gather.cu
@@ -81,6 +86,47 @@ __global__ void __launch_bounds__(512, 1) k_gather(int n_instr_out) {
             acc0 += v.x; acc1 += v.y; acc2 += v.z; acc3 += v.w;
           }
         }
+      } else if constexpr (MODE >= 6) {
+        // per-tree level biases (warp-uniform) already in entropy order: |p_d - 1/2| grows
+        // with d (uniform order statistics of the distance), random side
+        uint32_t tr = mix((uint32_t)(it * 4 + u) * 2654435761u + blockIdx.x);
+        uint32_t pd[10];
+#pragma unroll
+        for (int d = 0; d < 10; ++d) {
+          tr = tr * 1664525u + 1013904223u;
+          const uint32_t dist = 51u * d + ((tr >> 10) % 51u);  // 0..510
+          pd[d] = (tr >> 31) ? 512u + dist : 512u - dist;
+        }
+        uint32_t id = 0;
+#pragma unroll
+        for (int d = 0; d < 10; ++d) {
+          h = h * 1664525u + 1013904223u;
+          id |= ((h >> 22) < pd[d] ? 1u : 0u) << d;
+        }
+        if constexpr (MODE == 6) {
+          const uint32_t rec = base + id * 48u;
+#pragma unroll
+          for (int r = 0; r < 3; ++r) {
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(rec + 16u * r));
+            acc0 += v.x; acc1 += v.y; acc2 += v.z; acc3 += v.w;
+          }
+        } else if constexpr (MODE == 7) {
+#pragma unroll
+          for (int c = 0; c < 10; ++c) {
+            float x;
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(base + 4096u * c + 4u * id));
+            acc0 += x;
+          }
+        } else {
+          // lanes 10j..10j+9 take object j's record: the object's id from lane 10j
+          const int j = lane / 10, c = lane % 10;
+          const uint32_t idj = __shfl_sync(0xffffffffu, id, j < 3 ? 10 * j : 0);
+          if (lane < 30) {
+            float x;
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(base + idj * 48u + 4u * c));
+            acc0 += x;
+          }
+        }
       } else if constexpr (MODE == 2) {
         const uint32_t a = base + (idx & 255u) * 4u;
         float x;
@@ -128,5 +174,8 @@ int main() {
   run<2>("256 x fp32 table, LDS.32", sms, 1);
   run<4>("48-B records, depth-10 random-split indices", sms, 3);
   run<5>("  same, third row as LDS.64 (40 bytes)", sms, 3);
+  run<6>("48-B records, entropy-ordered depth-10 indices", sms, 3);
+  run<7>("  same indices, 10 SoA planes, 10 x LDS.32", sms, 10);
+  run<8>("  same indices, lane = (object of 3, output): per 3 objects", sms, 1);
   return 0;
 }
