@@ -414,21 +414,34 @@ def reference_pkg_baseline(spec, x, budget_s: float) -> dict:
 
 
 def fp16_report(model, x, p16, device: int) -> dict:
-    """Config 3: the fp16-leaf predictions of the timed batch against the fp32-leaf ones
-    (reference oracle.py:57-92 metrics, flips at threshold 0, and the reference's bound
-    |scale| * T * max|leaf| * 2^-10 of test_acceptance.py:156)."""
+    """Config 3 (and --leaves fp16): the fp16-leaf predictions of the timed batch against
+    the fp32-leaf ones (reference oracle.py:57-92 metrics, flips at threshold 0, and the
+    reference's bound |scale| * T * max|leaf| * 2^-10 of test_acceptance.py:156); for a
+    multi-output model over every (object, output)."""
+    import numpy as np
+
     import paper_2211_00391_b200 as obt
 
-    ev32 = obt.Evaluator(model, obt.EvalConfig(strategy=obt.LeafStrategy.NAIVE), device=device)
-    p32 = ev32.predict_device(x).cpu().numpy()
-    p16 = p16.cpu().numpy()
+    if hasattr(model, "subset"):
+        from paper_2211_00391_b200 import multiclass
+
+        ev32 = multiclass.MultiOutputEvaluator(model, device=device)
+        from paper_2211_00391_b200.model import half_bank_values
+
+        halves, sat = half_bank_values(model.leaves)
+        max_abs, sat_count = float(np.max(np.abs(halves.astype(np.float64)))), sat
+    else:
+        ev32 = obt.Evaluator(model, obt.EvalConfig(strategy=obt.LeafStrategy.NAIVE), device=device)
+        bank = obt.build_leaf_bank(model, obt.LeafPrecision.BINARY16)
+        max_abs, sat_count = bank.max_abs_leaf, bank.saturation_count
+    p32 = ev32.predict_device(x).cpu().numpy().ravel()
+    p16 = p16.cpu().numpy().ravel()
     m = obt.deviation_metrics(p32, p16)
-    bank = obt.build_leaf_bank(model, obt.LeafPrecision.BINARY16)
-    bound = abs(model.scale) * model.n_trees * bank.max_abs_leaf * 2.0 ** -10
+    bound = abs(model.scale) * model.n_trees * max_abs * 2.0 ** -10
     return {"vs": "fp32-leaf (binary64-fold) predictions of the same timed batch", "objects": int(p16.size),
             "max_abs": m.max_abs, "mean_abs": m.mean_abs, "median_abs": m.median_abs, "rms": m.rms,
             "flips_at_0": obt.classification_flip_count(p32, p16, 0.0), "bound": bound,
-            "within_bound": bool(m.max_abs <= bound), "saturated_leaves": bank.saturation_count}
+            "within_bound": bool(m.max_abs <= bound), "saturated_leaves": sat_count}
 
 
 def run_reference(args, world, rank):
@@ -439,6 +452,9 @@ def run_reference(args, world, rank):
     from paper_2211_00391_b200 import synthetic
 
     spec = synthetic.CONFIGS[args.config]
+    if args.leaves:
+        spec = synthetic.WorkloadSpec(**{**spec.__dict__, "half_leaves": args.leaves == "fp16",
+                                         "name": spec.name + ("-fp16" if args.leaves == "fp16" else "")})
     if spec.n_outputs > 1:
         from paper_2211_00391_b200 import multiclass
 
@@ -550,6 +566,9 @@ def run_ours(args, world, rank, local):
         spec = synthetic.WorkloadSpec(**{**spec.__dict__, "n_objects": args.objects})
     if args.trees:
         spec = synthetic.WorkloadSpec(**{**spec.__dict__, "n_trees": args.trees})
+    if args.leaves:
+        spec = synthetic.WorkloadSpec(**{**spec.__dict__, "half_leaves": args.leaves == "fp16",
+                                         "name": spec.name + ("-fp16" if args.leaves == "fp16" else "")})
     device = local
     torch.cuda.set_device(device)
     plan = Plan(args, spec, world, rank)
@@ -559,7 +578,7 @@ def run_ours(args, world, rank, local):
         from paper_2211_00391_b200 import multiclass
 
         full_model = multiclass.from_arrays(synthetic.model_arrays(spec))
-        config = None
+        config = obt.EvalConfig(strategy=obt.LeafStrategy.NAIVE16) if spec.half_leaves else None
     else:
         full_model = synthetic.build_model(spec)
         config = obt.EvalConfig(strategy=obt.LeafStrategy.NAIVE16 if spec.half_leaves else obt.LeafStrategy.NAIVE)
@@ -570,7 +589,7 @@ def run_ours(args, world, rank, local):
         sharded = sharding.GridShardedEvaluator(full_model, *plan.grid, config=config, device=device)
         ev, group = sharded.trees.local_evaluator, sharded.trees.group
     elif multi:
-        ev = multiclass.MultiOutputEvaluator(full_model, device=device)
+        ev = multiclass.MultiOutputEvaluator(full_model, device=device, config=config)
     else:
         ev = obt.Evaluator(full_model, config, device=device)
     x = synthetic.device_features(spec, n_objects=plan.n, seed=plan.data_seed, device=f"cuda:{device}")
@@ -815,6 +834,8 @@ def main():
     ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--objects", type=int, default=0, help="override the configuration's object count")
     ap.add_argument("--trees", type=int, default=0, help="override the tree count (experiments)")
+    ap.add_argument("--leaves", choices=["fp32", "fp16"], default=None,
+                    help="leaf family override: fp16 = binary16 leaves folded in binary32 (config 3 is config 2 + fp16)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
                     help="objects: strong = the configuration's batch split over the GPUs (config 4's default), "

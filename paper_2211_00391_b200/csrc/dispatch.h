@@ -38,7 +38,8 @@ const void* pick_fan(int di, int cmp, int leaf);
 #endif
 constexpr int kWideIndexWarps = OBT_WIDE_NIDX;
 const void* pick_wide(int di, int cmp, int leaf, int dsrc);
-// K5 staged multi-output (fp32 records; depths 4/6/8/10, outputs 2..10)
-const void* pick_multi_staged(int di, int cmp, int c, int* di_out);
+// K5 staged multi-output (depths 4/6/8/10, outputs 2..10; leaf 1 = binary32 records,
+// 2 = binary16 records with binary32 accumulators)
+const void* pick_multi_staged(int di, int cmp, int c, int leaf, int* di_out);
 
 }  // namespace obt

@@ -374,8 +374,9 @@ int validate(const obt_model_desc* d) {
   if (d->n_trees < 0) return fail(OBT_E_INVALID, "invalid model: negative tree count");
   if (d->n_outputs < 1 || d->n_outputs > kMaxOutputs)
     return fail(OBT_E_UNSUPPORTED, "n_outputs=%d outside 1..%d", d->n_outputs, kMaxOutputs);
-  if (d->n_outputs > 1 && d->precision != OBT_PRECISION_BINARY64)
-    return fail(OBT_E_UNSUPPORTED, "multi-output models support the binary64 family only");
+  if (d->n_outputs > 1 && d->precision == OBT_PRECISION_BINARY16 && (d->n_outputs > 10 || d->max_depth > 10))
+    return fail(OBT_E_UNSUPPORTED,
+                "binary16 multi-output models run on the staged kernel: at most 10 outputs and depth 10");
   if (d->n_trees > 0 && (d->max_depth < 1 || d->max_depth > 16))
     return fail(OBT_E_INVALID, "invalid model: max_depth %d outside 1..16", d->max_depth);
   if (d->n_trees > 0 && instantiated_depth(d->max_depth) < 0)
@@ -1159,7 +1160,7 @@ int launch_wide(obt_model* m, const uint8_t* q, int64_t n, double* out, cudaStre
 
 int launch_multi_staged(obt_model* m, const uint8_t* q, int64_t n, double* out, cudaStream_t stream) {
   int di = 0;
-  const void* fn = obt::pick_multi_staged(m->depth_inst, m->compare_mode, m->n_outputs, &di);
+  const void* fn = obt::pick_multi_staged(m->depth_inst, m->compare_mode, m->n_outputs, m->leaf_storage, &di);
   if (!fn || di != m->depth_inst) return fail(OBT_E_UNSUPPORTED, "no staged multi-output kernel for depth %d", di);
   obt::StagedParams p{};
   p.q = q;
@@ -1447,24 +1448,27 @@ int obt_model_create(const obt_model_desc* d, int device, obt_model** out) {
   const size_t ls = leaf_size(m->leaf_storage);
   if (C > 1) {
     // multi-output records, one leaf's C values contiguous in 16-byte rows (K4, K5)
-    // K5 (staged tables and rows) for fp32 records, C <= 10, depth <= 10, when at least
-    // two stages (one tree's table + its bucket rows each) fit shared memory
+    // K5 (staged tables and rows) for binary32 or binary16 records, C <= 10, depth <= 10,
+    // when at least two stages (one tree's table + its bucket rows each) fit shared memory;
+    // the binary16 family runs nowhere else
     {
-      const int CPs = obt::staged_record_values(C);
-      const uint32_t table = (uint32_t)((per_tree * CPs * 4 + 15) / 16 * 16);
+      const int CPs = obt::staged_record_values(C, m->leaf_storage);
+      const uint32_t table = (uint32_t)((per_tree * CPs * ls + 15) / 16 * 16);
       const uint32_t stage = (table + (uint32_t)DI * obt::kStagedTile + 127u) & ~127u;
       const int stages = std::min(8, (int)(((size_t)m->smem_optin - 512) / stage));
       int sdi = 0;
-      const bool ok = m->leaf_storage == 1 && C <= 10 && stages >= 2 &&
-                      obt::pick_multi_staged(DI, m->compare_mode, C, &sdi) != nullptr && sdi == DI;
-      if (ok && opt(OPT_MULTI_STAGED) != 0) {
+      const bool ok = m->leaf_storage != 0 && C <= 10 && stages >= 2 &&
+                      obt::pick_multi_staged(DI, m->compare_mode, C, m->leaf_storage, &sdi) != nullptr && sdi == DI;
+      if (ok && (opt(OPT_MULTI_STAGED) != 0 || m->leaf_storage == 2)) {
         m->multi_staged = 1;
         m->staged_stages = stages;
         m->staged_table_bytes = table;
         m->staged_stage_bytes = stage;
       }
     }
-    m->multi_slot = m->multi_staged ? obt::staged_record_values(C) * (int)ls
+    if (m->leaf_storage == 2 && !m->multi_staged)
+      return fail(OBT_E_UNSUPPORTED, "binary16 multi-output model does not fit the staged kernel");
+    m->multi_slot = m->multi_staged ? obt::staged_record_values(C, m->leaf_storage) * (int)ls
                                     : obt::multi_record_values(m->leaf_storage, C) * (int)ls;
     // records in the predict path's level order (record j' holds reference leaf
     // reference_leaf(perm, DI, j'); entries past 2^D belong to sentinel levels, never read)
@@ -1476,8 +1480,16 @@ int obt_model_create(const obt_model_desc* d, int device, obt_model** out) {
           if (i >= per_tree_in) continue;
           const double v = d->leaves[(((size_t)t * C + c) << D) + i];
           uint8_t* dst = rec.data() + ((size_t)t * per_tree + j) * m->multi_slot + (size_t)c * ls;
-          if (m->leaf_storage == 0) std::memcpy(dst, &v, 8);
-          else { const float f = (float)v; std::memcpy(dst, &f, 4); }
+          if (m->leaf_storage == 0) {
+            std::memcpy(dst, &v, 8);
+          } else if (m->leaf_storage == 1) {
+            const float f = (float)v;
+            std::memcpy(dst, &f, 4);
+          } else {
+            // the binary16 bank (model.py:262-268): the caller's bits, or RNE + saturation
+            const uint16_t h = d->leaves_f16 ? d->leaves_f16[(((size_t)t * C + c) << D) + i] : half_bank_entry(v);
+            std::memcpy(dst, &h, 2);
+          }
         }
     CUDA_TRY(cudaMalloc(&m->d_multi_leaves, rec.size()));
     CUDA_TRY(cudaMemcpy(m->d_multi_leaves, rec.data(), rec.size(), cudaMemcpyHostToDevice));

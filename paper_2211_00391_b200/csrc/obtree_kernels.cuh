@@ -1678,7 +1678,7 @@ __global__ void __launch_bounds__(kMultiThreads, multi_min_blocks(LEAF, C)) appl
       if (obj_of(k) >= p.n) continue;
 #pragma unroll
       for (int c = 0; c < C; ++c)
-        p.out[obj_of(k) * C + c] = p.last ? __dadd_rn(__dmul_rn(acc[k][c], p.scale), p.bias) : acc[k][c];
+        p.out[obj_of(k) * C + c] = p.last ? __dadd_rn(__dmul_rn((double)acc[k][c], p.scale), p.bias) : (double)acc[k][c];
     }
   }
 }
@@ -1693,18 +1693,21 @@ __global__ void __launch_bounds__(kMultiThreads, multi_min_blocks(LEAF, C)) appl
 // shared memory only: one table load serves 2048 objects (24 B of L2 traffic per
 // object-tree instead of a 48-byte record fetch), and every load the fold waits on is a
 // shared-memory load.  Descriptors come from the K4 array ({f * 512, k} / {(f*512) << 8 | k, s}).
-#ifndef OBT_STAGED_ODD
-// K5 records with an odd stride (C or C + 1 fp32 values) read as 4-byte loads, so the
-// 32 lanes' records start on all 32 banks: measured 441 vs 334 ms at config 5 (ten
-// loads of ~3.5 wavefronts each cost more than three 16-byte loads of ~10)
-#define OBT_STAGED_ODD 0
-#endif
-__host__ __device__ constexpr int staged_record_values(int c) {
-  return OBT_STAGED_ODD ? (c % 2 ? c : c + 1) : (c + 3) / 4 * 4;
+// K5 record: one leaf's C values.  Binary64 family: binary32 values in 16-byte rows (C
+// rounded up to 4; a 48-byte record at C = 10 puts row r of record i in 16-byte bank
+// group (3i + r) mod 8, all eight reachable).  Binary16 family: two values per 32-bit word
+// (the half2 packing of PAPER.md:414, "combine 16-bit numbers into 32- or 64-bit words")
+// in an ODD number of 8-byte units read with 8-byte loads, so a random record's unit u
+// lands in 8-byte group (units * i + u) mod 16, every group reachable -- 32-byte records
+// (even stride) reach only even groups and measured 371 vs 273 ms at config 5.  Measured
+// and dropped for binary32 (round 1): odd-stride records read with 4-byte loads (441 vs
+// 334 ms) and 8-byte loads of the C values (472 vs 334 ms).
+__host__ __device__ constexpr int staged_half_units(int c) {
+  return ((2 * c + 7) / 8) % 2 ? (2 * c + 7) / 8 : (2 * c + 7) / 8 + 1;
 }
-#ifndef OBT_STAGED_V2
-#define OBT_STAGED_V2 0  // K5 record reads as 8-byte loads (C values) instead of 16-byte rows
-#endif
+__host__ __device__ constexpr int staged_record_values(int c, int leaf) {
+  return leaf == 2 ? 4 * staged_half_units(c) : (c + 3) / 4 * 4;
+}
 constexpr int kStagedThreadsConsumers = 512;
 constexpr int kStagedTile = 4 * kStagedThreadsConsumers;  // 2048 objects
 constexpr int kStagedThreads = kStagedThreadsConsumers + 32;
@@ -1712,7 +1715,7 @@ constexpr int kStagedThreads = kStagedThreadsConsumers + 32;
 struct StagedParams {
   const uint8_t* q;          // tiled buckets [n_tiles][F][2048]
   const uint32_t* desc;      // K4 descriptors [T][DI][2] (tile 512 offsets)
-  const float* leaves;       // [T][2^DI][CP] fp32 records
+  const float* leaves;       // [T][2^DI] records of CP binary32 (or binary16) values
   double* out;               // [n][C]
   int64_t n;
   int32_t n_features;
@@ -1724,10 +1727,13 @@ struct StagedParams {
   double scale, bias;
 };
 
-template <int DI, int CMP, int C>
+template <int DI, int CMP, int C, int LEAF>
 __global__ void __launch_bounds__(kStagedThreads, 1) apply_multi_staged_kernel(const __grid_constant__ StagedParams p) {
-  constexpr int CP = staged_record_values(C);
-  constexpr int kRows = CP / 4;
+  static_assert(LEAF == 1 || LEAF == 2, "K5: binary32 or binary16 records");
+  constexpr int CP = staged_record_values(C, LEAF);
+  constexpr int kRecBytes = CP * (LEAF == 2 ? 2 : 4);
+  constexpr int kRows = LEAF == 2 ? 0 : kRecBytes / 16;
+  using acc_t = typename LeafT<LEAF>::Acc;  // binary64 / binary32 fold
   extern __shared__ __align__(128) unsigned char st_raw[];
   unsigned char* smem = st_raw + ((128u - (smem_u32(st_raw) & 127u)) & 127u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [S]
@@ -1747,46 +1753,87 @@ __global__ void __launch_bounds__(kStagedThreads, 1) apply_multi_staged_kernel(c
   const uint8_t* qtile = p.q + tile_idx * (int64_t)p.n_features * kStagedTile;
   const int warp_id = __shfl_sync(0xffffffffu, tid / 32, 0);
   if (warp_id == 0) {
-    if (tid == 0) {
-      for (int i = 0; i < n_trees; ++i) {
-        const int t = p.tree_begin + i;
-        const int s = i % p.n_stages;
-        if (i >= p.n_stages) mbar_wait(&empty[s], (uint32_t)(i / p.n_stages - 1) & 1u);
-        unsigned char* dst = stages + (size_t)s * p.stage_bytes;
-        mbar_expect_tx(&full[s], p.table_bytes + (uint32_t)DI * kStagedTile);
-        bulk_g2s_split(dst, p.leaves + ((size_t)t << DI) * CP, p.table_bytes, &full[s]);
-        const uint2* ds = reinterpret_cast<const uint2*>(p.desc) + (size_t)t * DI;
-#pragma unroll
+    // producer warp: lane d < DI copies the bucket row of depth d (its descriptor loaded
+    // one tree ahead, so no global-load latency sits between a stage's release and its
+    // refill), lane 0 the tree's record table and the stage's expect_tx.  Row copies may
+    // complete before lane 0's arrive.expect_tx: the phase needs that arrival anyway.
+    // Measured at config 5: binary16 records 196 ms with per-lane row copies vs 251 ms
+    // with one thread issuing every copy; binary32 records the other way round (289 vs
+    // 266 ms), so the binary32 family keeps the single issuing thread.
+    constexpr bool kSerial = LEAF == 1;
+    const int lane = tid;
+    if (kSerial && lane > 0) return;
+    const uint2* desc = reinterpret_cast<const uint2*>(p.desc);
+    uint2 dd = lane < DI && n_trees > 0 ? __ldg(desc + (size_t)p.tree_begin * DI + lane) : make_uint2(0u, 0u);
+    for (int i = 0; i < n_trees; ++i) {
+      const int t = p.tree_begin + i;
+      const int s = i % p.n_stages;
+      const uint2 next = lane < DI && i + 1 < n_trees ? __ldg(desc + (size_t)(t + 1) * DI + lane) : make_uint2(0u, 0u);
+      if (i >= p.n_stages) {
+        if (lane == 0) mbar_wait(&empty[s], (uint32_t)(i / p.n_stages - 1) & 1u);
+        if (!kSerial) __syncwarp();
+      }
+      unsigned char* dst = stages + (size_t)s * p.stage_bytes;
+      if (kSerial) {
+        const uint2* ds = desc + (size_t)t * DI;
         for (int d = 0; d < DI; ++d) {
-          const uint2 dd = __ldg(ds + d);
-          const uint32_t off512 = CMP == 7 ? dd.x : (dd.x >> 8);  // f * 512 (sentinel splits: 0)
+          const uint2 e = __ldg(ds + d);
+          const uint32_t off512 = CMP == 7 ? e.x : (e.x >> 8);
           bulk_g2s(dst + p.table_bytes + (size_t)d * kStagedTile, qtile + (size_t)(off512 / 512u) * kStagedTile,
                    kStagedTile, &full[s]);
         }
+      } else if (lane < DI) {
+        const uint32_t off512 = CMP == 7 ? dd.x : (dd.x >> 8);  // f * 512 (sentinel splits: 0)
+        bulk_g2s(dst + p.table_bytes + (size_t)lane * kStagedTile, qtile + (size_t)(off512 / 512u) * kStagedTile,
+                 kStagedTile, &full[s]);
       }
+      if (lane == 0) {
+        mbar_expect_tx(&full[s], p.table_bytes + (uint32_t)DI * kStagedTile);
+        // tree t's records: 2^DI x kRecBytes = table_bytes (no padding between trees)
+        bulk_g2s_split(dst, reinterpret_cast<const unsigned char*>(p.leaves) + (size_t)t * p.table_bytes, p.table_bytes,
+                       &full[s]);
+      }
+      dd = next;
     }
     return;
   }
   const int word = tid - 32;  // bucket word of this thread: objects word_object(.., word, k)
   const int64_t tile_base = tile_idx * kStagedTile;
   auto obj_of = [&](int k) { return word_object(tile_base, word, k); };
-  double acc[4][C];
+  acc_t acc[4][C];
 #pragma unroll
   for (int k = 0; k < 4; ++k)
 #pragma unroll
-    for (int c = 0; c < C; ++c) acc[k][c] = (p.first || obj_of(k) >= p.n) ? 0.0 : p.out[obj_of(k) * C + c];
+    for (int c = 0; c < C; ++c) acc[k][c] = (p.first || obj_of(k) >= p.n) ? (acc_t)0 : (acc_t)p.out[obj_of(k) * C + c];
   const uint32_t stages_s = smem_u32(stages);
+  // the binary16 family (40 binary32 accumulators) has the registers to load the next
+  // tree's descriptors while this tree folds; the binary64 family (80) loads them per tree
+  constexpr bool kPrefetch = LEAF == 2;
+  const uint2* desc = reinterpret_cast<const uint2*>(p.desc);
+  uint2 dnext[kPrefetch ? DI : 1];
+  if constexpr (kPrefetch) {
+#pragma unroll
+    for (int d = 0; d < DI; ++d) dnext[d] = n_trees > 0 ? __ldg(desc + (size_t)p.tree_begin * DI + d) : make_uint2(0u, 0u);
+  }
   for (int i = 0; i < n_trees; ++i) {
     const int t = p.tree_begin + i;
     const int s = i % p.n_stages;
+    uint2 dcur[kPrefetch ? DI : 1];
+    if constexpr (kPrefetch) {
+#pragma unroll
+      for (int d = 0; d < DI; ++d) {
+        dcur[d] = dnext[d];
+        dnext[d] = i + 1 < n_trees ? __ldg(desc + (size_t)(t + 1) * DI + d) : make_uint2(0u, 0u);
+      }
+    }
     mbar_wait_warp(&full[s], (uint32_t)(i / p.n_stages) & 1u);
     const uint32_t tab = stages_s + (uint32_t)s * p.stage_bytes;
     const uint32_t rows = tab + p.table_bytes + 4u * (uint32_t)word;
-    const uint2* ds = reinterpret_cast<const uint2*>(p.desc) + (size_t)t * DI;
+    const uint2* ds = desc + (size_t)t * DI;
     uint32_t lo = 0, hi = 0;
 #pragma unroll
     for (int d = 0; d < DI; ++d) {
-      const uint2 dd = __ldg(ds + d);  // warp-uniform: one broadcast
+      const uint2 dd = kPrefetch ? dcur[kPrefetch ? d : 0] : __ldg(ds + d);  // warp-uniform: one broadcast
       const uint32_t w = lds_u32(rows + (uint32_t)d * kStagedTile);
       uint32_t b7;
       if constexpr (CMP == 7) {
@@ -1800,27 +1847,38 @@ __global__ void __launch_bounds__(kStagedThreads, 1) apply_multi_staged_kernel(c
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const uint32_t idx = ((lo >> (8 * k)) & 0xffu) | (DI > 8 ? ((hi >> (8 * k)) & 0xffu) << 8 : 0u);
-      const uint32_t rec = tab + idx * (uint32_t)(CP * 4);
-      float v[CP];
-      if constexpr (OBT_STAGED_ODD) {
-        // odd record stride: value c of 32 random records spreads over all 32 banks
-#pragma unroll
-        for (int c = 0; c < C; ++c) v[c] = lds_leaf<1>(rec + 4u * c);
-      } else if constexpr (OBT_STAGED_V2) {
-        // 8-byte loads of the C values only (no padding read): half-warp phases
-#pragma unroll
-        for (int r = 0; r < (C + 1) / 2; ++r)
-          asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v[2 * r]), "=f"(v[2 * r + 1]) : "r"(rec + 8u * r));
-      } else {
+      const uint32_t rec = tab + idx * (uint32_t)kRecBytes;
+      if constexpr (LEAF == 1) {
+        float v[CP];
 #pragma unroll
         for (int r = 0; r < kRows; ++r) {
           asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                        : "=f"(v[4 * r]), "=f"(v[4 * r + 1]), "=f"(v[4 * r + 2]), "=f"(v[4 * r + 3])
                        : "r"(rec + 16u * r));
         }
-      }
 #pragma unroll
-      for (int c = 0; c < C; ++c) acc[k][c] += (double)v[c];
+        for (int c = 0; c < C; ++c) acc[k][c] += (double)v[c];
+      } else {
+        // binary16 pairs, 8-byte units; the last unit loads only the word that holds values
+        constexpr int kWords = (C + 1) / 2;
+        uint32_t w[CP / 2];
+#pragma unroll
+        for (int u = 0; u < (kWords + 1) / 2; ++u) {
+          if (2 * u + 1 < kWords) {
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w[2 * u]), "=r"(w[2 * u + 1]) : "r"(rec + 8u * u));
+          } else {
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w[2 * u]) : "r"(rec + 8u * u));
+          }
+        }
+        // widen each pair to binary32 and fold two outputs per packed FADD2 (two
+        // independent round-to-nearest adds: the bits of two FADDs)
+#pragma unroll
+        for (int c = 0; c + 1 < C; c += 2) {
+          const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[c / 2]));
+          fadd2(acc[k][c], acc[k][c + 1], f.x, f.y);
+        }
+        if constexpr (C % 2) acc[k][C - 1] += __half2float(__ushort_as_half((unsigned short)(w[C / 2] & 0xffffu)));
+      }
     }
     mbar_arrive(&empty[s]);
   }
@@ -1829,7 +1887,7 @@ __global__ void __launch_bounds__(kStagedThreads, 1) apply_multi_staged_kernel(c
     if (obj_of(k) >= p.n) continue;
 #pragma unroll
     for (int c = 0; c < C; ++c)
-      p.out[obj_of(k) * C + c] = p.last ? __dadd_rn(__dmul_rn(acc[k][c], p.scale), p.bias) : acc[k][c];
+      p.out[obj_of(k) * C + c] = p.last ? __dadd_rn(__dmul_rn((double)acc[k][c], p.scale), p.bias) : (double)acc[k][c];
   }
 }
 

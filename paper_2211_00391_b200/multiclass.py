@@ -5,6 +5,14 @@ SPEC.md:15), so this module extends its semantics the natural way, as the CPU
 restatement in oracle/ does: every tree has one leaf table per output,
 all outputs share the tree's splits, each output folds its leaves in tree order in
 binary64, and prediction[o][c] = scale * sum_t leaf[t][c][index_t(o)] + bias.
+
+The binary16 family (``EvalConfig(strategy=NAIVE16 | PERMUTE16)``) extends the same way:
+each output's leaves go through the reference's binary16 bank (model.py:262-268: RNE,
+saturation to +/-65504) and fold in binary32 (accumulate.py:94-97) -- the multiclass
+FP16 permutation the paper leaves as future work ("if each leaf holds 2 or
+4 values, combine the 16-bit numbers into 32- or 64-bit words").  On the GPU a leaf's C
+binary16 values sit two per 32-bit word in one record, and the fold adds two outputs
+per packed FADD2.
 """
 
 from __future__ import annotations
@@ -16,8 +24,9 @@ from typing import Optional
 import numpy as np
 
 from . import _checks, _native
+from .config import EvalConfig, LeafPrecision
 from .matrix import FeatureMatrix, Layout, layout_code
-from .model import MAX_BORDERS
+from .model import MAX_BORDERS, half_bank_values
 
 MAX_MULTI_DEPTH = 12
 MAX_OUTPUTS = 16
@@ -99,10 +108,15 @@ class MultiOutputModel:
 
 
 class MultiOutputEvaluator:
-    """A multi-output model resident on one GPU (K4 multi-output apply kernel)."""
+    """A multi-output model resident on one GPU (K5 staged kernel, K4 where K5 does not
+    apply).  ``config`` selects the precision family as EvalConfig does for one output
+    (evaluate.py:106-135): NAIVE / GATHER / PERMUTE64 binary64, NAIVE16 / PERMUTE16
+    binary16 (depth <= 10 and <= 10 outputs)."""
 
-    def __init__(self, model: MultiOutputModel, device: Optional[int] = None):
+    def __init__(self, model: MultiOutputModel, device: Optional[int] = None, config: Optional[EvalConfig] = None):
         model.require_valid()
+        self.config = config if config is not None else EvalConfig()
+        self.precision = self.config.strategy.precision
         lib = _native.require_gpu()
         import torch
 
@@ -114,7 +128,9 @@ class MultiOutputEvaluator:
         for f, b in enumerate(model.borders):
             borders[f, : b.size] = b
         so = model.split_ordinal.astype(np.uint8)
-        keep = (counts, borders, model.split_feature, so, model.leaves)
+        half = self.precision is LeafPrecision.BINARY16
+        bank = np.ascontiguousarray(half_bank_values(model.leaves)[0].view(np.uint16)) if half else None
+        keep = (counts, borders, model.split_feature, so, model.leaves, bank)
         desc = _native.ModelDesc()
         desc.n_features, desc.n_trees = model.n_features, model.n_trees
         desc.max_depth, desc.n_outputs = model.depth if model.n_trees else 0, model.n_outputs
@@ -122,8 +138,9 @@ class MultiOutputEvaluator:
         desc.split_feature = model.split_feature.ctypes.data if model.n_trees else None
         desc.split_ordinal = so.ctypes.data if model.n_trees else None
         desc.leaves = model.leaves.ctypes.data if model.n_trees else None
-        desc.leaves_f16 = None
-        desc.scale, desc.bias, desc.precision = model.scale, model.bias, _native.PRECISION_BINARY64
+        desc.leaves_f16 = bank.ctypes.data if half and model.n_trees else None
+        desc.scale, desc.bias = model.scale, model.bias
+        desc.precision = _native.PRECISION_BINARY16 if half else _native.PRECISION_BINARY64
         handle = ctypes.c_void_p()
         _native.check(lib.obt_model_create(ctypes.byref(desc), self.device, ctypes.byref(handle)))
         del keep

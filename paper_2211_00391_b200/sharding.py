@@ -110,7 +110,7 @@ class ObjectShardedEvaluator:
             if hasattr(model, "subset"):  # a multi-output model (config 5): [n][C] scores per shard
                 from .multiclass import MultiOutputEvaluator
 
-                ev = MultiOutputEvaluator(model, device=device)
+                ev = MultiOutputEvaluator(model, device=device, config=config)
             else:
                 from .evaluate import Evaluator
 
@@ -204,7 +204,7 @@ class TreeShardedEvaluator:
             if hasattr(self.submodel, "subset"):
                 from .multiclass import MultiOutputEvaluator
 
-                ev = MultiOutputEvaluator(self.submodel, device=device)
+                ev = MultiOutputEvaluator(self.submodel, device=device, config=config)
             else:
                 from .evaluate import Evaluator
 

@@ -13,7 +13,7 @@ import pytest
 
 import oracle
 import paper_2211_00391_b200 as obt
-from paper_2211_00391_b200 import stages, synthetic
+from paper_2211_00391_b200 import _native, stages, synthetic
 
 pytestmark = pytest.mark.gpu
 
@@ -327,6 +327,47 @@ def test_multi_output_bit_exact(paths, kernel, D, C, F, B):
     paths(leaf_storage=0)
     ev64 = multiclass.MultiOutputEvaluator(model)
     assert np.array_equal(ev64.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR)), want)
+
+
+@pytest.mark.parametrize("D,C,F,B", [(10, 10, 40, 254), (6, 3, 17, 64), (8, 8, 9, 128), (3, 2, 5, 7),
+                                     (10, 9, 33, 100), (4, 5, 8, 200), (10, 4, 2, 254), (8, 7, 12, 16)])
+def test_multi_output_binary16_half2_records(D, C, F, B):
+    """The binary16 family for multi-output models (EvalConfig NAIVE16): each output's
+    leaves through the reference's binary16 bank (RNE, +-65504 saturation) and a
+    binary32 fold; on the GPU the records pack two binary16 outputs per word (half2) and
+    fold two outputs per FADD2.  Bit-exact against the oracle's BINARY16 evaluation,
+    both layouts, including saturated leaves."""
+    from paper_2211_00391_b200 import multiclass
+
+    spec = synthetic.WorkloadSpec("m", 1, F, B, 57, D, 0.01, n_outputs=C, cfg=5)
+    arrays = synthetic.model_arrays(spec, seed=D * 100 + C + 7, affine=True)
+    arrays["leaves"][0, 0, :2] = (7.0e4, -9.0e4)   # saturate to +-65504 (model.py:262-268)
+    arrays["leaves"][1, C - 1, 3] = np.inf
+    model = multiclass.from_arrays(arrays)
+    x = _features(obt.ObliviousModel(tuple(obt.FloatFeatureBorders(f, b) for f, b in enumerate(arrays["borders"])),
+                                      (), 1.0, 0.0), 4097, seed=D + C + 1)
+    fm = oracle.FlatModel(np.stack(arrays["borders"]), np.full(F, B, np.int32), np.full(57, D, np.int32),
+                          arrays["split_feature"], arrays["split_ordinal"], arrays["leaves"], model.scale, model.bias)
+    want = oracle.evaluate_scalar(fm, x, oracle.OBJECT_MAJOR, oracle.BINARY16)
+    ev = multiclass.MultiOutputEvaluator(model, config=obt.EvalConfig(strategy=obt.LeafStrategy.NAIVE16))
+    assert ev.leaf_storage == "fp16" and ev.apply_kernel() == "staged"
+    got = ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
+    assert got.shape == (4097, C)
+    assert np.array_equal(got, want), int(np.count_nonzero(got != want))
+    dev = ev.predict_device(torch.from_numpy(np.ascontiguousarray(x.T)).cuda(), obt.Layout.FEATURE_MAJOR).cpu().numpy()
+    assert np.array_equal(dev, want)
+
+
+def test_multi_output_binary16_limits():
+    """The binary16 multi-output family runs on the staged kernel only: more than 10
+    outputs or depth above 10 are refused with a message, not run elsewhere."""
+    from paper_2211_00391_b200 import multiclass
+
+    for D, C in ((12, 3), (6, 12)):
+        spec = synthetic.WorkloadSpec("m", 1, 6, 16, 9, D, 0.01, n_outputs=C, cfg=5)
+        model = multiclass.from_arrays(synthetic.model_arrays(spec, seed=3))
+        with pytest.raises(_native.NativeError, match="binary16 multi-output"):
+            multiclass.MultiOutputEvaluator(model, config=obt.EvalConfig(strategy=obt.LeafStrategy.NAIVE16))
 
 
 def test_multi_output_tree_shard_partials_sum_to_prediction():
