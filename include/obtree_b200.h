@@ -112,6 +112,9 @@ int obt_model_multi_kernel(const obt_model* model, int32_t* kind);
  *   "lut_cells"    256, 512, 1024 cells per feature table (read by obt_model_create)
  *   "leaf_storage" 0: binary64 tables even when binary32 is exact (obt_model_create)
  *   "multi_staged" 0 / 1 K4 / K5 for multi-output models (obt_model_create)
+ *   "leaf_select"  1: K2 takes leaves by warp shuffle from a register-resident table
+ *                  (binary16 depth <= 6, binary32 depth <= 5; the PERMUTE16 / PERMUTE64
+ *                  strategies of accumulate.py:116-159); default shared-memory gathers
  * Not synchronised with concurrent predict calls: set them between calls.  No
  * reference counterpart (the reference has one CPU path). */
 int obt_set_path_option(const char* name, int value);

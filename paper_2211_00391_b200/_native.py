@@ -54,7 +54,7 @@ EXPORTED_SYMBOLS = (
 
 # Planner choices a caller may force (obt_set_path_option; -1 = automatic).
 PATH_OPTIONS = ("desc_source", "tpw", "wide", "fan", "pdl", "tail_split", "quant_lut", "lut_cells",
-                "leaf_storage", "multi_staged")
+                "leaf_storage", "multi_staged", "leaf_select")
 
 
 class NativeUnavailable(RuntimeError):

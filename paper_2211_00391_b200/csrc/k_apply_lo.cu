@@ -11,7 +11,12 @@ static ApplyKernel apply_leaf(int leaf, bool write_idx) {
   if (write_idx) k.fn = (const void*)apply_kernel<DI, CMP, 1, true, 1, DSRC>;
   else if (leaf == 0) k.fn = (const void*)apply_kernel<DI, CMP, 0, false, 1, DSRC>;
   else if (leaf == 1) k.fn = (const void*)apply_kernel<DI, CMP, 1, false, 1, DSRC>;
-  else k.fn = (const void*)apply_kernel<DI, CMP, 2, false, 1, DSRC>;
+  else if (leaf == 2) k.fn = (const void*)apply_kernel<DI, CMP, 2, false, 1, DSRC>;
+  // 3 / 4: shuffle "permute" leaf selection of binary16 (depth <= 6) / binary32 (depth <= 5)
+  else if constexpr (DI <= 6) {
+    if (leaf == 3) k.fn = (const void*)apply_kernel<DI, CMP, 3, false, 1, DSRC>;
+    else if constexpr (DI <= 5) k.fn = (const void*)apply_kernel<DI, CMP, 4, false, 1, DSRC>;
+  }
   return k;
 }
 

@@ -52,12 +52,13 @@ enum PathOption {
   OPT_LUT_CELLS,     // 256, 512 or 1024 cells per feature table (read at model creation)
   OPT_LEAF_STORAGE,  // 0: binary64 leaf tables even when binary32 is exact (model creation)
   OPT_MULTI_STAGED,  // 0 / 1: K4 / K5 for multi-output models (model creation)
+  OPT_LEAF_SELECT,   // 1: K2 selects leaves by warp shuffle from register-resident tables
   OPT_COUNT
 };
 const char* const kPathOptionNames[OPT_COUNT] = {"desc_source", "tpw", "wide", "fan", "pdl",
                                                  "tail_split", "quant_lut", "lut_cells", "leaf_storage",
-                                                 "multi_staged"};
-std::atomic<int> g_opt[OPT_COUNT] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
+                                                 "multi_staged", "leaf_select"};
+std::atomic<int> g_opt[OPT_COUNT] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
 int opt(PathOption o) { return g_opt[o].load(std::memory_order_relaxed); }
 
 
@@ -906,8 +907,14 @@ int launch_apply(obt_model* m, const uint8_t* q, int64_t n, int tile, int tpw, d
   const TilePlan* tp = nullptr;
   int rc = get_tile_plan(m, tile, tpw > 1 ? 1 : write_idx ? 2 : 0, &tp);
   if (rc != OBT_OK) return rc;
+  // leaf selection: shared-memory gathers, or (path option leaf_select = 1) warp shuffles
+  // from a register-resident table where the table is one word per lane
+  int leaf_code = m->leaf_storage;
+  if (opt(OPT_LEAF_SELECT) == 1 && !write_idx && tpw == 1 &&
+      ((m->leaf_storage == 2 && m->depth_inst <= 6) || (m->leaf_storage == 1 && m->depth_inst <= 5)))
+    leaf_code = m->leaf_storage == 2 ? 3 : 4;
   ApplyKernel k = tpw > 1 ? pick_split(m->depth_inst, m->compare_mode, m->leaf_storage, tpw)
-                          : pick_apply(m->depth_inst, m->compare_mode, m->leaf_storage, write_idx, dsrc);
+                          : pick_apply(m->depth_inst, m->compare_mode, leaf_code, write_idx, dsrc);
   if (!k.fn) return fail(OBT_E_UNSUPPORTED, "no apply kernel for depth %d", m->depth_inst);
   const int64_t n_tiles = (n + tile - 1) / tile;
   // parameter-bank launches stream tables-only ring chunks (their descriptors travel in

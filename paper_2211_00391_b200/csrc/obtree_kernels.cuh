@@ -844,6 +844,12 @@ template <> struct LeafT<1> { using T = float; using Acc = double; static conste
   static __device__ __forceinline__ double widen(float v) { return (double)v; } };
 template <> struct LeafT<2> { using T = __half; using Acc = float; static constexpr int kShift = 1;
   static __device__ __forceinline__ float widen(__half v) { return __half2float(v); } };
+// Register/shuffle "permute" leaf selection (K2 only; PERMUTE16 / PERMUTE64 of the
+// reference, accumulate.py:116-159, section 8.2-8.3): a tree's whole table, 128
+// bytes, sits one word per lane, and a lane takes its objects' leaves with SHFL.
+//   3: binary16 leaves, depth <= 6 (two leaves per word)   4: binary32 leaves, depth <= 5
+template <> struct LeafT<3> : LeafT<2> {};
+template <> struct LeafT<4> : LeafT<1> {};
 
 __device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) {
   return (a & b) | (a & c) | (b & c);
@@ -955,6 +961,10 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid
   // (index << kShift) directly and a gather is PRMT + LDS.
   constexpr bool kPrescaled = !WRITE_IDX && (DI + LT::kShift) <= 8;
   constexpr int kBitBase = kPrescaled ? LT::kShift : 0;
+  constexpr bool kPermute = LEAF >= 3;
+  constexpr bool kHalfFold = LEAF == 2 || LEAF == 3;
+  static_assert(!kPermute || (kPrescaled && W == 1 && (1 << DI) * (int)sizeof(typename LT::T) <= 128),
+                "permute selection: one 128-byte table per warp");
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   // 256-byte aligned working base (the host reserves 256 bytes of slack)
@@ -1055,6 +1065,8 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid
       constexpr int kPF = OBT_PF_TREES;
       uint32_t wbuf[kPF + 1][DI][W];  // bucket words of the trees in flight
       uint32_t kbuf[kPF + 1][DI];     // DSRC 1: k replicated per depth
+      uint32_t twbuf[kPF + 1];         // permute: this lane's word of the tree's table
+      (void)twbuf;
       constexpr int kLag = OBT_FOLD_LAG;
       typename LT::T gbuf[kLag + 1][4 * W];  // gathered leaves awaiting their fold
       (void)kbuf; (void)gbuf;
@@ -1089,6 +1101,8 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid
               lds_words<W, true>(my_q + ((CMP == 7 && kDW == 2) ? d0 : (d0 >> 8)), wbuf[sl][d]);
             }
           }
+          if constexpr (kPermute)  // one conflict-free word per lane: the table in registers
+            twbuf[sl] = lds_u32<true>(leaf_base + (uint32_t)(g * kTreeGroup + tt) * 256u + 4u * (ctid & 31));
         }
         if (it >= kPF && it - kPF < kTreeGroup) {  // stage B: index + leaf requests of tree ti
           const int ti = it - kPF, sl = ti % (kPF + 1);
@@ -1147,6 +1161,20 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid
                   if (o < p.n) row[o] = (uint16_t)idx;
                 }
               }
+            } else if constexpr (kPermute) {
+              // leaf of byte offset `off`: word off / 4 of the table, from lane off / 4;
+              // binary16: the half (off / 2) & 1 of that word
+              typename LT::T* gv = gbuf[ti % (kLag + 1)] + 4 * x;
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const uint32_t off = (lo >> (8 * k)) & 0xffu;
+                const uint32_t v = __shfl_sync(0xffffffffu, twbuf[sl], (int)(off >> 2));
+                if constexpr (LEAF == 3) {
+                  gv[k] = __ushort_as_half((unsigned short)__byte_perm(v, 0u, (off & 2u) ? 0x3232u : 0x1010u));
+                } else {
+                  gv[k] = __uint_as_float(v);
+                }
+              }
             } else if constexpr (kPrescaled) {
               const uint32_t tab = leaf_base + (uint32_t)t * 256u;
               typename LT::T* gv = gbuf[ti % (kLag + 1)] + 4 * x;
@@ -1173,7 +1201,7 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid
             const int tf = it - kPF - kLag;
 #pragma unroll
             for (int k = 0; k < 4 * W; k += 2) {
-              if constexpr (LEAF == 2 && OBT_FADD2) {
+              if constexpr (kHalfFold && OBT_FADD2) {
                 // binary32 fold of two objects in one packed FADD2 (two independent
                 // round-to-nearest adds: the same bits as two FADDs)
                 fadd2(acc[k], acc[k + 1], LT::widen(gbuf[tf % (kLag + 1)][k]), LT::widen(gbuf[tf % (kLag + 1)][k + 1]));

@@ -893,3 +893,24 @@ def test_wide_apply_is_the_default_at_config4_shape():
     ev = obt.Evaluator(model, device=0)
     got = ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
     assert np.array_equal(got, oracle.evaluate_scalar(oracle.flatten(model), x))
+
+
+# ---------------------------------------------------------------------------
+# Register/shuffle "permute" leaf selection (PERMUTE16 / PERMUTE64 of
+# the reference, accumulate.py:116-159): K2 holds each 128-byte table one word per lane
+# and selects leaves with SHFL instead of shared-memory gathers.
+
+@pytest.mark.parametrize("D", [1, 3, 5, 6])
+@pytest.mark.parametrize("B", [16, 200])
+@pytest.mark.parametrize("source", [0, 1])
+def test_permute_leaf_selection_bit_exact(paths, D, B, source):
+    paths(leaf_select=1, fan=0, wide=0, tpw=1, desc_source=source)
+    model = _model(23, B, 97, D, seed=D * 7 + B)
+    x = _features(model, 70_001, seed=D + B)
+    fm = oracle.flatten(model)
+    for strategy, prec in ((obt.LeafStrategy.NAIVE16, oracle.BINARY16), (obt.LeafStrategy.NAIVE, oracle.BINARY64)):
+        if prec == oracle.BINARY64 and D > 5:
+            continue  # 64 binary32 leaves are two words per lane: gathers only
+        ev = obt.Evaluator(model, obt.EvalConfig(strategy=strategy), device=0)
+        got = ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
+        assert np.array_equal(got, oracle.evaluate_scalar(fm, x, oracle.OBJECT_MAJOR, prec)), (strategy, D, B)
