@@ -18,6 +18,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/obtree_b200.h"
@@ -1743,6 +1744,53 @@ int obt_quantize_dev(const obt_model* m, const float* x, int64_t n, int32_t layo
   return launch_quantize(m, x, n, layout, buckets, false, 0, n, false, static_cast<cudaStream_t>(stream));
 }
 
+}  // extern "C"
+
+namespace {
+
+// Pinned staging for pageable feature arrays (the literal drop-in call passes a plain
+// numpy array): the driver stages a pageable H2D through its own small pinned buffer at
+// ~10 GB/s and blocks the caller.  Here host threads copy each chunk into one of two
+// pinned buffers (kept per device, allocated on first use) while the previous chunk's
+// DMA and the one before's kernels run.
+struct HostStaging {
+  std::mutex mu;
+  void* buf[2] = {nullptr, nullptr};
+  size_t bytes = 0;
+  cudaEvent_t h2d_done[2] = {nullptr, nullptr};
+};
+HostStaging* host_staging(int device) {
+  static std::mutex mu;
+  static std::map<int, std::unique_ptr<HostStaging>> all;
+  std::lock_guard<std::mutex> lock(mu);
+  auto& s = all[device];
+  if (!s) s.reset(new HostStaging());
+  return s.get();
+}
+
+// memcpy with up to 16 host threads (one per 8 MB piece at least); measured on the GPU
+// box's 16 cores from pageable into pinned memory: 14 GB/s on one thread, 51 on 16
+// (tools/memcpy_probe.cu)
+void parallel_copy(void* dst, const void* src, size_t bytes) {
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const size_t piece = (size_t)8 << 20;
+  const int nt = (int)std::min<size_t>(std::min(16u, hw), (bytes + piece - 1) / piece);
+  if (nt <= 1) { std::memcpy(dst, src, bytes); return; }
+  const size_t per = (bytes + nt - 1) / nt / 64 * 64 + 64;
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t) {
+    const size_t b = (size_t)t * per;
+    if (b >= bytes) break;
+    const size_t len = std::min(per, bytes - b);
+    th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + b, static_cast<const char*>(src) + b, len); });
+  }
+  for (auto& t : th) t.join();
+}
+
+}  // namespace
+
+extern "C" {
+
 int obt_predict_host(const obt_model* mc, const float* x_host, int64_t n, int32_t layout, double* out_host,
                      void* stream_v) {
   g_launches = 0;
@@ -1806,8 +1854,43 @@ int obt_predict_host(const obt_model* mc, const float* x_host, int64_t n, int32_
     return rc;
   }
   const int nbuf = n_chunks > 1 ? 2 : 1;
+  // pageable object-major features go through the pinned staging buffers; scores for a
+  // pageable output gather on the device and cross once at the end (a D2H into pageable
+  // memory blocks the host until the stream drains, which would serialise the pipeline)
+  cudaPointerAttributes pattr{};
+  const bool pageable = cudaPointerGetAttributes(&pattr, x_host) != cudaSuccess || pattr.type == cudaMemoryTypeUnregistered;
+  cudaGetLastError();  // an unregistered pointer is not an error here
+  const bool out_pageable = cudaPointerGetAttributes(&pattr, out_host) != cudaSuccess ||
+                            pattr.type == cudaMemoryTypeUnregistered;
+  cudaGetLastError();
+  HostStaging* stg = nullptr;
+  std::unique_lock<std::mutex> stg_lock;
+  if (pageable && layout == OBT_LAYOUT_OBJECT_MAJOR) {
+    stg = host_staging(m->device);
+    stg_lock = std::unique_lock<std::mutex>(stg->mu);
+    const size_t need = (size_t)rows * F * 4;
+    if (stg->bytes < need) {
+      for (int b = 0; b < 2; ++b) {
+        if (stg->buf[b]) cudaFreeHost(stg->buf[b]);
+        stg->buf[b] = nullptr;
+      }
+      stg->bytes = 0;
+      bool ok = true;
+      for (int b = 0; b < 2 && ok; ++b) ok = cudaHostAlloc(&stg->buf[b], need, cudaHostAllocPortable) == cudaSuccess;
+      for (int b = 0; b < 2 && ok; ++b)
+        if (!stg->h2d_done[b]) ok = cudaEventCreateWithFlags(&stg->h2d_done[b], cudaEventDisableTiming) == cudaSuccess;
+      if (ok) {
+        stg->bytes = need;
+      } else {
+        cudaGetLastError();
+        stg_lock.unlock();
+        stg = nullptr;  // no pinned memory to spare: the driver's own staging
+      }
+    }
+  }
   float* x_dev[2] = {nullptr, nullptr};
   double* out_dev[2] = {nullptr, nullptr};
+  double* out_all = nullptr;  // pageable output: every chunk's scores, one D2H at the end
   cudaStream_t copy = nullptr;
   cudaEvent_t copied[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
   rc = OBT_OK;
@@ -1816,9 +1899,12 @@ int obt_predict_host(const obt_model* mc, const float* x_host, int64_t n, int32_
     return rc == OBT_OK;
   };
   cuda_ok(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking), "copy stream");
+  if (out_pageable)
+    cuda_ok(pool_alloc(reinterpret_cast<void**>(&out_all), (size_t)n * C * 8, m->device, stream), "score buffer");
   for (int b = 0; b < nbuf && rc == OBT_OK; ++b) {
     cuda_ok(pool_alloc(reinterpret_cast<void**>(&x_dev[b]), (size_t)rows * F * 4, m->device, stream), "feature buffer");
-    cuda_ok(pool_alloc(reinterpret_cast<void**>(&out_dev[b]), (size_t)rows * C * 8, m->device, stream), "score buffer");
+    if (!out_pageable)
+      cuda_ok(pool_alloc(reinterpret_cast<void**>(&out_dev[b]), (size_t)rows * C * 8, m->device, stream), "score buffer");
     cuda_ok(cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming), "event");
     cuda_ok(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming), "event");
   }
@@ -1833,7 +1919,15 @@ int obt_predict_host(const obt_model* mc, const float* x_host, int64_t n, int32_
     const int b = (int)(i % nbuf);
     const int64_t o0 = bounds[i], ni = bounds[i + 1] - bounds[i];
     if (i >= nbuf) cuda_ok(cudaStreamWaitEvent(copy, done[b], 0), "stream wait");  // buffer b free again
-    if (layout == OBT_LAYOUT_OBJECT_MAJOR) {
+    if (stg) {
+      // staging buffer b is free once its previous DMA is done; fill it on the host
+      // while the DMA of chunk i - 1 and the kernels of chunk i - 2 run
+      if (i >= 2) cuda_ok(cudaEventSynchronize(stg->h2d_done[b]), "staging wait");
+      if (rc != OBT_OK) break;
+      parallel_copy(stg->buf[b], x_host + o0 * F, (size_t)ni * F * 4);
+      cuda_ok(cudaMemcpyAsync(x_dev[b], stg->buf[b], (size_t)ni * F * 4, cudaMemcpyHostToDevice, copy), "H2D");
+      cuda_ok(cudaEventRecord(stg->h2d_done[b], copy), "event record");
+    } else if (layout == OBT_LAYOUT_OBJECT_MAJOR) {
       cuda_ok(cudaMemcpyAsync(x_dev[b], x_host + o0 * F, (size_t)ni * F * 4, cudaMemcpyHostToDevice, copy), "H2D");
     } else {  // feature-major: ni columns of every feature row
       cuda_ok(cudaMemcpy2DAsync(x_dev[b], (size_t)ni * 4, x_host + o0, (size_t)n * 4, (size_t)ni * 4, F,
@@ -1842,11 +1936,15 @@ int obt_predict_host(const obt_model* mc, const float* x_host, int64_t n, int32_
     cuda_ok(cudaEventRecord(copied[b], copy), "event record");
     cuda_ok(cudaStreamWaitEvent(stream, copied[b], 0), "stream wait");
     if (rc != OBT_OK) break;
-    rc = predict_impl(m, x_dev[b], ni, layout, out_dev[b], nullptr, 0, 0, nullptr, 0, stream);
+    double* od = out_pageable ? out_all + o0 * C : out_dev[b];
+    rc = predict_impl(m, x_dev[b], ni, layout, od, nullptr, 0, 0, nullptr, 0, stream);
     launches += g_launches;
-    cuda_ok(cudaMemcpyAsync(out_host + o0 * C, out_dev[b], (size_t)ni * C * 8, cudaMemcpyDeviceToHost, stream), "D2H");
+    if (!out_pageable)
+      cuda_ok(cudaMemcpyAsync(out_host + o0 * C, od, (size_t)ni * C * 8, cudaMemcpyDeviceToHost, stream), "D2H");
     cuda_ok(cudaEventRecord(done[b], stream), "event record");
   }
+  if (out_pageable && rc == OBT_OK)
+    cuda_ok(cudaMemcpyAsync(out_host, out_all, (size_t)n * C * 8, cudaMemcpyDeviceToHost, stream), "D2H");
   g_launches = launches;
   // the stream-ordered frees below must also follow every copy issued on `copy` (an
   // error may have left a copy that `stream` never waited for)
@@ -1855,6 +1953,7 @@ int obt_predict_host(const obt_model* mc, const float* x_host, int64_t n, int32_
     if (x_dev[b]) cudaFreeAsync(x_dev[b], stream);
     if (out_dev[b]) cudaFreeAsync(out_dev[b], stream);
   }
+  if (out_all) cudaFreeAsync(out_all, stream);
   const cudaError_t e = cudaStreamSynchronize(stream);
   if (rc == OBT_OK && e != cudaSuccess) rc = fail(OBT_E_CUDA, "stream synchronize failed: %s", cudaGetErrorString(e));
   cudaStreamSynchronize(copy);

@@ -914,3 +914,21 @@ def test_permute_leaf_selection_bit_exact(paths, D, B, source):
         ev = obt.Evaluator(model, obt.EvalConfig(strategy=strategy), device=0)
         got = ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
         assert np.array_equal(got, oracle.evaluate_scalar(fm, x, oracle.OBJECT_MAJOR, prec)), (strategy, D, B)
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_host_predict_chunked_pageable_and_pinned(pinned):
+    """Evaluator.predict on host arrays larger than one 128 MB chunk: pageable numpy input
+    goes through the library's pinned staging buffers (host threads fill them while the
+    previous chunk's DMA runs), pinned input straight to DMA; both equal the oracle."""
+    model = _model(64, 32, 40, 6, seed=91)
+    x = _features(model, 700_001, seed=92, specials=False)
+    if pinned:
+        xt = torch.from_numpy(x).pin_memory()
+        x = xt.numpy()
+    want = oracle.evaluate_scalar(oracle.flatten(model), x)
+    ev = obt.Evaluator(model, device=0)
+    got = ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
+    assert np.array_equal(got, want)
+    again = ev.predict(obt.FeatureMatrix(x[:300_001], obt.Layout.OBJECT_MAJOR))  # staging reused
+    assert np.array_equal(again, want[:300_001])
