@@ -1778,12 +1778,18 @@ void parallel_copy(void* dst, const void* src, size_t bytes) {
   if (nt <= 1) { std::memcpy(dst, src, bytes); return; }
   const size_t per = (bytes + nt - 1) / nt / 64 * 64 + 64;
   std::vector<std::thread> th;
-  for (int t = 0; t < nt; ++t) {
-    const size_t b = (size_t)t * per;
-    if (b >= bytes) break;
-    const size_t len = std::min(per, bytes - b);
-    th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + b, static_cast<const char*>(src) + b, len); });
+  size_t next = per;  // piece 0 is this thread's; `next` = first byte not handed out
+  try {
+    for (int t = 1; t < nt && next < bytes; ++t) {
+      const size_t b = next, len = std::min(per, bytes - next);
+      th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + b, static_cast<const char*>(src) + b, len); });
+      next += len;
+    }
+  } catch (...) {
+    // no thread to spare (std::system_error): the rest is copied here
   }
+  std::memcpy(dst, src, std::min(per, bytes));
+  if (next < bytes) std::memcpy(static_cast<char*>(dst) + next, static_cast<const char*>(src) + next, bytes - next);
   for (auto& t : th) t.join();
 }
 
