@@ -279,8 +279,10 @@ def verify_timed(x, out, fm, precision: int, rows, exact: bool) -> dict:
     want = want.reshape(got.shape)
     rel = np.abs(got - want) / np.maximum(np.maximum(np.abs(got), np.abs(want)), 1e-300)
     rel = np.where(got == want, 0.0, rel)
+    ab = np.where(got == want, 0.0, np.abs(got - want))
     return {"rows": int(rows.size), "bit_exact": bool(np.array_equal(got, want)),
-            "max_rel_dev": float(np.nanmax(rel)) if rel.size else 0.0, "expect_bit_exact": exact}
+            "max_rel_dev": float(np.nanmax(rel)) if rel.size else 0.0,
+            "max_abs_dev": float(np.nanmax(ab)) if ab.size else 0.0, "expect_bit_exact": exact}
 
 
 def cpu_baseline_port(spec, fm, x, trees: int, seconds: float) -> dict:
@@ -666,10 +668,24 @@ def run_ours(args, world, rank, local):
     ver = verify_timed(x, out, fm_full, prec, rows, exact=not plan.reduce)
     red = reduce_over_ranks([ver["rows"]], world, "sum")
     mx = reduce_over_ranks([ver["max_rel_dev"]], world, "max")[0]
+    mabs = reduce_over_ranks([ver["max_abs_dev"]], world, "max")[0]
     mn = reduce_over_ranks([1.0 if ver["bit_exact"] else 0.0], world, "min")[0]
+    # tree / grid sharding reassociates the fold: binary64 partials within 1e-12 relative;
+    # binary32 partials (binary16 family) within the reference's FP16 acceptance bound
+    # |scale| * T * max|leaf| * 2^-10 (test_acceptance.py:156), absolute
+    if plan.reduce and spec.half_leaves:
+        from paper_2211_00391_b200.model import half_bank_values
+
+        halves = half_bank_values(full_model.leaves if multi else np.concatenate(
+            [np.asarray(t.leaf_values, np.float64) for t in full_model.trees]) if full_model.n_trees else np.zeros(1))[0]
+        bound = abs(full_model.scale) * spec.n_trees * float(np.max(np.abs(halves.astype(np.float64)))) * 2.0 ** -10
+        tol, passed = {"abs": bound}, bool(mabs <= bound)
+    elif plan.reduce:
+        tol, passed = {"rel": 1e-12}, bool(mx <= 1e-12)
+    else:
+        tol, passed = 0.0, bool(mn == 1.0)
     verify = {"rows": int(red[0]), "ranks": world, "bit_exact": bool(mn == 1.0), "max_rel_dev": mx,
-              "tolerance": 0.0 if not plan.reduce else 1e-12,
-              "passed": bool(mn == 1.0) if not plan.reduce else bool(mx <= 1e-12),
+              "max_abs_dev": mabs, "tolerance": tol, "passed": passed,
               "rows_spec": "per rank: first and last 1024 rows + every k-th row of its timed batch",
               "oracle": "oracle/obtree_oracle.c evaluate_scalar (full model)"}
 

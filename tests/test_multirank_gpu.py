@@ -91,7 +91,8 @@ def test_two_ranks_gpu_evaluator(case):
     mp.spawn(_worker, args=(2, _free_port(), case), nprocs=2, join=True)
 
 
-@pytest.mark.parametrize("config,extra", [(1, []), (5, ["--objects", "20000", "--trees", "64"])])
+@pytest.mark.parametrize("config,extra", [(1, []), (5, ["--objects", "20000", "--trees", "64"]),
+                                          (5, ["--objects", "20000", "--trees", "64", "--leaves", "fp16"])])
 def test_bench_self_spawns_two_ranks(config, extra):
     """`bench.py --gpus 2` launches two ranks itself (gloo on one GPU here); the line
     reports n_gpus 2 and a verified timed batch."""
