@@ -5,6 +5,7 @@ timeout 900 python bench.py --config 2 > gpurun_out/r2final/bench_cfg2.json 2> g
 timeout 900 python bench.py --config 3 > gpurun_out/r2final/bench_cfg3.json 2> gpurun_out/r2final/bench_cfg3.err; echo "cfg3 rc=$?"
 timeout 600 python bench.py --config 1 > gpurun_out/r2final/bench_cfg1.json 2> gpurun_out/r2final/bench_cfg1.err; echo "cfg1 rc=$?"
 timeout 1500 python bench.py --config 5 --steps 5 --warmup 3 > gpurun_out/r2final/bench_cfg5.json 2> gpurun_out/r2final/bench_cfg5.err; echo "cfg5 rc=$?"
+timeout 1500 python bench.py --config 5 --steps 5 --warmup 3 --leaves fp16 > gpurun_out/r2final/bench_cfg5h.json 2> gpurun_out/r2final/bench_cfg5h.err; echo "cfg5h rc=$?"
 timeout 900 python bench.py --impl reference > gpurun_out/r2final/bench_reference.json 2> gpurun_out/r2final/bench_reference.err; echo "ref rc=$?"
 for f in gpurun_out/r2final/bench_*.json; do python -c "
 import json;d=json.loads(open('$f').read().strip().splitlines()[-1])
