@@ -847,7 +847,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5, 6],
+                    help="BASELINE configs 1-5; 6 = the reference bench's epsilon8k64 shape (informational)")
     ap.add_argument("--objects", type=int, default=0, help="override the configuration's object count")
     ap.add_argument("--trees", type=int, default=0, help="override the tree count (experiments)")
     ap.add_argument("--leaves", choices=["fp32", "fp16"], default=None,

@@ -149,6 +149,10 @@ struct obt_model {
   LutTable used_lut;         // cell tables of `used` (K1L), kmax 0 if not applicable
   void* d_multi_leaves = nullptr;   // multi-output records [T][2^DI][CP] (K4) or [T][2^DI] slots (K4s)
   int multi_staged = 0;             // 1: K5 (tree tables + bucket rows staged in shared memory)
+  // the K4 / K5 record path: multi-output models, and single-output models whose F bytes
+  // per object leave no room for K2's 128-object bucket tile (K5 stages only the rows a
+  // tree reads: the paper's epsilon model has F = 2,000)
+  int multi_style = 0;
   int staged_stages = 0;
   uint32_t staged_table_bytes = 0, staged_stage_bytes = 0;
   int multi_slot = 0;
@@ -677,7 +681,7 @@ constexpr int kMaxParamLaunches = 4;
 // Largest tile (multiple of 256 objects) whose bucket tile fits next to the stage ring;
 // then shrink for small batches so the grid still covers the SMs.
 int plan_tile(const obt_model* m, int64_t n) {
-  if (m->n_outputs > 1) return m->multi_staged ? obt::kStagedTile : kMultiTile;
+  if (m->multi_style) return m->multi_staged ? obt::kStagedTile : kMultiTile;
   const int64_t fixed = 512 + (int64_t)kStages * m->chunk_bytes;
   int64_t tmax = (m->smem_optin - fixed) / m->n_features;
   tmax = std::min<int64_t>(tmax / kTileQuantum * kTileQuantum, 4 * (obt::kApplyMaxThreads - obt::kApplyProducerThreads) / kTileQuantum * kTileQuantum);
@@ -728,7 +732,7 @@ int choose_tpw(const obt_model* m, int tile, bool write_idx) {
 // Lanes per bucket word for one predict, decided once (the quantize launch lays the
 // buckets out for it).
 int apply_lanes(const obt_model* m, int tile, bool write_idx) {
-  if (m->n_outputs > 1) return 1;
+  if (m->multi_style) return 1;
   if (opt(OPT_DESC_SOURCE) == 1) return 1;  // the parameter-bank kernels have one lane per word
   return choose_tpw(m, tile, write_idx);
 }
@@ -1115,7 +1119,7 @@ int get_wide_plan(obt_model* m, const WidePlan** out) {
 // K2w where the K2 tile would hold few objects: the bucket tile (F bytes per object)
 // leaves K2 too few warps per SM (config 4, F = 500: 256 objects, 2 warps).
 bool wide_eligible(const obt_model* m) {
-  if (m->n_outputs > 1 || m->depth_inst > 8 || m->n_trees == 0) return false;
+  if (m->multi_style || m->depth_inst > 8 || m->n_trees == 0) return false;
   int ts = 0, ns = 0;
   if (!wide_rings(m, wide_dsrc(), &ts, &ns)) return false;
   if (!obt::pick_wide(m->depth_inst, m->compare_mode, m->leaf_storage, wide_dsrc())) return false;
@@ -1272,7 +1276,7 @@ int fan_stages(const obt_model* m) {
 }
 size_t fan_smem(const obt_model* m) { return fan_fixed_smem(m) + (size_t)fan_stages(m) * m->chunk_bytes; }
 bool fan_eligible(const obt_model* m, int64_t n) {
-  if (m->n_outputs > 1 || m->depth_inst > 8 || m->n_trees == 0 || n <= 0) return false;
+  if (m->multi_style || m->depth_inst > 8 || m->n_trees == 0 || n <= 0) return false;
   if (fan_stages(m) < 2 || fan_smem(m) > (size_t)m->smem_optin) return false;
   if (!obt::pick_fan(m->depth_inst, m->compare_mode, m->leaf_storage)) return false;
   if (opt(OPT_FAN) == 0) return false;
@@ -1296,7 +1300,7 @@ Regions plan_regions(const obt_model* m, int64_t n, bool split_ok) {
   }
   r.tile[0] = plan_tile(m, n);
   const int split = opt(OPT_TAIL_SPLIT);  // 0 never, 1 whenever a tail exists
-  if (!split_ok || r.tile[0] < 0 || m->n_outputs > 1 || split == 0) return r;
+  if (!split_ok || r.tile[0] < 0 || m->multi_style || split == 0) return r;
   // Not behind a parameter-bank main region: the tail then runs with shared-memory
   // descriptors at ~60% of the main region's rate, and one more launch; measured at
   // cfg2 (3 parameter-bank launches): apply 1.045 ms without the split, 1.081 with it.
@@ -1382,9 +1386,9 @@ int obt_model_create(const obt_model_desc* d, int device, obt_model** out) {
   m->precision = d->precision;
   m->scale = d->scale;
   m->bias = d->bias;
-  m->depth_inst = d->n_trees > 0 ? (d->n_outputs > 1 ? obt::multi_depth(d->max_depth)
-                                                      : instantiated_depth(d->max_depth))
-                                  : (d->n_outputs > 1 ? 4 : 1);
+  m->multi_style = d->n_outputs > 1;  // (single-output models join below when K2 cannot hold them)
+  m->depth_inst = d->n_trees > 0 ? (m->multi_style ? obt::multi_depth(d->max_depth) : instantiated_depth(d->max_depth))
+                                  : (m->multi_style ? 4 : 1);
   CUDA_TRY(cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount, device));
   CUDA_TRY(cudaDeviceGetAttribute(&m->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
 
@@ -1394,7 +1398,7 @@ int obt_model_create(const obt_model_desc* d, int device, obt_model** out) {
   // so the predict path quantizes against R_f and compares with the split's rank j.
   // Fewer borders mean fewer search levels, and <= 127 used borders per feature keep
   // the 7-bit SWAR compare even when a feature has up to 254 borders.
-  const int D = m->max_depth, DI = m->depth_inst;
+  const int D = m->max_depth;
   std::vector<std::vector<int>> used(d->n_features);
   for (int t = 0; t < m->n_trees; ++t)
     for (int s = 0; s < D; ++s) {
@@ -1425,6 +1429,37 @@ int obt_model_create(const obt_model_desc* d, int device, obt_model** out) {
   for (int f = 0; f < d->n_features; ++f) umax = std::max(umax, (int)used_counts[f]);
   m->compare_mode = umax <= 127 ? 7 : 8;
 
+  // leaf bank: binary16 bits, or binary64 stored as fp32 when that is exact
+  const size_t per_tree_in = (size_t)1 << D;
+  const int C = d->n_outputs;
+  if (d->precision == OBT_PRECISION_BINARY16) {
+    m->leaf_storage = 2;
+  } else {
+    bool exact32 = true;
+    for (size_t i = 0; i < (size_t)m->n_trees * C * per_tree_in && exact32; ++i) {
+      const double v = d->leaves[i];
+      const float f = (float)v;
+      exact32 = std::isfinite(f) && (double)f == v && !(v == 0.0 && std::signbit(v) != std::signbit(f));
+    }
+    m->leaf_storage = (exact32 && opt(OPT_LEAF_STORAGE) != 0) ? 1 : 0;
+  }
+
+  // K2 holds a 128-object bucket tile (F bytes per object) next to a ring of at least one
+  // tree group per stage; a single-output model that leaves no room for that runs on the
+  // record path (K5 stages only the bucket rows each tree reads)
+  if (!m->multi_style && m->n_trees > 0) {
+    const int di = m->depth_inst;
+    const size_t per_tree_rec = std::max<size_t>((size_t)obt::desc_words_per_tree(di, m->compare_mode) * 4,
+                                                 (size_t)di * obt::kSplitDescBytes) +
+                                (size_t)obt::leaf_table_stride(di, (int)leaf_size(m->leaf_storage));
+    const size_t min_chunk = ((per_tree_rec * obt::tree_group(di) + 255) & ~(size_t)255) + 256;
+    if (512 + (size_t)kStages * min_chunk + (size_t)m->n_features * kTileQuantum > (size_t)m->smem_optin) {
+      m->multi_style = 1;
+      m->depth_inst = obt::multi_depth(D);
+    }
+  }
+  const int DI = m->depth_inst;
+
   // splits (ordinals as ranks among the used borders), padded to the instantiated
   // depth with sentinels
   m->split_feature.assign((size_t)m->n_trees * DI, 0);
@@ -1439,22 +1474,12 @@ int obt_model_create(const obt_model_desc* d, int device, obt_model** out) {
 
   plan_level_order(m.get(), d);
 
-  // leaf bank: binary16 bits, or binary64 stored as fp32 when that is exact
-  const size_t per_tree_in = (size_t)1 << D, per_tree = (size_t)1 << DI;
-  const int C = d->n_outputs;
-  if (d->precision == OBT_PRECISION_BINARY16) {
-    m->leaf_storage = 2;
-  } else {
-    bool exact32 = true;
-    for (size_t i = 0; i < (size_t)m->n_trees * C * per_tree_in && exact32; ++i) {
-      const double v = d->leaves[i];
-      const float f = (float)v;
-      exact32 = std::isfinite(f) && (double)f == v && !(v == 0.0 && std::signbit(v) != std::signbit(f));
-    }
-    m->leaf_storage = (exact32 && opt(OPT_LEAF_STORAGE) != 0) ? 1 : 0;
-  }
+  const size_t per_tree = (size_t)1 << DI;
   const size_t ls = leaf_size(m->leaf_storage);
-  if (C > 1) {
+  if (m->multi_style) {
+    if (m->depth_inst < 0 || m->depth_inst > 10 + 2 * (C > 1))
+      return fail(OBT_E_UNSUPPORTED, "%d features per object need the staged kernel, which takes depth <= 10",
+                  m->n_features);
     // multi-output records, one leaf's C values contiguous in 16-byte rows (K4, K5)
     // K5 (staged tables and rows) for binary32 or binary16 records, C <= 10, depth <= 10,
     // when at least two stages (one tree's table + its bucket rows each) fit shared memory;
@@ -1465,7 +1490,7 @@ int obt_model_create(const obt_model_desc* d, int device, obt_model** out) {
       const uint32_t stage = (table + (uint32_t)DI * obt::kStagedTile + 127u) & ~127u;
       const int stages = std::min(8, (int)(((size_t)m->smem_optin - 512) / stage));
       int sdi = 0;
-      const bool ok = m->leaf_storage != 0 && C <= 10 && stages >= 2 &&
+      const bool ok = (m->leaf_storage != 0 || C == 1) && C <= 10 && stages >= 2 &&
                       obt::pick_multi_staged(DI, m->compare_mode, C, m->leaf_storage, &sdi) != nullptr && sdi == DI;
       if (ok && (opt(OPT_MULTI_STAGED) != 0 || m->leaf_storage == 2)) {
         m->multi_staged = 1;
@@ -1560,7 +1585,7 @@ int obt_model_quantize_kernel(const obt_model* m, int32_t* kind, int32_t* param)
 
 int obt_model_multi_kernel(const obt_model* m, int32_t* kind) {
   if (!m || !kind) return fail(OBT_E_INVALID, "null argument");
-  *kind = m->n_outputs <= 1 ? -1 : m->multi_staged ? 2 : 0;
+  *kind = !m->multi_style ? -1 : m->multi_staged ? 2 : 0;
   return OBT_OK;
 }
 
@@ -1643,8 +1668,9 @@ static int predict_impl(obt_model* m, const float* x, int64_t n, int32_t layout,
   if (rc == OBT_OK && ev_mid) CUDA_TRY(cudaEventRecord(ev_mid, stream));
   for (int i = 0; i < reg.n_reg && rc == OBT_OK; ++i) {
     const int64_t b = reg.begin[i], c = reg.count[i];
-    if (m->n_outputs > 1) {
-      rc = idx_out ? fail(OBT_E_UNSUPPORTED, "leaf-index dumps are implemented for single-output models")
+    if (m->multi_style) {
+      rc = idx_out ? fail(OBT_E_UNSUPPORTED, "leaf-index dumps are implemented for the K2 path (single output, "
+                                             "F x 128 bytes of buckets in shared memory)")
                    : launch_multi(m, qr[i], c, out + b * m->n_outputs, stream);
     } else if (reg.fan) {
       rc = launch_fan(m, qr[i], c, out + b, stream);

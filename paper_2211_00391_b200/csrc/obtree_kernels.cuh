@@ -1733,8 +1733,10 @@ __global__ void __launch_bounds__(kMultiThreads, multi_min_blocks(LEAF, C)) appl
 __host__ __device__ constexpr int staged_half_units(int c) {
   return ((2 * c + 7) / 8) % 2 ? (2 * c + 7) / 8 : (2 * c + 7) / 8 + 1;
 }
+// One output (single-output models whose F bytes per object do not fit K2's bucket
+// tile): a record is the leaf itself, binary64 / binary32 / binary16.
 __host__ __device__ constexpr int staged_record_values(int c, int leaf) {
-  return leaf == 2 ? 4 * staged_half_units(c) : (c + 3) / 4 * 4;
+  return c == 1 ? 1 : leaf == 2 ? 4 * staged_half_units(c) : (c + 3) / 4 * 4;
 }
 constexpr int kStagedThreadsConsumers = 512;
 constexpr int kStagedTile = 4 * kStagedThreadsConsumers;  // 2048 objects
@@ -1757,9 +1759,9 @@ struct StagedParams {
 
 template <int DI, int CMP, int C, int LEAF>
 __global__ void __launch_bounds__(kStagedThreads, 1) apply_multi_staged_kernel(const __grid_constant__ StagedParams p) {
-  static_assert(LEAF == 1 || LEAF == 2, "K5: binary32 or binary16 records");
+  static_assert(LEAF == 1 || LEAF == 2 || (LEAF == 0 && C == 1), "K5: binary32 or binary16 records (binary64: one output)");
   constexpr int CP = staged_record_values(C, LEAF);
-  constexpr int kRecBytes = CP * (LEAF == 2 ? 2 : 4);
+  constexpr int kRecBytes = CP * (LEAF == 0 ? 8 : LEAF == 2 ? 2 : 4);
   constexpr int kRows = LEAF == 2 ? 0 : kRecBytes / 16;
   using acc_t = typename LeafT<LEAF>::Acc;  // binary64 / binary32 fold
   extern __shared__ __align__(128) unsigned char st_raw[];
@@ -1788,7 +1790,7 @@ __global__ void __launch_bounds__(kStagedThreads, 1) apply_multi_staged_kernel(c
     // Measured at config 5: binary16 records 196 ms with per-lane row copies vs 251 ms
     // with one thread issuing every copy; binary32 records the other way round (289 vs
     // 266 ms), so the binary32 family keeps the single issuing thread.
-    constexpr bool kSerial = LEAF == 1;
+    constexpr bool kSerial = LEAF == 1 && C > 1;
     const int lane = tid;
     if (kSerial && lane > 0) return;
     const uint2* desc = reinterpret_cast<const uint2*>(p.desc);
@@ -1836,7 +1838,7 @@ __global__ void __launch_bounds__(kStagedThreads, 1) apply_multi_staged_kernel(c
   const uint32_t stages_s = smem_u32(stages);
   // the binary16 family (40 binary32 accumulators) has the registers to load the next
   // tree's descriptors while this tree folds; the binary64 family (80) loads them per tree
-  constexpr bool kPrefetch = LEAF == 2;
+  constexpr bool kPrefetch = LEAF == 2 || C == 1;
   const uint2* desc = reinterpret_cast<const uint2*>(p.desc);
   uint2 dnext[kPrefetch ? DI : 1];
   if constexpr (kPrefetch) {
@@ -1876,7 +1878,9 @@ __global__ void __launch_bounds__(kStagedThreads, 1) apply_multi_staged_kernel(c
     for (int k = 0; k < 4; ++k) {
       const uint32_t idx = ((lo >> (8 * k)) & 0xffu) | (DI > 8 ? ((hi >> (8 * k)) & 0xffu) << 8 : 0u);
       const uint32_t rec = tab + idx * (uint32_t)kRecBytes;
-      if constexpr (LEAF == 1) {
+      if constexpr (C == 1) {
+        acc[k][0] += LeafT<LEAF>::widen(lds_leaf<LEAF>(rec));
+      } else if constexpr (LEAF == 1) {
         float v[CP];
 #pragma unroll
         for (int r = 0; r < kRows; ++r) {

@@ -63,6 +63,10 @@ CONFIGS = {
     3: WorkloadSpec("cfg3-1m-f200-b64-t2000-d6-fp16", 1_000_000, 200, 64, 2000, 6, 0.05, half_leaves=True, cfg=3),
     4: WorkloadSpec("cfg4-8m-f500-b128-t8000-d8", 8_000_000, 500, 128, 8000, 8, 0.02, cfg=4),
     5: WorkloadSpec("cfg5-16m-f1000-b254-t4000-d10-c10", 16_000_000, 1000, 254, 4000, 10, 0.01, n_outputs=10, cfg=5),
+    # informational (not a BASELINE config): the shape of the reference bench's
+    # "epsilon8k64" preset -- the paper's published single-core model, 2,000 features,
+    # 64 borders, 8,000 depth-6 trees (reference bench.py:40-44) -- on 1M N(0,1) objects
+    6: WorkloadSpec("eps8k64-1m-f2000-b64-t8000-d6", 1_000_000, 2000, 64, 8000, 6, 0.05, cfg=6),
 }
 
 

@@ -932,3 +932,33 @@ def test_host_predict_chunked_pageable_and_pinned(pinned):
     assert np.array_equal(got, want)
     again = ev.predict(obt.FeatureMatrix(x[:300_001], obt.Layout.OBJECT_MAJOR))  # staging reused
     assert np.array_equal(again, want[:300_001])
+
+
+# ---------------------------------------------------------------------------
+# Single-output models whose F bytes per object do not fit K2's 128-object bucket tile
+# (the reference has no feature limit; its own bench preset epsilon8k64 has F = 2,000):
+# the record path, K5 with one output, staging only the bucket rows each tree reads.
+
+@pytest.mark.parametrize("F,D,B", [(2000, 6, 64), (2500, 8, 200), (6000, 3, 16)])
+def test_large_feature_count_single_output(F, D, B):
+    model = _model(F, B, 45, D, seed=F + D)
+    x = _features(model, 3001, seed=D)
+    fm = oracle.flatten(model)
+    for strategy, prec in ((obt.LeafStrategy.NAIVE, oracle.BINARY64), (obt.LeafStrategy.NAIVE16, oracle.BINARY16)):
+        ev = obt.Evaluator(model, obt.EvalConfig(strategy=strategy), device=0)
+        want = oracle.evaluate_scalar(fm, x, oracle.OBJECT_MAJOR, prec)
+        assert np.array_equal(ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR)), want), (F, D, strategy)
+        xt = torch.from_numpy(np.ascontiguousarray(x.T)).cuda()
+        assert np.array_equal(ev.predict_device(xt, layout=obt.Layout.FEATURE_MAJOR).cpu().numpy(), want)
+
+
+def test_large_feature_count_binary64_leaves():
+    """Leaves that are not binary32-exact keep binary64 records on the record path."""
+    base = _model(3000, 32, 30, 6, seed=11)
+    rng = np.random.default_rng(12)
+    trees = tuple(obt.ObliviousTree(t.depth, t.splits, rng.uniform(-1, 1, t.leaf_values.size)) for t in base.trees)
+    model = obt.ObliviousModel(base.float_features, trees, base.scale, base.bias)
+    x = _features(model, 2000, seed=13)
+    ev = obt.Evaluator(model, device=0)
+    assert ev.leaf_storage == "fp64"
+    assert np.array_equal(ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR)), oracle.evaluate_scalar(oracle.flatten(model), x))
