@@ -1447,7 +1447,7 @@ int obt_model_create(const obt_model_desc* d, int device, obt_model** out) {
   // K2 holds a 128-object bucket tile (F bytes per object) next to a ring of at least one
   // tree group per stage; a single-output model that leaves no room for that runs on the
   // record path (K5 stages only the bucket rows each tree reads)
-  if (!m->multi_style && m->n_trees > 0) {
+  if (!m->multi_style) {
     const int di = m->depth_inst;
     const size_t per_tree_rec = std::max<size_t>((size_t)obt::desc_words_per_tree(di, m->compare_mode) * 4,
                                                  (size_t)di * obt::kSplitDescBytes) +
@@ -1455,7 +1455,7 @@ int obt_model_create(const obt_model_desc* d, int device, obt_model** out) {
     const size_t min_chunk = ((per_tree_rec * obt::tree_group(di) + 255) & ~(size_t)255) + 256;
     if (512 + (size_t)kStages * min_chunk + (size_t)m->n_features * kTileQuantum > (size_t)m->smem_optin) {
       m->multi_style = 1;
-      m->depth_inst = obt::multi_depth(D);
+      m->depth_inst = obt::multi_depth(std::max(D, 1));
     }
   }
   const int DI = m->depth_inst;

@@ -962,3 +962,54 @@ def test_large_feature_count_binary64_leaves():
     ev = obt.Evaluator(model, device=0)
     assert ev.leaf_storage == "fp64"
     assert np.array_equal(ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR)), oracle.evaluate_scalar(oracle.flatten(model), x))
+
+
+def test_random_model_shapes_fuzz():
+    """60 seeded random shapes across every planner branch (F 1..3,000, depth 1..8, 1..254
+    borders, 0..150 trees, batches 0..9,000, both precision families, both layouts,
+    affine finalize): predictions equal the oracle bit for bit."""
+    rng = np.random.default_rng(20261021)
+    for case in range(60):
+        F = int(rng.choice([1, 3, 4, 17, 50, 200, 501, 1203, 1800, 3000]))
+        D = int(rng.integers(1, 9))
+        B = int(rng.choice([1, 2, 7, 16, 64, 127, 128, 200, 254]))
+        T = int(rng.choice([0, 1, 5, 33, 150]))
+        n = int(rng.choice([0, 1, 129, 1000, 9000]))
+        model = _model(F, B, T, D, seed=case) if T else obt.ObliviousModel(_model(F, B, 1, D, seed=case).float_features,
+                                                                              (), 1.5, -0.25)
+        x = _features(model, n, seed=case + 1000)
+        fm = oracle.flatten(model)
+        strategy, prec = ((obt.LeafStrategy.NAIVE, oracle.BINARY64), (obt.LeafStrategy.NAIVE16, oracle.BINARY16))[case % 2]
+        ev = obt.Evaluator(model, obt.EvalConfig(strategy=strategy), device=0)
+        want = oracle.evaluate_scalar(fm, x, oracle.OBJECT_MAJOR, prec)
+        layout = obt.Layout.OBJECT_MAJOR if case % 3 else obt.Layout.FEATURE_MAJOR
+        xin = x if layout is obt.Layout.OBJECT_MAJOR else np.ascontiguousarray(x.T)
+        got = ev.predict(obt.FeatureMatrix(xin, layout))
+        assert got.shape == (n,)
+        assert np.array_equal(got, want), (case, F, D, B, T, n, strategy, layout)
+
+
+def test_random_shapes_and_forced_paths_fuzz(paths):
+    """Seeded random shapes with a random forced planner choice each (descriptor source,
+    lanes per word, K2w / K2f on or off, tail split, quantize search, permute selection):
+    every combination the planner accepts equals the oracle."""
+    rng = np.random.default_rng(77)
+    options = [("desc_source", (0, 1)), ("tpw", (1, 2, 4)), ("wide", (0, 1)), ("fan", (0, 1)),
+               ("tail_split", (0, 1)), ("quant_lut", (0, 1)), ("leaf_select", (1,)), ("pdl", (0,))]
+    for case in range(40):
+        F = int(rng.choice([4, 12, 50, 200, 500, 800]))
+        D = int(rng.choice([2, 4, 6, 8]))
+        B = int(rng.choice([7, 64, 128, 200]))
+        T = int(rng.choice([20, 97, 700]))
+        n = int(rng.choice([1, 300, 5000, 70_000]))
+        name, values = options[int(rng.integers(len(options)))]
+        value = int(rng.choice(values))
+        paths(**{name: value})
+        model = _model(F, B, T, D, seed=case + 500)
+        x = _features(model, n, seed=case + 600)
+        strategy, prec = ((obt.LeafStrategy.NAIVE, oracle.BINARY64), (obt.LeafStrategy.NAIVE16, oracle.BINARY16))[case % 2]
+        ev = obt.Evaluator(model, obt.EvalConfig(strategy=strategy), device=0)
+        want = oracle.evaluate_scalar(oracle.flatten(model), x, oracle.OBJECT_MAJOR, prec)
+        got = ev.predict_device(torch.from_numpy(x).cuda()).cpu().numpy()
+        assert np.array_equal(got, want), (case, F, D, B, T, n, name, value, strategy)
+        paths(**{name: -1})
