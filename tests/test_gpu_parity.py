@@ -1013,3 +1013,31 @@ def test_random_shapes_and_forced_paths_fuzz(paths):
         got = ev.predict_device(torch.from_numpy(x).cuda()).cpu().numpy()
         assert np.array_equal(got, want), (case, F, D, B, T, n, name, value, strategy)
         paths(**{name: -1})
+
+
+def test_random_multi_output_fuzz(paths):
+    """Seeded random multi-output shapes (C 2..16, depth 1..12, F 1..3,000, both families
+    where they apply, K4 / K5), against the multi-output restatement."""
+    from paper_2211_00391_b200 import multiclass
+
+    rng = np.random.default_rng(4242)
+    for case in range(24):
+        C = int(rng.choice([2, 3, 7, 10, 16]))
+        D = int(rng.choice([1, 4, 7, 10, 12]))
+        F = int(rng.choice([1, 9, 300, 3000]))
+        B = int(rng.choice([3, 64, 254]))
+        n = int(rng.choice([1, 513, 4097]))
+        half = bool(case % 3 == 0) and C <= 10 and D <= 10
+        paths(multi_staged=int(rng.integers(0, 2)) if not half else -1)
+        spec = synthetic.WorkloadSpec("m", 1, F, B, 37, D, 0.01, n_outputs=C, cfg=5)
+        arrays = synthetic.model_arrays(spec, seed=case + 900, affine=True)
+        model = multiclass.from_arrays(arrays)
+        x = _features(obt.ObliviousModel(tuple(obt.FloatFeatureBorders(f, b) for f, b in enumerate(arrays["borders"])),
+                                          (), 1.0, 0.0), n, seed=case + 901)
+        fm = oracle.FlatModel(np.stack(arrays["borders"]), np.full(F, B, np.int32), np.full(37, D, np.int32),
+                              arrays["split_feature"], arrays["split_ordinal"], arrays["leaves"], model.scale, model.bias)
+        cfg = obt.EvalConfig(strategy=obt.LeafStrategy.NAIVE16 if half else obt.LeafStrategy.NAIVE)
+        want = oracle.evaluate_scalar(fm, x, oracle.OBJECT_MAJOR, oracle.BINARY16 if half else oracle.BINARY64)
+        ev = multiclass.MultiOutputEvaluator(model, config=cfg)
+        got = ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
+        assert np.array_equal(got, want.reshape(got.shape)), (case, C, D, F, B, n, half, ev.apply_kernel())
