@@ -236,9 +236,6 @@ __device__ __forceinline__ uint32_t eytz_level(uint32_t o, float x, const float*
   return add_if_greater(o * two + four, x, b, four);
 }
 
-#ifndef OBT_BUCKETS_EVICT_LAST
-#define OBT_BUCKETS_EVICT_LAST 0  // bucket-tile stores with an L2 evict-last policy (experiment)
-#endif
 // Store the packed buckets of one feature for a lane's 4 objects (base + lane + 32k):
 // tiled -> word `lane` of the 128-object block's row, plain -> 4 bytes of row f.
 template <bool TILED>
@@ -257,13 +254,7 @@ __device__ __forceinline__ void store_bucket_word(const QuantizeParams& p, uint3
     const bool sw = (second ? p.swizzle2 : p.swizzle) && (f & 1);
     const int64_t t = rb / tl, w = (rb - t * tl + 4 * lane) ^ (sw ? 64 : 0);
     uint32_t* dst = reinterpret_cast<uint32_t*>((second ? p.out2 : p.out) + (t * p.n_features + f) * tl + w);
-    if constexpr (OBT_BUCKETS_EVICT_LAST) {
-      uint64_t pol;
-      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-      asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(dst), "r"(word), "l"(pol) : "memory");
-    } else {
-      *dst = word;
-    }
+    *dst = word;
   } else {
 #pragma unroll
     for (int k = 0; k < 4; ++k)
@@ -504,25 +495,6 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-// The same with an L2 eviction-priority policy (createpolicy).  Marking feature rows
-// evict-first (to leave L2 to the bucket tiles the apply reads next) measured 0.347 vs
-// 0.198 ms at cfg2: each promoted 128-byte line serves four 8-feature steps, and
-// evict-first lines are gone before the later steps arrive.  Off.
-__device__ __forceinline__ uint64_t l2_policy_evict_first() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
-                                                 uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;"
-      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
-      : "memory");
-}
-#ifndef OBT_FEATURES_EVICT_FIRST
-#define OBT_FEATURES_EVICT_FIRST 0
-#endif
 
 template <int L>
 __global__ void __launch_bounds__(kQTThreads, 2) quantize_tma_kernel(const __grid_constant__ CUtensorMap rows,
@@ -711,7 +683,6 @@ __global__ void __launch_bounds__(kQTThreads, 2) quantize_lut_kernel(const __gri
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint64_t pol = OBT_FEATURES_EVICT_FIRST ? l2_policy_evict_first() : 0;
       for (int st = 0; st < n_steps; ++st) {
         const int s = st % kQTStages;
         if (st >= kQTStages) mbar_wait(&empty[s], (uint32_t)(st / kQTStages - 1) & 1u);
@@ -719,12 +690,8 @@ __global__ void __launch_bounds__(kQTThreads, 2) quantize_lut_kernel(const __gri
         unsigned char* dst = ring + (size_t)s * kQTStageBytes;
 #pragma unroll
         for (int b = 0; b < kQuantBlock / kQTBoxRows; ++b)
-          if (OBT_FEATURES_EVICT_FIRST)
-            tma_load_2d_hint(dst + b * kQTBoxRows * kQuantStep * 4, &rows, f0 + st * kQuantStep,
-                             (int)(row0 + b * kQTBoxRows), &full[s], pol);
-          else
-            tma_load_2d(dst + b * kQTBoxRows * kQuantStep * 4, &rows, f0 + st * kQuantStep,
-                        (int)(row0 + b * kQTBoxRows), &full[s]);
+          tma_load_2d(dst + b * kQTBoxRows * kQuantStep * 4, &rows, f0 + st * kQuantStep,
+                      (int)(row0 + b * kQTBoxRows), &full[s]);
       }
     }
     return;
@@ -791,15 +758,9 @@ __host__ __device__ constexpr int tree_group(int di) { return di <= 6 ? OBT_GROU
 #ifndef OBT_FOLD_LAG
 #define OBT_FOLD_LAG 1         // apply pipeline: leaves folded this many trees after their request
 #endif
-#ifndef OBT_SINGLE_CHAIN
-#define OBT_SINGLE_CHAIN 1     // index bits merged in one LOP3 chain (not even/odd chains)
-#endif
-#ifndef OBT_PACKED_DESC
-#define OBT_PACKED_DESC 0
-#endif
-// Shared-memory descriptor words per split: 7-bit compare {off, k replicated} (2 words,
-// or 1 packed word (off << 8) | k with OBT_PACKED_DESC), 8-bit {(off << 8) | k, s}.
-__host__ __device__ constexpr int desc_words(int cmp) { return (cmp == 7 && OBT_PACKED_DESC) ? 1 : 2; }
+// Shared-memory descriptor words per split: 7-bit compare {off, k replicated}, 8-bit
+// {(off << 8) | k, s}.
+__host__ __device__ constexpr int desc_words(int) { return 2; }
 __host__ __device__ constexpr int desc_words_per_tree(int di, int cmp) { return di * desc_words(cmp); }
 
 struct ApplyParams {
@@ -1098,7 +1059,7 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid
               kbuf[sl][d] = krep;
             } else {
               const uint32_t d0 = dw[(tt * DI + d) * kDW];
-              lds_words<W, true>(my_q + ((CMP == 7 && kDW == 2) ? d0 : (d0 >> 8)), wbuf[sl][d]);
+              lds_words<W, true>(my_q + (CMP == 7 ? d0 : (d0 >> 8)), wbuf[sl][d]);
             }
           }
           if constexpr (kPermute)  // one conflict-free word per lane: the table in registers
@@ -1107,9 +1068,9 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid
         if (it >= kPF && it - kPF < kTreeGroup) {  // stage B: index + leaf requests of tree ti
           const int ti = it - kPF, sl = ti % (kPF + 1);
           const int t = g * kTreeGroup + ti;
-          uint32_t lo_even[W], lo_odd[W], hi[W];
+          uint32_t lo_acc[W], hi[W];
 #pragma unroll
-          for (int x = 0; x < W; ++x) { lo_even[x] = 0; lo_odd[x] = 0; hi[x] = 0; }
+          for (int x = 0; x < W; ++x) { lo_acc[x] = 0; hi[x] = 0; }
 #pragma unroll
           for (int d = 0; d < DI; ++d) {
             uint32_t b7s[W];  // [q > ordinal] in bit 7 of each byte, garbage below
@@ -1117,12 +1078,8 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid
               b7s[0] = wbuf[sl][d][0] + kbuf[sl][d];
             } else {
               // shared-memory descriptors: 7-bit {off, k replicated}; 8-bit {(off << 8) | k, s}
-              const uint32_t d0 = dw[(ti * DI + d) * kDW], d1 = dw[(ti * DI + d) * kDW + (kDW - 1)];
-              if constexpr (CMP == 7 && kDW == 1) {
-                const uint32_t krep = __byte_perm(d0, 0u, 0x0000u);
-#pragma unroll
-                for (int x = 0; x < W; ++x) b7s[x] = wbuf[sl][d][x] + krep;
-              } else if constexpr (CMP == 7) {
+              const uint32_t d0 = dw[(ti * DI + d) * kDW], d1 = dw[(ti * DI + d) * kDW + 1];
+              if constexpr (CMP == 7) {
 #pragma unroll
                 for (int x = 0; x < W; ++x) b7s[x] = wbuf[sl][d][x] + d1;
               } else {
@@ -1141,7 +1098,7 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid
               if (pos < 8) {
                 const uint32_t term = (pos == 7 ? b7 : (b7 >> (7 - pos))) & (0x01010101u << pos);
                 // one OR chain: each depth is one LOP3 (mask | acc) after its shift
-                if ((d & 1) && !OBT_SINGLE_CHAIN) lo_odd[x] |= term; else lo_even[x] |= term;
+                lo_acc[x] |= term;
               } else {
                 hi[x] |= (pos == 15 ? b7 : (b7 >> (15 - pos))) & (0x01010101u << (pos - 8));
               }
@@ -1149,7 +1106,7 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid
           }
 #pragma unroll
           for (int x = 0; x < W; ++x) {
-            const uint32_t lo = lo_even[x] | lo_odd[x];
+            const uint32_t lo = lo_acc[x];
             if constexpr (WRITE_IDX) {
               const int tg = t_base + t;
               if (tg >= p.tree_begin && tg < p.tree_end) {
@@ -1337,11 +1294,9 @@ __global__ void __launch_bounds__(kFanThreads, 1) apply_fan_kernel(const __grid_
       uint32_t lo = 0, hi = 0;
 #pragma unroll
       for (int d = 0; d < DI; ++d) {
-        const uint32_t d0 = dw[(t * DI + d) * kDW], d1 = dw[(t * DI + d) * kDW + (kDW - 1)];
+        const uint32_t d0 = dw[(t * DI + d) * kDW], d1 = dw[(t * DI + d) * kDW + 1];
         uint32_t b7;
-        if constexpr (CMP == 7 && kDW == 1) {
-          b7 = lds_u32(my_q + (d0 >> 8)) + __byte_perm(d0, 0u, 0x0000u);
-        } else if constexpr (CMP == 7) {
+        if constexpr (CMP == 7) {
           b7 = lds_u32(my_q + d0) + d1;
         } else {
           const uint32_t w = lds_u32(my_q + (d0 >> 8));
@@ -1563,21 +1518,12 @@ constexpr int kMultiThreads = kMultiTileObjects / 4 * kMultiLanesPerWord;
 
 // Values per multi-output leaf record: fp32 records in 16-byte rows (48 bytes at C = 10;
 // 32-byte rows with 256-bit loads measured slower), fp64 records in 16-byte rows.
-#ifndef OBT_MULTI_ROW32
-#define OBT_MULTI_ROW32 0
-#endif
+// Measured and dropped for K4: bucket words requested one tree ahead (590 against 565 ms
+// at config 5 -- the held words cost more than the overlap), L2 prefetch of the bucket
+// rows 4-16 trees ahead (no gain).
 __host__ __device__ constexpr int multi_record_values(int leaf, int c) {
-  return leaf == 1 ? (OBT_MULTI_ROW32 ? (c + 7) / 8 * 8 : (c + 3) / 4 * 4) : (c + 1) / 2 * 2;
+  return leaf == 1 ? (c + 3) / 4 * 4 : (c + 1) / 2 * 2;
 }
-#ifndef OBT_MULTI_PF
-#define OBT_MULTI_PF 0  // measured no gain at cfg5 (L2 prefetch 4-16 trees ahead)
-#endif
-#ifndef OBT_MULTI_AHEAD
-// K4: bucket words requested one tree ahead.  Measured at config 5 (128 registers):
-// 590 ms against 565 ms without -- the kernel is bound by how many record round trips
-// the SM keeps in flight, and the held words cost more than the overlap gains
-#define OBT_MULTI_AHEAD 0
-#endif
 
 #ifndef OBT_MULTI_MINB
 // 4 resident CTAs per SM (a 128-register cap) up to C = 10: uncapped, ptxas took 196
@@ -1609,40 +1555,14 @@ __global__ void __launch_bounds__(kMultiThreads, multi_min_blocks(LEAF, C)) appl
 #pragma unroll
       for (int c = 0; c < C; ++c)
         acc[k][c] = (p.first || obj_of(k) >= p.n) ? 0.0 : p.out[obj_of(k) * C + c];
-    // OBT_MULTI_AHEAD: bucket words (and descriptors) of tree t + 1 requested before tree
-    // t's records are folded (27% of config 5's long-scoreboard stalls wait on bucket
-    // words, 66% on records; measured slower, see the define)
-    uint32_t wnext[DI];
-    uint2 dnext[DI];
-    auto load_words = [&](int t, uint32_t (&w)[DI], uint2 (&dv)[DI]) {
-      const uint2* ds = reinterpret_cast<const uint2*>(p.desc) + (size_t)t * DI;
-#pragma unroll
-      for (int d = 0; d < DI; ++d) {
-        dv[d] = __ldg(ds + d);  // warp-uniform address: one broadcast
-        w[d] = __ldg(reinterpret_cast<const uint32_t*>(qrow0 + (CMP == 7 ? dv[d].x : (dv[d].x >> 8))));
-      }
-    };
-    if (OBT_MULTI_AHEAD && p.tree_begin < p.tree_end) load_words(p.tree_begin, wnext, dnext);
     for (int t = p.tree_begin; t < p.tree_end; ++t) {
       uint32_t wcur[DI];
       uint2 dcur[DI];
-      if (OBT_MULTI_AHEAD) {
+      const uint2* ds = reinterpret_cast<const uint2*>(p.desc) + (size_t)t * DI;
 #pragma unroll
-        for (int d = 0; d < DI; ++d) { wcur[d] = wnext[d]; dcur[d] = dnext[d]; }
-        if (t + 1 < p.tree_end) load_words(t + 1, wnext, dnext);
-      } else {
-        load_words(t, wcur, dcur);
-      }
-      if (OBT_MULTI_PF > 0 && t + OBT_MULTI_PF < p.tree_end) {
-        // the bucket rows of a tree OBT_MULTI_PF ahead into L2: the tile's rows do not stay
-        // L2-resident between uses (F = 1000 bytes per object), so without this every
-        // tree's index waits on HBM
-        const uint2* dp = reinterpret_cast<const uint2*>(p.desc) + (size_t)(t + OBT_MULTI_PF) * DI;
-#pragma unroll
-        for (int d = 0; d < DI; ++d) {
-          const uint32_t off = CMP == 7 ? __ldg(&dp[d].x) : (__ldg(&dp[d].x) >> 8);
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(qrow0 + off));
-        }
+      for (int d = 0; d < DI; ++d) {
+        dcur[d] = __ldg(ds + d);  // warp-uniform address: one broadcast
+        wcur[d] = __ldg(reinterpret_cast<const uint32_t*>(qrow0 + (CMP == 7 ? dcur[d].x : (dcur[d].x >> 8))));
       }
       uint32_t lo = 0, hi = 0;
 #pragma unroll
@@ -1661,28 +1581,7 @@ __global__ void __launch_bounds__(kMultiThreads, multi_min_blocks(LEAF, C)) appl
       const leaf_t* tab = reinterpret_cast<const leaf_t*>(p.leaves) + ((size_t)t << DI) * CP;
       // all 4 objects' records are requested before any is consumed: the L2 round trips
       // overlap (each record is CP values in 16-byte rows)
-      if constexpr (LEAF == 1 && OBT_MULTI_ROW32) {
-        // fp32 records: one 256-bit load per 32-byte row
-        constexpr int kRows = (C + 7) / 8;
-        float rec[OPL][kRows * 8];
-#pragma unroll
-        for (int k = 0; k < OPL; ++k) {
-          const int kb = sub * OPL + k;  // byte of the word
-          const uint32_t idx = ((lo >> (8 * kb)) & 0xffu) | (DI > 8 ? ((hi >> (8 * kb)) & 0xffu) << 8 : 0u);
-          const float* r = reinterpret_cast<const float*>(tab) + (size_t)idx * CP;
-#pragma unroll
-          for (int i = 0; i < kRows; ++i) {
-            float* d = rec[k] + 8 * i;
-            asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                         : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3]), "=f"(d[4]), "=f"(d[5]), "=f"(d[6]), "=f"(d[7])
-                         : "l"(r + 8 * i));
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < OPL; ++k)
-#pragma unroll
-          for (int c = 0; c < C; ++c) acc[k][c] += (double)rec[k][c];
-      } else {
+      {
         constexpr int kRows = CP * (int)sizeof(leaf_t) / 16;
         uint4 rec[OPL][kRows];
 #pragma unroll
