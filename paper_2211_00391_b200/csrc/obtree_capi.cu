@@ -1060,12 +1060,18 @@ size_t wide_smem(const obt_model* m, int ts, int ns, int dsrc) {
          (((size_t)m->n_features * obt::kWideTile + 15) & ~(size_t)15);
 }
 // Ring depths: 3 table stages (2 if that is all that fits) and as many descriptor /
-// panel slots as fit, up to 12 (the index warps' lead over the fold).
+// panel slots as fit, up to 12 (the index warps' lead over the fold); then more table
+// stages while they fit, up to 8: small chunks (config 2: 4 KB of tables folded in
+// ~0.3 us) need more than two chunks of lead to cover a bulk copy's L2 latency.
 bool wide_rings(const obt_model* m, int dsrc, int* ts, int* ns) {
   for (int t = 3; t >= 2; --t) {
     int n = 12;
     while (n >= 4 && wide_smem(m, t, n, dsrc) > (size_t)m->smem_optin) --n;
-    if (n >= 4) { *ts = t; *ns = n; return true; }
+    if (n >= 4) {
+      while (t < obt::kWideMaxTStages && wide_smem(m, t + 1, n, dsrc) <= (size_t)m->smem_optin) ++t;
+      *ts = t; *ns = n;
+      return true;
+    }
   }
   return false;
 }
@@ -1151,7 +1157,7 @@ int launch_wide(obt_model* m, const uint8_t* q, int64_t n, double* out, cudaStre
   p.bias = m->bias;
   CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, m->smem_optin));
   const dim3 grid((unsigned)std::min<int64_t>(p.n_tiles, m->sm_count)),
-      block(32 * (1 + obt::kWideIndexWarps + obt::kWideFoldWarps));
+      block(32 * (3 + obt::kWideIndexWarps + obt::kWideFoldWarps));
   // one launch (descriptor ring), or one per parameter bank of descriptors, the fold
   // carried through `out` between launches
   const int per = ds ? obt::wide_bank_chunks(m->depth_inst) : std::max(w->n_chunks, 1);

@@ -7,9 +7,11 @@
 // of work, too few to cover shared-memory latency; K2w splits the work by role instead
 // of by object:
 //
-//   producer warp   lane 0 streams tree chunks (descriptors + leaf tables) into an
-//                   S-stage ring, lane 1 streams the CTA's bucket tiles (persistent
-//                   CTA: one per SM, looping over tiles)
+//   producer warps  three one-lane roles in three warps (three lanes of one warp, each in
+//                   its own barrier wait, delayed each other's copies: config 4 apply 47.9
+//                   -> 45.3 ms when split): chunk descriptors into an NS-slot ring, leaf
+//                   tables into a TS-stage ring, the CTA's bucket tiles (persistent CTA:
+//                   one per SM, looping over tiles)
 //   index warps     NIDX warps share each chunk's 4-tree groups; a lane builds the packed
 //                   leaf indices of bucket words l and l + 32 (8 objects, SWAR: per depth
 //                   one LDS per word, one add carrying [q > ordinal] into bit 7 of each
@@ -119,7 +121,7 @@ struct RingPos {
 };
 
 template <int DI, int CMP, int LEAF, int NIDX, int DSRC>
-__global__ void __launch_bounds__(32 * (1 + NIDX + kWideFoldWarps), 1) apply_wide_kernel(const __grid_constant__ WideArgs<DSRC> args) {
+__global__ void __launch_bounds__(32 * (3 + NIDX + kWideFoldWarps), 1) apply_wide_kernel(const __grid_constant__ WideArgs<DSRC> args) {
   const WideParams& p = args.p;
   static_assert(DI >= 1 && DI <= 8, "K2w: one index byte per object");
   using LT = LeafT<LEAF>;
@@ -165,8 +167,12 @@ __global__ void __launch_bounds__(32 * (1 + NIDX + kWideFoldWarps), 1) apply_wid
   const int64_t n_my_tiles = p.n_tiles > blockIdx.x ? (p.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int nc = p.n_chunks;
 
-  if (warp == 0) {
-    if (lane == 0 && DSRC == 0) {
+  // producer roles, one per warp (lanes of one warp in three different waits serialise
+  // each other's issue): warp 0 descriptors, the last two warps bucket tiles and tables
+  const int role = warp == 0 ? 0 : warp == 1 + NIDX + kWideFoldWarps ? 1 : warp == 2 + NIDX + kWideFoldWarps ? 2 : -1;
+  if (role >= 0) {
+    if (lane != 0) return;
+    if (role == 0 && DSRC == 0) {
       // descriptors, NS chunks ahead of the fold: index warps run ahead of the fold by
       // up to NS chunks, decoupled from the (larger) table ring
       RingPos r;
@@ -179,7 +185,7 @@ __global__ void __launch_bounds__(32 * (1 + NIDX + kWideFoldWarps), 1) apply_wid
           r.next(NS);
         }
       }
-    } else if (lane == 1) {
+    } else if (role == 1) {
       // bucket tiles: the next one as soon as the index warps release the current one
       for (int64_t i = 0; i < n_my_tiles; ++i) {
         const int64_t tile = blockIdx.x + i * gridDim.x;
@@ -188,7 +194,7 @@ __global__ void __launch_bounds__(32 * (1 + NIDX + kWideFoldWarps), 1) apply_wid
         bulk_g2s_split(qtile, p.q + tile * (int64_t)p.q_tile_bytes, p.q_tile_bytes, tile_full);
         if (i + 1 < n_my_tiles) bulk_prefetch_l2(p.q + (tile + gridDim.x) * (int64_t)p.q_tile_bytes, p.q_tile_bytes);
       }
-    } else if (lane == 2) {
+    } else if (role == 2) {
       // leaf tables, TS chunks ahead of the fold
       RingPos r;
       for (int64_t i = 0; i < n_my_tiles; ++i) {
