@@ -783,6 +783,9 @@ EncodeTiledFn encode_tiled() {
   return fn;
 }
 
+#ifndef OBT_QUANT_RB
+#define OBT_QUANT_RB 8
+#endif
 #ifndef OBT_TMA_L2
 #define OBT_TMA_L2 128  // measured: 256 B reads 1.2 GB for 0.8 GB of features, 128 B 0.99 GB, same time
 #endif
@@ -870,7 +873,15 @@ int launch_quantize(const obt_model* m, const float* x, int64_t n, int layout, u
       const size_t smem = use_lut ? obt::kQTSmemFixed + lut_fixed + (size_t)std::min(fc, F) * (lt.cells + lt.rec_stride)
                                   : obt::kQTSmemFixed + (bt.levels > 0 ? (size_t)std::min(fc, F) * bt.pitch * 4 : 16);
       CUDA_TRY(cudaFuncSetAttribute(tfn, cudaFuncAttributeMaxDynamicSharedMemorySize, m->smem_optin));
-      const dim3 grid(blocks * (unsigned)((F + fc - 1) / fc));
+      // K1L: up to OBT_QUANT_RB row blocks per CTA (the chunk's tables staged once for
+      // all of them) while the grid keeps >= 8 waves of 2 CTAs per SM.  Config 4 (1.5 KB
+      // of tables per feature): 1 / 4 / 8 blocks 4.57 / 3.85 / 3.81 ms; config 2 keeps 1
+      // (fewer, longer CTAs measured 0.243 vs 0.204 ms there)
+      const unsigned n_fch = (unsigned)((F + fc - 1) / fc);
+      int rb = use_lut ? OBT_QUANT_RB : 1;
+      while (rb > 1 && (blocks + rb - 1) / rb * n_fch < 16u * (unsigned)m->sm_count) --rb;
+      p.row_blocks = rb;
+      const dim3 grid((blocks + rb - 1) / rb * n_fch);
       tfn<<<grid, obt::kQTThreads, smem, stream>>>(map, p);
       ++g_launches;
       CUDA_TRY(cudaGetLastError());

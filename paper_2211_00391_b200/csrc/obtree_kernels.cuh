@@ -204,6 +204,7 @@ struct QuantizeParams {
   const unsigned char* lrec;
   int32_t lrec_stride;
   int32_t chunk_inner;  // grid order: feature chunk fastest (1) or row block fastest (0)
+  int32_t row_blocks;   // K1L: consecutive 1024-row blocks per CTA (the chunk's tables staged once)
 };
 
 constexpr int kQuantObjects = 128;    // tile quantum: a quantize warp's 128 objects never straddle tiles
@@ -649,28 +650,52 @@ __global__ void __launch_bounds__(kQTThreads, 2) quantize_lut_kernel(const __gri
   luts += (256u - (smem_u32(luts) & 255u)) & 255u;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int fc = p.chunk_features;
-  // grid.x = row blocks x feature chunks.  chunk_inner: the chunk varies fastest, so the
-  // chunks of one row block run side by side and the L2 lines their row segments share
-  // are read from HBM once (K1L at cfg2: 1.08 -> 0.96 GB, 0.217 -> 0.198 ms); otherwise
-  // the row block varies fastest (the Eytzinger kernels measured 1-4% faster that way)
+  // grid.x = row-block groups x feature chunks.  chunk_inner: the chunk varies fastest, so
+  // the chunks of one row block run side by side and the L2 lines their row segments
+  // share are read from HBM once (K1L at cfg2: 1.08 -> 0.96 GB, 0.217 -> 0.198 ms);
+  // otherwise the row block varies fastest (the Eytzinger kernels measured 1-4% faster
+  // that way).  A CTA quantizes row_blocks consecutive 1024-row blocks of its chunk, so
+  // the chunk's tables (config 4: 32 features x 1.5 KB, as many bytes as 1.5 row blocks
+  // of the chunk's features) are staged once per row_blocks blocks.
   const int n_fch = (p.n_features + fc - 1) / fc;
-  const unsigned n_rb = gridDim.x / (unsigned)n_fch;
-  const int f0 = (int)(p.chunk_inner ? blockIdx.x % (unsigned)n_fch : blockIdx.x / n_rb) * fc;
-  const int64_t rblock = (int64_t)(p.chunk_inner ? blockIdx.x / (unsigned)n_fch : blockIdx.x % n_rb);
+  const unsigned n_rg = gridDim.x / (unsigned)n_fch;
+  const int f0 = (int)(p.chunk_inner ? blockIdx.x % (unsigned)n_fch : blockIdx.x / n_rg) * fc;
+  const int64_t rgroup = (int64_t)(p.chunk_inner ? blockIdx.x / (unsigned)n_fch : blockIdx.x % n_rg);
   const int nf = min(fc, p.n_features - f0);
   unsigned char* recs = luts + (size_t)nf * CELLS;  // this chunk's nf features (the host sizes min(fc, F))
   const int rs = p.lrec_stride;
   const int n_steps = (nf + kQuantStep - 1) / kQuantStep;
-  const int64_t row0 = rblock * kQuantBlock;
-  const int64_t blocks_left = (p.n_slots - row0 + 127) / 128;
-  const int active = blocks_left < kQTConsumerWarps ? (int)blocks_left : kQTConsumerWarps;
+  const int64_t row_first = rgroup * p.row_blocks * kQuantBlock;
+  const int64_t rows_left = p.n_slots - row_first;
+  const int64_t rb_left = (rows_left + kQuantBlock - 1) / kQuantBlock;
+  const int n_rb = rb_left < p.row_blocks ? (int)rb_left : p.row_blocks;
+  const int total = n_rb * n_steps;  // pipeline steps: row block r, feature step st
   if (threadIdx.x == 0) {
     for (int s = 0; s < kQTStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 32 * active);
+      mbar_init(&empty[s], 32 * kQTConsumerWarps);
     }
     fence_mbar_init();
   }
+  __syncthreads();
+  auto issue = [&](int it) {  // producer: row stage `it` (row block it / n_steps, step it % n_steps)
+    const int s = it % kQTStages;
+    const int rb = it / n_steps, st = it - rb * n_steps;
+    const int64_t row0 = row_first + (int64_t)rb * kQuantBlock;
+    if (it >= kQTStages) mbar_wait(&empty[s], (uint32_t)(it / kQTStages - 1) & 1u);
+    mbar_expect_tx(&full[s], kQTStageBytes);
+    unsigned char* dst = ring + (size_t)s * kQTStageBytes;
+#pragma unroll
+    for (int b = 0; b < kQuantBlock / kQTBoxRows; ++b)
+      tma_load_2d(dst + b * kQTBoxRows * kQuantStep * 4, &rows, f0 + st * kQuantStep, (int)(row0 + b * kQTBoxRows),
+                  &full[s]);
+  };
+  // the first row stages land while every thread copies the chunk's tables (cfg4 K1L
+  // 4.81 -> 4.57 ms; plain coalesced loads: two bulk copies measured slower, cfg2 0.215
+  // vs 0.200 ms)
+  const int head = total < kQTStages ? total : kQTStages;
+  if (threadIdx.x == 0)
+    for (int it = 0; it < head; ++it) issue(it);
   {
     const uint4* src = reinterpret_cast<const uint4*>(p.lut + (size_t)f0 * CELLS);
     uint4* dst = reinterpret_cast<uint4*>(luts);
@@ -682,42 +707,38 @@ __global__ void __launch_bounds__(kQTThreads, 2) quantize_lut_kernel(const __gri
   __syncthreads();
 
   if (warp == 0) {
-    if (lane == 0) {
-      for (int st = 0; st < n_steps; ++st) {
-        const int s = st % kQTStages;
-        if (st >= kQTStages) mbar_wait(&empty[s], (uint32_t)(st / kQTStages - 1) & 1u);
-        mbar_expect_tx(&full[s], kQTStageBytes);
-        unsigned char* dst = ring + (size_t)s * kQTStageBytes;
-#pragma unroll
-        for (int b = 0; b < kQuantBlock / kQTBoxRows; ++b)
-          tma_load_2d(dst + b * kQTBoxRows * kQuantStep * 4, &rows, f0 + st * kQuantStep,
-                      (int)(row0 + b * kQTBoxRows), &full[s]);
-      }
-    }
+    if (lane == 0)
+      for (int it = head; it < total; ++it) issue(it);
     return;
   }
   const int cw = warp - 1;
-  if (cw >= active) return;
-  const int64_t base = row0 + cw * 128;
-  const bool full_objs = base + lane + 96 < p.n;
   const uint32_t luts_s = smem_u32(luts), recs_s = smem_u32(recs);
-  for (int st = 0; st < n_steps; ++st) {
-    const int s = st % kQTStages;
-    mbar_wait_warp(&full[s], (uint32_t)(st / kQTStages) & 1u);
-    const unsigned char* stage = ring + (size_t)s * kQTStageBytes;
-    float v[kQuantStep][4];
+  int s = 0;
+  uint32_t phase = 0;
+  for (int rb = 0; rb < n_rb; ++rb) {
+    const int64_t base = row_first + (int64_t)rb * kQuantBlock + cw * 128;
+    const bool live = base < p.n_slots;  // warp-uniform: rows past the grid's slots are skipped
+    const bool full_objs = base + lane + 96 < p.n;
+    for (int st = 0; st < n_steps; ++st) {
+      mbar_wait_warp(&full[s], phase);
+      const unsigned char* stage = ring + (size_t)s * kQTStageBytes;
+      float v[kQuantStep][4];
+      if (live) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int r = cw * 128 + lane + 32 * k;
-      const unsigned char* rp = stage + 32 * r;
-      const uint32_t sw = (uint32_t)((r >> 2) & 1) * 16u;
-      const float4 a = *reinterpret_cast<const float4*>(rp + sw);
-      const float4 b = *reinterpret_cast<const float4*>(rp + (16u ^ sw));
-      v[0][k] = a.x; v[1][k] = a.y; v[2][k] = a.z; v[3][k] = a.w;
-      v[4][k] = b.x; v[5][k] = b.y; v[6][k] = b.z; v[7][k] = b.w;
+        for (int k = 0; k < 4; ++k) {
+          const int r = cw * 128 + lane + 32 * k;
+          const unsigned char* rp = stage + 32 * r;
+          const uint32_t sw = (uint32_t)((r >> 2) & 1) * 16u;
+          const float4 a = *reinterpret_cast<const float4*>(rp + sw);
+          const float4 b = *reinterpret_cast<const float4*>(rp + (16u ^ sw));
+          v[0][k] = a.x; v[1][k] = a.y; v[2][k] = a.z; v[3][k] = a.w;
+          v[4][k] = b.x; v[5][k] = b.y; v[6][k] = b.z; v[7][k] = b.w;
+        }
+      }
+      mbar_arrive(&empty[s]);
+      if (++s == kQTStages) { s = 0; phase ^= 1u; }
+      if (live) lut_step<KMAX, CELLS>(p, luts_s, recs, recs_s, v, f0, st * kQuantStep, nf, base, lane, full_objs);
     }
-    mbar_arrive(&empty[s]);
-    lut_step<KMAX, CELLS>(p, luts_s, recs, recs_s, v, f0, st * kQuantStep, nf, base, lane, full_objs);
   }
 }
 

@@ -952,6 +952,23 @@ def test_large_feature_count_single_output(F, D, B):
         assert np.array_equal(ev.predict_device(xt, layout=obt.Layout.FEATURE_MAJOR).cpu().numpy(), want)
 
 
+@pytest.mark.parametrize("F,n", [(500, 620_001), (2000, 150_001)])
+def test_cell_table_quantize_row_block_groups(paths, F, n):
+    """K1L quantizing several consecutive 1024-row blocks per CTA with the chunk's tables
+    staged once (F = 500: 4 blocks per CTA over 16 feature chunks; F = 2,000: 5 blocks
+    over ~84 chunks), the last group partial: every row's prediction equals the oracle
+    bit for bit (a 300-tree model reads most features of every chunk)."""
+    paths(quant_lut=1)
+    model = _model(F, 128, 300, 6, seed=F)
+    x = _features(model, n, seed=F + 1)
+    ev = obt.Evaluator(model, device=0)
+    assert ev.quantize_kernel()[0].startswith("cells")
+    oracle.set_threads(oracle.host_cores())
+    want = oracle.evaluate_scalar(oracle.flatten(model), x)
+    got = ev.predict_device(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.array_equal(got, want), int(np.count_nonzero(got != want))
+
+
 def test_large_feature_count_binary64_leaves():
     """Leaves that are not binary32-exact keep binary64 records on the record path."""
     base = _model(3000, 32, 30, 6, seed=11)
