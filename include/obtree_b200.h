@@ -139,6 +139,31 @@ int obt_predict_dev(const obt_model* model, const float* x_dev, int64_t n_object
 int obt_predict_host(const obt_model* model, const float* x_host, int64_t n_objects,
                      int32_t layout, double* out_host, void* stream);
 
+/* One call over several devices of this process (the reference's
+ * Evaluator.predict, evaluate.py:268-300, has one CPU path and no counterpart).  `shards`
+ * holds n_shards (1..16) model handles, normally one per GPU (handles may share a device).
+ *   OBT_SHARD_OBJECTS  every handle is the whole model; shard s evaluates a contiguous
+ *                      range of objects (256-object quanta) on its device from its own host
+ *                      thread through the obt_predict_host pipeline.  No data crosses
+ *                      between devices; results are bit-identical to one device
+ *                      (predictions depend only on their own row, oracle.py:42-51).
+ *                      scale / bias are ignored (each handle carries the model's own).
+ *   OBT_SHARD_TREES    handle s holds trees [t_s, t_{s+1}) as a raw partial-sum model
+ *                      (scale 1, bias 0); every device evaluates every object against its
+ *                      trees, the binary64 partial sums are copied to shard 0's device
+ *                      (peer copies: NVLink between the GPUs of one box), added in shard
+ *                      order and finalized as sum * scale + bias with two roundings.  This
+ *                      reassociates the reference's tree-order fold (~1e-16 relative of the
+ *                      partial magnitudes for binary64 leaves, ~1e-7 for the binary16 family).
+ * x_host float32 [n][F] or [F][n]; out_host float64 [n][C]; returns when out_host is valid.
+ * (The one-process-per-GPU form of both modes, with an NCCL all_reduce for the tree
+ * shards, lives in the Python sharding module over torch.distributed.) */
+#define OBT_SHARD_OBJECTS 0
+#define OBT_SHARD_TREES 1
+int obt_predict_sharded(const obt_model* const* shards, int32_t n_shards, int32_t mode,
+                        const float* x_host, int64_t n_objects, int32_t layout, double scale,
+                        double bias, double* out_host);
+
 /* Stage 1 alone -- quantize_block (quantize.py:136-172) over the whole batch:
  * buckets_dev uint8 [F][n], bucket = #{k : x > border_k}, NaN -> 0. */
 int obt_quantize_dev(const obt_model* model, const float* x_dev, int64_t n_objects,

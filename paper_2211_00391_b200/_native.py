@@ -23,6 +23,8 @@ OBT_E_NOMEM = -4
 
 LAYOUT_OBJECT_MAJOR = 0
 LAYOUT_FEATURE_MAJOR = 1
+SHARD_OBJECTS = 0
+SHARD_TREES = 1
 PRECISION_BINARY64 = 0
 PRECISION_BINARY16 = 1
 
@@ -38,6 +40,7 @@ EXPORTED_SYMBOLS = (
     "obt_workspace_size",
     "obt_predict_dev",
     "obt_predict_host",
+    "obt_predict_sharded",
     "obt_quantize_dev",
     "obt_leaf_indices_dev",
     "obt_predict_dev_marked",
@@ -118,6 +121,8 @@ def load_library() -> ctypes.CDLL:
         "obt_workspace_size": (ctypes.c_int, [vp, i64, ctypes.POINTER(sz)]),
         "obt_predict_dev": (ctypes.c_int, [vp, vp, i64, i32, vp, vp, sz, vp]),
         "obt_predict_host": (ctypes.c_int, [vp, vp, i64, i32, vp, vp]),
+        "obt_predict_sharded": (ctypes.c_int, [ctypes.POINTER(vp), i32, i32, vp, i64, i32, ctypes.c_double,
+                                               ctypes.c_double, vp]),
         "obt_quantize_dev": (ctypes.c_int, [vp, vp, i64, i32, vp, vp]),
         "obt_leaf_indices_dev": (ctypes.c_int, [vp, vp, i64, i32, i32, i32, vp, vp]),
         "obt_predict_dev_marked": (ctypes.c_int, [vp, vp, i64, i32, vp, vp, sz, vp, vp, vp, vp]),

@@ -1840,18 +1840,14 @@ void parallel_copy(void* dst, const void* src, size_t bytes) {
 
 extern "C" {
 
-int obt_predict_host(const obt_model* mc, const float* x_host, int64_t n, int32_t layout, double* out_host,
-                     void* stream_v) {
+// obt_predict_host over objects [0, n) of a host matrix whose feature-major rows are `ld`
+// objects long (ld == n for a whole matrix; an object shard of a feature-major matrix
+// keeps the parent's row length).  Object-major input ignores ld.
+static int predict_host_impl(obt_model* m, const float* x_host, int64_t n, int64_t ld, int32_t layout,
+                             double* out_host, cudaStream_t stream) {
   g_launches = 0;
-  obt_model* m = const_cast<obt_model*>(mc);
-  if (!m) return fail(OBT_E_INVALID, "null model");
-  int rc = check_layout(layout);
-  if (rc != OBT_OK) return rc;
-  if (n < 0) return fail(OBT_E_INVALID, "negative object count");
-  if (n == 0) return OBT_OK;
-  if (!x_host || !out_host) return fail(OBT_E_INVALID, "null feature or output pointer");
+  int rc = OBT_OK;
   DeviceGuard guard(m->device);
-  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
   const int F = m->n_features, C = m->n_outputs;
   // Chunked pipeline: the features of chunk i+1 cross PCIe on a copy stream while chunk
   // i is quantized and applied on `stream`; each chunk's scores go back right behind its
@@ -1890,7 +1886,10 @@ int obt_predict_host(const obt_model* mc, const float* x_host, int64_t n, int32_
     };
     if (ok(pool_alloc(reinterpret_cast<void**>(&xd), (size_t)n * F * 4, m->device, stream), "feature buffer") &&
         ok(pool_alloc(reinterpret_cast<void**>(&od), (size_t)n * C * 8, m->device, stream), "score buffer") &&
-        ok(cudaMemcpyAsync(xd, x_host, (size_t)n * F * 4, cudaMemcpyHostToDevice, stream), "H2D")) {
+        ok(layout == OBT_LAYOUT_FEATURE_MAJOR && ld != n
+               ? cudaMemcpy2DAsync(xd, (size_t)n * 4, x_host, (size_t)ld * 4, (size_t)n * 4, F, cudaMemcpyHostToDevice, stream)
+               : cudaMemcpyAsync(xd, x_host, (size_t)n * F * 4, cudaMemcpyHostToDevice, stream),
+           "H2D")) {
       rc = predict_impl(m, xd, n, layout, od, nullptr, 0, 0, nullptr, 0, stream);
       if (rc == OBT_OK) ok(cudaMemcpyAsync(out_host, od, (size_t)n * C * 8, cudaMemcpyDeviceToHost, stream), "D2H");
     }
@@ -1979,7 +1978,7 @@ int obt_predict_host(const obt_model* mc, const float* x_host, int64_t n, int32_
     } else if (layout == OBT_LAYOUT_OBJECT_MAJOR) {
       cuda_ok(cudaMemcpyAsync(x_dev[b], x_host + o0 * F, (size_t)ni * F * 4, cudaMemcpyHostToDevice, copy), "H2D");
     } else {  // feature-major: ni columns of every feature row
-      cuda_ok(cudaMemcpy2DAsync(x_dev[b], (size_t)ni * 4, x_host + o0, (size_t)n * 4, (size_t)ni * 4, F,
+      cuda_ok(cudaMemcpy2DAsync(x_dev[b], (size_t)ni * 4, x_host + o0, (size_t)ld * 4, (size_t)ni * 4, F,
                                 cudaMemcpyHostToDevice, copy), "H2D");
     }
     cuda_ok(cudaEventRecord(copied[b], copy), "event record");
@@ -2013,6 +2012,222 @@ int obt_predict_host(const obt_model* mc, const float* x_host, int64_t n, int32_
   if (ready) cudaEventDestroy(ready);
   if (copy) cudaStreamDestroy(copy);
   return rc;
+}
+
+int obt_predict_host(const obt_model* mc, const float* x_host, int64_t n, int32_t layout, double* out_host,
+                     void* stream_v) {
+  g_launches = 0;
+  obt_model* m = const_cast<obt_model*>(mc);
+  if (!m) return fail(OBT_E_INVALID, "null model");
+  int rc = check_layout(layout);
+  if (rc != OBT_OK) return rc;
+  if (n < 0) return fail(OBT_E_INVALID, "negative object count");
+  if (n == 0) return OBT_OK;
+  if (!x_host || !out_host) return fail(OBT_E_INVALID, "null feature or output pointer");
+  return predict_host_impl(m, x_host, n, n, layout, out_host, static_cast<cudaStream_t>(stream_v));
+}
+
+}  // extern "C"
+
+namespace {
+
+constexpr int kMaxShards = 16;
+
+// Tree-sharded combine: the shards' raw partial sums added in shard order (binary64),
+// then the affine finalize with two roundings (evaluate.py:298-299).
+struct PartialSet {
+  const double* part[kMaxShards];
+};
+__global__ void fold_partials_kernel(PartialSet ps, int n_parts, int64_t count, double scale, double bias,
+                                     double* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+    double acc = ps.part[0][i];
+    for (int s = 1; s < n_parts; ++s) acc = __dadd_rn(acc, ps.part[s][i]);
+    out[i] = __dadd_rn(__dmul_rn(acc, scale), bias);
+  }
+}
+
+// Object shards: shard s evaluates a contiguous object range (256-object quanta, as the
+// Python ObjectShardedEvaluator) on its own device from its own host thread; every shard
+// runs the chunked host pipeline of obt_predict_host.  No data crosses between devices.
+int predict_sharded_objects(obt_model* const* shards, int n_shards, const float* x_host, int64_t n, int32_t layout,
+                            double* out_host) {
+  const int64_t units = (n + 255) / 256, base = units / n_shards, extra = units % n_shards;
+  std::vector<int64_t> begin(n_shards + 1, 0);
+  for (int s = 0; s < n_shards; ++s) begin[s + 1] = std::min(n, begin[s] + (base + (s < extra ? 1 : 0)) * 256);
+  std::vector<int> rcs(n_shards, OBT_OK), launches(n_shards, 0);
+  std::vector<std::string> errors(n_shards);
+  auto run = [&](int s) {
+    obt_model* m = shards[s];
+    const int64_t b = begin[s], cnt = begin[s + 1] - begin[s];
+    if (cnt == 0) return;
+    DeviceGuard guard(m->device);
+    cudaStream_t stream = nullptr;
+    if (cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking) != cudaSuccess) {
+      rcs[s] = OBT_E_CUDA;
+      errors[s] = "shard stream creation failed";
+      cudaGetLastError();
+      return;
+    }
+    const float* xs = layout == OBT_LAYOUT_OBJECT_MAJOR ? x_host + b * m->n_features : x_host + b;
+    rcs[s] = predict_host_impl(m, xs, cnt, n, layout, out_host + b * m->n_outputs, stream);
+    if (rcs[s] != OBT_OK) errors[s] = g_error;
+    launches[s] = g_launches;
+    cudaStreamDestroy(stream);
+  };
+  // this thread runs shard 0 and any shard no thread could be made for
+  std::vector<std::thread> th;
+  try {
+    for (int s = 1; s < n_shards; ++s) th.emplace_back(run, s);
+  } catch (...) {
+  }
+  run(0);
+  for (int s = (int)th.size() + 1; s < n_shards; ++s) run(s);
+  for (auto& t : th) t.join();
+  int total = 0;
+  for (int s = 0; s < n_shards; ++s) {
+    total += launches[s];
+    if (rcs[s] != OBT_OK) return fail(rcs[s], "shard %d: %s", s, errors[s].c_str());
+  }
+  g_launches = total;
+  return OBT_OK;
+}
+
+// Tree shards: shard s holds trees [t_s, t_{s+1}) as a raw partial-sum model (scale 1,
+// bias 0) on its own device.  Per chunk of objects every shard receives the chunk's
+// features and evaluates its trees; the partial sums travel to shard 0's device with peer
+// copies (NVLink between the GPUs of one box), are added there in shard order and
+// finalized with the caller's scale and bias, and the scores go back to the host.  All
+// asynchronous: the shards' streams wait on each other through events only.
+int predict_sharded_trees(obt_model* const* shards, int n_shards, const float* x_host, int64_t n, int32_t layout,
+                          double scale, double bias, double* out_host) {
+  const int F = shards[0]->n_features, C = shards[0]->n_outputs;
+  int64_t rows = std::max<int64_t>(1024, ((int64_t)128 << 20) / ((int64_t)F * 4) / 1024 * 1024);
+  rows = std::min(rows, n);
+  const size_t x_bytes = (size_t)rows * F * 4, p_bytes = (size_t)rows * C * 8;
+  struct Shard {
+    cudaStream_t stream = nullptr;
+    float* x = nullptr;
+    double* part = nullptr;      // on the shard's device
+    double* gathered = nullptr;  // on shard 0's device (shards >= 1)
+    cudaEvent_t part_ready = nullptr, part_taken = nullptr;
+  };
+  std::vector<Shard> sh(n_shards);
+  double* out_dev = nullptr;
+  int rc = OBT_OK, launches = 0;
+  auto ok = [&](cudaError_t e, const char* what) {
+    if (e != cudaSuccess && rc == OBT_OK) rc = fail(OBT_E_CUDA, "%s failed: %s", what, cudaGetErrorString(e));
+    return rc == OBT_OK;
+  };
+  const int root = shards[0]->device;
+  for (int s = 0; s < n_shards && rc == OBT_OK; ++s) {
+    DeviceGuard guard(shards[s]->device);
+    ok(cudaStreamCreateWithFlags(&sh[s].stream, cudaStreamNonBlocking), "shard stream");
+    if (rc != OBT_OK) break;
+    ok(pool_alloc(reinterpret_cast<void**>(&sh[s].x), x_bytes, shards[s]->device, sh[s].stream), "feature buffer");
+    ok(pool_alloc(reinterpret_cast<void**>(&sh[s].part), p_bytes, shards[s]->device, sh[s].stream), "partial-sum buffer");
+    ok(cudaEventCreateWithFlags(&sh[s].part_ready, cudaEventDisableTiming), "event");
+  }
+  if (rc == OBT_OK) {
+    DeviceGuard guard(root);
+    ok(pool_alloc(reinterpret_cast<void**>(&out_dev), p_bytes, root, sh[0].stream), "score buffer");
+    for (int s = 1; s < n_shards && rc == OBT_OK; ++s) {
+      ok(pool_alloc(reinterpret_cast<void**>(&sh[s].gathered), p_bytes, root, sh[0].stream), "gather buffer");
+      ok(cudaEventCreateWithFlags(&sh[s].part_taken, cudaEventDisableTiming), "event");
+    }
+  }
+  for (int64_t o0 = 0; o0 < n && rc == OBT_OK; o0 += rows) {
+    const int64_t ni = std::min(rows, n - o0);
+    for (int s = 0; s < n_shards && rc == OBT_OK; ++s) {
+      DeviceGuard guard(shards[s]->device);
+      // the partial-sum buffer is free once shard 0 has taken the previous chunk's sums
+      // (shard 0's own buffer is read by the fold on the same stream)
+      if (s > 0 && o0 > 0) ok(cudaStreamWaitEvent(sh[s].stream, sh[s].part_taken, 0), "stream wait");
+      if (layout == OBT_LAYOUT_OBJECT_MAJOR) {
+        ok(cudaMemcpyAsync(sh[s].x, x_host + o0 * F, (size_t)ni * F * 4, cudaMemcpyHostToDevice, sh[s].stream), "H2D");
+      } else {
+        ok(cudaMemcpy2DAsync(sh[s].x, (size_t)ni * 4, x_host + o0, (size_t)n * 4, (size_t)ni * 4, F,
+                             cudaMemcpyHostToDevice, sh[s].stream), "H2D");
+      }
+      if (rc != OBT_OK) break;
+      rc = predict_impl(shards[s], sh[s].x, ni, layout, sh[s].part, nullptr, 0, 0, nullptr, 0, sh[s].stream);
+      launches += g_launches;
+      if (rc == OBT_OK) ok(cudaEventRecord(sh[s].part_ready, sh[s].stream), "event record");
+    }
+    if (rc != OBT_OK) break;
+    DeviceGuard guard(root);
+    PartialSet ps{};
+    ps.part[0] = sh[0].part;
+    for (int s = 1; s < n_shards && rc == OBT_OK; ++s) {
+      ok(cudaStreamWaitEvent(sh[0].stream, sh[s].part_ready, 0), "stream wait");
+      ok(cudaMemcpyPeerAsync(sh[s].gathered, root, sh[s].part, shards[s]->device, (size_t)ni * C * 8, sh[0].stream),
+         "peer copy");
+      ok(cudaEventRecord(sh[s].part_taken, sh[0].stream), "event record");
+      ps.part[s] = sh[s].gathered;
+    }
+    if (rc != OBT_OK) break;
+    const int64_t count = ni * C;
+    const int blocks = (int)std::min<int64_t>((count + 255) / 256, (int64_t)shards[0]->sm_count * 8);
+    fold_partials_kernel<<<blocks, 256, 0, sh[0].stream>>>(ps, n_shards, count, scale, bias, out_dev);
+    ok(cudaGetLastError(), "fold launch");
+    ++launches;
+    ok(cudaMemcpyAsync(out_host + o0 * C, out_dev, (size_t)count * 8, cudaMemcpyDeviceToHost, sh[0].stream), "D2H");
+  }
+  // drain every stream before the buffers go (shard 0 last: it consumes the others' sums)
+  for (int s = n_shards - 1; s >= 0; --s) {
+    if (!sh[s].stream) continue;
+    DeviceGuard guard(shards[s]->device);
+    const cudaError_t e = cudaStreamSynchronize(sh[s].stream);
+    if (e != cudaSuccess && rc == OBT_OK) rc = fail(OBT_E_CUDA, "stream synchronize failed: %s", cudaGetErrorString(e));
+  }
+  {
+    DeviceGuard guard(root);
+    if (out_dev) cudaFreeAsync(out_dev, sh[0].stream);
+    for (int s = 1; s < n_shards; ++s) {
+      if (sh[s].gathered) cudaFreeAsync(sh[s].gathered, sh[0].stream);
+      if (sh[s].part_taken) cudaEventDestroy(sh[s].part_taken);
+    }
+  }
+  for (int s = 0; s < n_shards; ++s) {
+    if (!sh[s].stream) continue;
+    DeviceGuard guard(shards[s]->device);
+    if (sh[s].x) cudaFreeAsync(sh[s].x, sh[s].stream);
+    if (sh[s].part) cudaFreeAsync(sh[s].part, sh[s].stream);
+    if (sh[s].part_ready) cudaEventDestroy(sh[s].part_ready);
+    cudaStreamSynchronize(sh[s].stream);
+    cudaStreamDestroy(sh[s].stream);
+  }
+  g_launches = launches;
+  return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int obt_predict_sharded(const obt_model* const* shards_c, int32_t n_shards, int32_t mode, const float* x_host,
+                        int64_t n, int32_t layout, double scale, double bias, double* out_host) {
+  g_launches = 0;
+  if (!shards_c || n_shards < 1 || n_shards > kMaxShards)
+    return fail(OBT_E_INVALID, "shard count must be 1..%d", kMaxShards);
+  if (mode != OBT_SHARD_OBJECTS && mode != OBT_SHARD_TREES) return fail(OBT_E_INVALID, "unknown shard mode %d", mode);
+  obt_model* const* shards = const_cast<obt_model* const*>(reinterpret_cast<const obt_model* const*>(shards_c));
+  for (int s = 0; s < n_shards; ++s) {
+    if (!shards[s]) return fail(OBT_E_INVALID, "null model (shard %d)", s);
+    if (shards[s]->n_features != shards[0]->n_features || shards[s]->n_outputs != shards[0]->n_outputs ||
+        shards[s]->precision != shards[0]->precision)
+      return fail(OBT_E_INVALID, "shard %d differs from shard 0 in features, outputs or leaf precision", s);
+    if (mode == OBT_SHARD_TREES && (shards[s]->scale != 1.0 || shards[s]->bias != 0.0))
+      return fail(OBT_E_INVALID, "tree shard %d must be a raw partial-sum model (scale 1, bias 0)", s);
+  }
+  int rc = check_layout(layout);
+  if (rc != OBT_OK) return rc;
+  if (n < 0) return fail(OBT_E_INVALID, "negative object count");
+  if (n == 0) return OBT_OK;
+  if (!x_host || !out_host) return fail(OBT_E_INVALID, "null feature or output pointer");
+  return mode == OBT_SHARD_OBJECTS ? predict_sharded_objects(shards, n_shards, x_host, n, layout, out_host)
+                                   : predict_sharded_trees(shards, n_shards, x_host, n, layout, scale, bias, out_host);
 }
 
 }  // extern "C"

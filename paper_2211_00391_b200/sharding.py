@@ -22,7 +22,12 @@ r = o * G_t + t evaluates object shard o against tree shard t and the G_t ranks 
 object shard o all_reduce their partials (one process group per object shard).
 G_t = 1 is object sharding, G_o = 1 tree sharding.
 
-Every class has a host path (``predict(FeatureMatrix)``, the reference's call) and a
+``LocalShardedEvaluator`` is the one-process form of object and tree sharding: one
+model handle per device of this process behind the C ABI's ``obt_predict_sharded`` (host
+threads per object shard; peer copies of the tree shards' partial sums to the first
+device, added there in shard order).  It needs no process group.
+
+Every distributed class has a host path (``predict(FeatureMatrix)``, the reference's call) and a
 device path (``predict_device(cuda tensor)``) whose collectives run on the tensors in
 HBM (NCCL) or, for gloo test runs, through host copies.
 """
@@ -303,3 +308,59 @@ class GridShardedEvaluator:
         """This rank's object shard (resident on its GPU) against its tree shard, reduced
         within the object shard's group and finalized: the shard's finished scores."""
         return self._trees.predict_device(x_local, layout, out=out, workspace=workspace)
+
+
+class LocalShardedEvaluator:
+    """One process, several GPUs, through ``obt_predict_sharded`` (include/obtree_b200.h).
+
+    ``mode="objects"``: the whole model on every device of ``devices``; a predict splits
+    the batch into contiguous object ranges (256-object quanta), one host thread and one
+    host->device pipeline per device, bit-identical to a single device.
+    ``mode="trees"``: device i holds trees ``tree_shard(T, i, len(devices))`` as a raw
+    partial-sum model; partial sums are peer-copied to ``devices[0]``, added in shard order
+    and finalized there (reassociates the fold, as ``TreeShardedEvaluator``).
+    ``devices`` may repeat a device (functional tests on a one-GPU box)."""
+
+    def __init__(self, model, devices, mode: str = "objects", config: Optional[EvalConfig] = None):
+        if mode not in ("objects", "trees"):
+            raise ValueError(f"unknown shard mode {mode!r}")
+        devices = [int(d) for d in devices]
+        if not 1 <= len(devices) <= 16:
+            raise ValueError("devices must name 1..16 GPUs")
+        self.model, self.mode, self.devices = model, mode, devices
+        multi = hasattr(model, "subset")
+        self.n_outputs = model.n_outputs if multi else 1
+
+        def make(sub, device):
+            if multi:
+                from .multiclass import MultiOutputEvaluator
+
+                return MultiOutputEvaluator(sub, device=device, config=config)
+            from .evaluate import Evaluator
+
+            return Evaluator(sub, config, device=device)
+
+        if mode == "objects":
+            self.tree_ranges = [(0, model.n_trees)] * len(devices)
+            self._evs = [make(model, d) for d in devices]
+        else:
+            self.tree_ranges = [tree_shard(model.n_trees, i, len(devices)) for i in range(len(devices))]
+            self._evs = [make(tree_submodel(model, b, e), d) for (b, e), d in zip(self.tree_ranges, devices)]
+        handles = [ev.handle if multi else ev._dev.handle for ev in self._evs]
+        import ctypes
+
+        self._handles = (ctypes.c_void_p * len(handles))(*[h.value for h in handles])
+
+    def predict(self, matrix: FeatureMatrix, out: Optional[np.ndarray] = None) -> np.ndarray:
+        from . import _checks, _native
+        from .matrix import layout_code
+
+        _checks.check_features(matrix.n_features, self.model.n_features)
+        out = _checks.host_out(out, matrix.n_objects, self.n_outputs)
+        if matrix.n_objects:
+            lib = _native.require_gpu()
+            code = _native.SHARD_OBJECTS if self.mode == "objects" else _native.SHARD_TREES
+            _native.check(lib.obt_predict_sharded(self._handles, len(self.devices), code, matrix.values.ctypes.data,
+                                                  matrix.n_objects, layout_code(matrix.layout),
+                                                  float(self.model.scale), float(self.model.bias), out.ctypes.data))
+        return out

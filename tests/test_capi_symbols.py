@@ -71,3 +71,15 @@ def test_no_environment_switches_in_the_library():
 
     for src in glob.glob(str(ROOT / "paper_2211_00391_b200" / "csrc" / "*")):
         assert "getenv(" not in Path(src).read_text(), src
+
+
+def test_sharded_entry_rejects_bad_arguments_without_gpu():
+    """obt_predict_sharded validates its arguments before touching a device."""
+    lib = _native.load_library()
+    none = (ctypes.c_void_p * 2)(None, None)
+    assert lib.obt_predict_sharded(none, 0, 0, None, 0, 0, 1.0, 0.0, None) == _native.OBT_E_INVALID
+    assert b"shard count" in lib.obt_last_error()
+    assert lib.obt_predict_sharded(none, 2, 7, None, 0, 0, 1.0, 0.0, None) == _native.OBT_E_INVALID
+    assert b"shard mode" in lib.obt_last_error()
+    assert lib.obt_predict_sharded(none, 2, _native.SHARD_TREES, None, 0, 0, 1.0, 0.0, None) == _native.OBT_E_INVALID
+    assert b"null model" in lib.obt_last_error()
