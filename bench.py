@@ -446,6 +446,21 @@ def fp16_report(model, x, p16, device: int) -> dict:
             "within_bound": bool(m.max_abs <= bound), "saturated_leaves": sat_count}
 
 
+def workload_config(spec, plan, world) -> dict:
+    """`config` of the JSON line: the workload and how it is partitioned -- the same dict
+    on both arms (ours and --impl reference), so the driver compares like with like.
+    What is specific to the GPU path (kernels chosen, per-GPU shares) goes in `device_path`."""
+    go, gt = plan.grid
+    per_gpu = plan.n
+    return {"workload": spec.name, "n_objects_total": plan.total_objects, "features": spec.n_features,
+            "borders": spec.borders, "trees": spec.n_trees, "depth": spec.depth, "outputs": spec.n_outputs,
+            "leaves": "fp16 (binary32 fold)" if spec.half_leaves else "fp32 values (binary64 fold)",
+            "l2": ("inputs larger than L2 (features 4NF bytes, buckets NF bytes > 126 MB)"
+                   if 4 * per_gpu * spec.n_features > 126e6 else
+                   "inputs L2-resident between steps (features 4NF bytes < 126 MB; a launch-bound size)"),
+            "parallelism": plan.parallelism(world), "shard": plan.shard}
+
+
 def run_reference(args, world, rank):
     """--impl reference: the CPU port of the reference algorithm, all host threads."""
     if rank != 0:
@@ -464,6 +479,7 @@ def run_reference(args, world, rank):
     else:
         model = synthetic.build_model(spec)
     fm = flat_model(model)
+    plan = Plan(args, spec, world, rank)
     oracle.set_threads(oracle.host_cores())  # torchrun exports OMP_NUM_THREADS=1; use every core
     prec = oracle.BINARY16 if spec.half_leaves else oracle.BINARY64
     n = min(args.ref_sample, spec.n_objects)
@@ -481,10 +497,11 @@ def run_reference(args, world, rank):
         "impl": "reference",
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True,
-        "scaling": "weak" if args.config in (1, 2, 3) else "strong",
-        "vs_baseline": None, "dtype": "f16/f32" if spec.half_leaves else "f64", "data": "synthetic",
-        "config": {"workload": spec.name, "n_objects_per_step": n, "features": spec.n_features,
-                   "borders": spec.borders, "trees": spec.n_trees, "depth": spec.depth},
+        "scaling": plan.scaling,
+        "vs_baseline": None, "dtype": "f16/f32" if spec.half_leaves else "f64",
+        "data": "synthetic (seeded; BASELINE names no dataset)",
+        "config": workload_config(spec, plan, world),
+        "sample_objects_per_step": n,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.max_threads(), "host_cpus": os.cpu_count(),
                          "kind": "port",
                          "sample": f"{n} objects per step drawn with the workload's generator ({spec.name}); the C "
@@ -778,19 +795,13 @@ def run_ours(args, world, rank, local):
         "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": plan.scaling, "vs_baseline": None,
         "dtype": "f16/f32" if spec.half_leaves else "f64",
         "data": "synthetic (seeded; BASELINE names no dataset)",
-        "config": {"workload": spec.name, "n_objects_total": plan.total_objects, "n_objects_per_gpu": N,
-                   "features": spec.n_features, "borders": spec.borders, "trees": spec.n_trees,
-                   "trees_per_gpu": te - tb, "depth": spec.depth, "outputs": spec.n_outputs,
-                   "leaves": "fp16 (binary32 fold)" if spec.half_leaves else "fp32 values (binary64 fold)",
-                   "leaf_storage_on_device": ev.leaf_storage,
-                   "quantize_search": quantize_search(ev, spec.n_features),
-                   **({"multi_apply": ev.apply_kernel()} if hasattr(ev, "apply_kernel") else {}),
-                   "l2": ("inputs larger than L2 (features 4NF bytes, buckets NF bytes > 126 MB)"
-                          if 4 * N * spec.n_features > 126e6 else
-                          "inputs L2-resident between steps (features 4NF bytes < 126 MB; a launch-bound size)"),
-                   "parallelism": plan.parallelism(world), "shard": plan.shard,
-                   "launch": "CUDA graph replay of one predict" if graph is not None else "stream launches",
-                   **({"path_options": dict(kv.split("=", 1) for kv in args.path)} if args.path else {})},
+        "config": workload_config(spec, plan, world),
+        "device_path": {"n_objects_per_gpu": N, "trees_per_gpu": te - tb,
+                        "leaf_storage_on_device": ev.leaf_storage,
+                        "quantize_search": quantize_search(ev, spec.n_features),
+                        **({"multi_apply": ev.apply_kernel()} if hasattr(ev, "apply_kernel") else {}),
+                        "launch": "CUDA graph replay of one predict" if graph is not None else "stream launches",
+                        **({"path_options": dict(kv.split("=", 1) for kv in args.path)} if args.path else {})},
         "verify": verify,
         "e2e": e2e,
         "e2e_pageable": e2e_pageable,
@@ -883,14 +894,15 @@ def main():
         args.warmup = 3
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(spawn_ranks(sys.argv[1:], args.gpus))
+    if args.impl == "reference":
+        # CPU only, rank 0 only: no process group (the other ranks exit 0 without work)
+        run_reference(args, int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")))
+        return
     world, rank, local = dist_setup()
     if args.gpus > 1 and world != args.gpus and rank == 0:
         print(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}; running {world} rank(s)", file=sys.stderr)
     try:
-        if args.impl == "reference":
-            run_reference(args, world, rank)
-        else:
-            run_ours(args, world, rank, local)
+        run_ours(args, world, rank, local)
     finally:
         if world > 1:
             import torch.distributed as dist
