@@ -111,6 +111,32 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// Consumer release of a buffer the producer refills with a bulk / tensor copy (async
+// proxy) after this thread read it with ordinary shared loads (generic proxy): the proxy
+// fence orders those reads before the refill.  Without it the arrive can overtake loads
+// still queued in the shared-memory pipe, and the copy engine then overwrites the stage
+// under them: K1L at F = 2,000 (a busy pipe: conflicted table lookups of the other warps)
+// quantized one warp's 128 objects of one 8-feature step from the NEXT step's rows in
+// ~20% of predicts (tools/debug/repro_buckets.py; 0 of 100 with the fence).
+__device__ __forceinline__ void mbar_release(uint64_t* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  mbar_arrive(bar);
+}
+
+// The same release without the fence, for K2w's fold warps, where a fence per chunk costs
+// too much (config 4 apply 44.7 -> 50.5 ms): the arrive's barrier address is made to depend
+// on `dep` (bar | (dep & zero), `zero` a kernel parameter that is 0), a value computed from
+// every load of the buffer -- the chunk's final sum -- so the arrive cannot issue before
+// all of them returned.
+__device__ __forceinline__ void mbar_arrive_after(uint64_t* bar, uint32_t dep, uint32_t zero) {
+  uint32_t a;
+  asm volatile("lop3.b32 %0, %1, %2, %3, 0xF8;" : "=r"(a) : "r"(smem_u32(bar)), "r"(dep), "r"(zero));
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ uint32_t dep_bits(double v) { return (uint32_t)__double2hiint(v); }
+__device__ __forceinline__ uint32_t dep_bits(float v) { return __float_as_uint(v); }
+
+
 // global -> shared bulk copy; bytes % 16 == 0, both addresses 16-byte aligned.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -570,7 +596,7 @@ __global__ void __launch_bounds__(kQTThreads, 2) quantize_tma_kernel(const __gri
       v[0][k] = a.x; v[1][k] = a.y; v[2][k] = a.z; v[3][k] = a.w;
       v[4][k] = b.x; v[5][k] = b.y; v[6][k] = b.z; v[7][k] = b.w;
     }
-    mbar_arrive(&empty[s]);  // values are in registers: the producer may refill the stage
+    mbar_release(&empty[s]);  // the rows were requested: the producer may refill the stage once they are read
     quantize_step<L, true>(p, ey, v, f0, st * kQuantStep, nf, base, lane, full_objs);
   }
 }
@@ -735,7 +761,7 @@ __global__ void __launch_bounds__(kQTThreads, 2) quantize_lut_kernel(const __gri
           v[4][k] = b.x; v[5][k] = b.y; v[6][k] = b.z; v[7][k] = b.w;
         }
       }
-      mbar_arrive(&empty[s]);
+      mbar_release(&empty[s]);
       if (++s == kQTStages) { s = 0; phase ^= 1u; }
       if (live) lut_step<KMAX, CELLS>(p, luts_s, recs, recs_s, v, f0, st * kQuantStep, nf, base, lane, full_objs);
     }
@@ -1192,7 +1218,7 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_kernel(const __grid
         }
       }
     }
-    mbar_arrive(&empty[s]);  // this thread is done reading stage s (no divergent branch)
+    mbar_release(&empty[s]);  // this thread is done reading stage s (no divergent branch)
   }
 
   if constexpr (!WRITE_IDX) {
@@ -1333,7 +1359,7 @@ __global__ void __launch_bounds__(kFanThreads, 1) apply_fan_kernel(const __grid_
         prow[(size_t)t * 128 + lane + 32 * k] = lds_leaf<LEAF>(tab + (idx << LT::kShift));
       }
     }
-    mbar_arrive(&sfree[s]);
+    mbar_release(&sfree[s]);
     mbar_arrive(&vfull[v]);
     // refill stage s with chunk c + S once every compute thread has read it
     if (cw == 0 && lane == 0 && c + S < n_chunks) {
@@ -1496,7 +1522,7 @@ __global__ void __launch_bounds__(kApplyMaxThreads, 1) apply_split_kernel(const 
         }
       }
     }
-    mbar_arrive(&empty[s]);
+    mbar_release(&empty[s]);
   }
 #pragma unroll
   for (int k = 0; k < kOPT; ++k) {
@@ -1832,7 +1858,9 @@ __global__ void __launch_bounds__(kStagedThreads, 1) apply_multi_staged_kernel(c
         if constexpr (C % 2) acc[k][C - 1] += __half2float(__ushort_as_half((unsigned short)(w[C / 2] & 0xffffu)));
       }
     }
-    mbar_arrive(&empty[s]);
+    // (releasing one tree later instead, behind the loop's back edge and without the fence,
+    // measured 270 vs 275 ms at config 5 but 14.2 vs 13.4 ms at the epsilon shape)
+    mbar_release(&empty[s]);
   }
 #pragma unroll
   for (int k = 0; k < 4; ++k) {

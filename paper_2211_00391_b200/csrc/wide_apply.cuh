@@ -60,6 +60,7 @@ struct WideParams {
   int32_t n_slots;           // descriptor + index-panel ring slots (<= kWideMaxSlots)
   int32_t chunk_begin;       // this launch folds chunks [chunk_begin, chunk_begin + n_chunks)
   int32_t first, last;       // start the fold at 0 / finalize into predictions (else carry in out)
+  uint32_t zero;             // 0 (opaque to the compiler: see mbar_arrive_after)
   double scale, bias;
 };
 
@@ -74,12 +75,22 @@ template <> struct WideArgs<0> { WideParams p; };
 template <> struct WideArgs<1> { WideParams p; uint32_t desc[kWideBankWords]; };
 static_assert(sizeof(WideArgs<1>) <= 32764, "kernel parameter space");
 
-// Warp-wide wait on the plain (potentially blocking) try_wait.  A suspend-time hint (a
+// Wait on the plain (potentially blocking) try_wait.  A suspend-time hint (a
 // TRYWAIT / NANOSLEEP.SYNCS / PHASECHK loop) measured slower at config 4 (48.9 vs 48.2
 // ms), and so did a nanosleep back-off in the fold warps' waits (200 ns: 47.74 vs 47.28).
 __device__ __forceinline__ void wide_wait(uint64_t* bar, uint32_t parity) {
-  while (!__all_sync(0xffffffffu, mbar_try(bar, parity))) {
-  }
+  // every lane retries on its own: two instructions per poll (try_wait, branch); the
+  // voted warp-uniform loop (three) measured 45.05 vs 44.72 ms at config 4, one polling
+  // lane joined by __syncwarp 89.6 ms
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WIDE_WAIT_RETRY:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra WIDE_WAIT_DONE;\n"
+      "bra WIDE_WAIT_RETRY;\n"
+      "WIDE_WAIT_DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
 }
 // Shared-memory layout (2048-byte aligned base):
 //   table ring           TS x kWideChunkTrees tables (each stride-aligned, so a gather
@@ -291,10 +302,12 @@ __global__ void __launch_bounds__(32 * (3 + NIDX + kWideFoldWarps), 1) apply_wid
                          "r"(o0[k]), "r"(o1[k]) : "memory");
         }
         rr -= kWideGroups;
+        // (the descriptor slot is refilled only after the fold's sfree arrive, and every
+        // descriptor and bucket word read here fed the panel stores above: none is in flight)
         mbar_arrive(&pfull[r.slot]);
         r.next(NS);
       }
-      mbar_arrive(tile_free);
+      mbar_release(tile_free);  // the bucket tile is refilled by a bulk copy
     }
     return;
   }
@@ -303,6 +316,14 @@ __global__ void __launch_bounds__(32 * (3 + NIDX + kWideFoldWarps), 1) apply_wid
   const int fw = warp - 1 - NIDX;
   const int ol = fw * 32 + lane;
   RingPos r, rt;
+  // Table release.  The copy engine refills a table stage once every fold thread has
+  // arrived on its tfree barrier, so a thread may arrive only after all its gathers from
+  // that stage returned (mbar_release explains what happens otherwise).  The arrive's
+  // address is made to depend on the chunk's final sum -- every gathered leaf went into
+  // it -- and is issued one chunk later, behind the next chunk's gathers, so the wait for
+  // the tail of the add chain overlaps their latency (arriving right behind the adds:
+  // 46.9 ms at config 4; a proxy fence per chunk: 50.5).
+  int pend = -1;  // table slot whose release awaits the sum of the chunk folded from it
   for (int64_t i = 0; i < n_my_tiles; ++i) {
     const int64_t tile = blockIdx.x + i * gridDim.x;
     const int64_t o = tile * kWideTile + ol;
@@ -327,14 +348,17 @@ __global__ void __launch_bounds__(32 * (3 + NIDX + kWideFoldWarps), 1) apply_wid
           v[g][j] = lds_leaf<LEAF, false>((((iwd[g] >> (8 * j)) << LT::kShift) & (0xffu << LT::kShift) | tables) +
                                           (uint32_t)(4 * g + j) * kStride);
       mbar_arrive(&sfree[r.slot]);
+      if (pend >= 0) mbar_arrive_after(&tfree[pend], dep_bits(acc), p.zero);  // acc: through the previous chunk
 #pragma unroll
       for (int g = 0; g < kWideGroups; ++g)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc += LT::widen(v[g][j]);
-      mbar_arrive(&tfree[rt.slot]);
+      pend = rt.slot;
       r.next(NS);
       rt.next(TS);
     }
+    if (pend >= 0) mbar_arrive_after(&tfree[pend], dep_bits(acc), p.zero);  // the tile's last chunk
+    pend = -1;
     // finalize: f64(acc) * scale + bias, two roundings (evaluate.py:298-299)
     if (o < p.n) p.out[o] = p.last ? __dadd_rn(__dmul_rn((double)acc, p.scale), p.bias) : (double)acc;
   }

@@ -1058,3 +1058,34 @@ def test_random_multi_output_fuzz(paths):
         ev = multiclass.MultiOutputEvaluator(model, config=cfg)
         got = ev.predict(obt.FeatureMatrix(x, obt.Layout.OBJECT_MAJOR))
         assert np.array_equal(got, want.reshape(got.shape)), (case, C, D, F, B, n, half, ev.apply_kernel())
+
+
+def test_quantize_stage_release_is_ordered_before_the_refill(paths):
+    """Regression: K1L / K1t released a row stage with a plain mbarrier arrive right behind
+    the loads that read it; under a busy shared-memory pipe the arrive overtook loads still
+    queued and the tensor copy refilled the stage under them (F = 2,000: one warp's 128
+    objects of one 8-feature step quantized from the next step's rows in ~20% of predicts).
+    Repeated predicts with other work in between: the tiled bucket matrix K1L leaves in the
+    workspace must equal K1t's every time, and the predictions the oracle's."""
+    F, n = 2000, 150_001
+    model = _model(F, 128, 300, 6, seed=F)
+    x = _features(model, n, seed=F + 1)
+    ev = obt.Evaluator(model, device=0)
+    xd = torch.from_numpy(x).cuda()
+    nbytes = ev.workspace_bytes(n)
+    qbytes = -(-n // 2048) * 2048 * F  # the K5 record path's 2048-object bucket tiles
+    assert qbytes <= nbytes
+    paths(quant_lut=0)
+    ws_ref = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
+    want = ev.predict_device(xd, workspace=ws_ref).clone()
+    oracle.set_threads(oracle.host_cores())
+    assert np.array_equal(want.cpu().numpy(), oracle.evaluate_scalar(oracle.flatten(model), x))
+    paths(quant_lut=1)
+    assert ev.quantize_kernel()[0].startswith("cells")
+    for it in range(40):
+        junk = torch.empty(64 << 20, dtype=torch.uint8, device="cuda").random_()  # disturb timing, evict L2
+        ws = torch.full((nbytes,), 0xEE, dtype=torch.uint8, device="cuda")
+        got = ev.predict_device(xd, workspace=ws)
+        assert torch.equal(ws[:qbytes], ws_ref[:qbytes]), (it, int((ws[:qbytes] != ws_ref[:qbytes]).sum()))
+        assert torch.equal(got, want), it
+        del junk
