@@ -14,7 +14,8 @@ timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --mast
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/s6d/launches_cfg4.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/s6d/ncu_launches_cfg4.log 2>&1; echo "launches cfg4 rc=$?"
 SKIP=0 timeout 900 bash tools/prof.sh w4 'apply_wide' --config 4 > gpurun_out/s6d/prof_w4.txt 2>&1
 SKIP=1 timeout 900 bash tools/prof.sh q4 'quantize_lut' --config 4 > gpurun_out/s6d/prof_q4.txt 2>&1
-for r in w4 q4; do cp gpurun_out/${r}_by_opcode.txt gpurun_out/s6d/; python tools/ncu_summary.py $NCU_DIR/$r.ncu-rep --json gpurun_out/s6d/ncu_$r.json > /dev/null 2>&1; done
+SKIP=1 timeout 1200 bash tools/prof.sh k5 "apply_multi_staged" --config 5 --objects 4000000 > gpurun_out/s6d/prof_k5.txt 2>&1
+for r in w4 q4 k5; do cp gpurun_out/${r}_by_opcode.txt gpurun_out/s6d/; python tools/ncu_summary.py $NCU_DIR/$r.ncu-rep --json gpurun_out/s6d/ncu_$r.json > /dev/null 2>&1; done
 for f in gpurun_out/s6d/bench_*.json; do python -c "
 import json;d=json.loads(open('$f').read().strip().splitlines()[-1])
 print('$f', d.get('ms_per_step'), d.get('value'), (d.get('e2e') or {}).get('value'), (d.get('roofline') or {}).get('frac'), (d.get('roofline_step') or {}).get('frac'), (d.get('verify') or {}).get('bit_exact'), (d.get('kernels') or {}))"; done
