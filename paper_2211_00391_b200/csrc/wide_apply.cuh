@@ -12,22 +12,24 @@
 //                   -> 45.3 ms when split): chunk descriptors into an NS-slot ring, leaf
 //                   tables into a TS-stage ring, the CTA's bucket tiles (persistent CTA:
 //                   one per SM, looping over tiles)
-//   index warps     NIDX warps share each chunk's 4-tree groups; a lane builds the packed
-//                   leaf indices of bucket words l and l + 32 (8 objects, SWAR: per depth
-//                   one LDS per word, one add carrying [q > ordinal] into bit 7 of each
-//                   byte, one shift-and-or) for the group's 4 trees, transposes the 4 x 4
-//                   index bytes of each word (8 PRMT) so that one word holds one object's
-//                   indices of the 4 trees, and stores those words to the chunk's index
-//                   panel [group][object] (32 consecutive words per store: conflict-free)
+//   index warps     NIDX warps share each chunk's 4-tree groups; the two halves of a warp
+//                   take two trees of the group each, over all 256 objects: a lane builds
+//                   the packed leaf indices of bucket words 4hl..4hl+3 (16 objects, SWAR:
+//                   per depth one LDS.128, per word one add carrying [q > ordinal] into bit
+//                   7 of each byte and one shift-and-or), so one descriptor load carries
+//                   two trees' splits (one address per half-warp); the halves swap two
+//                   words per tree (4 SHFL), each lane transposes the 4 x 4 index bytes of
+//                   its two words (12 PRMT) so that one word holds one object's indices of
+//                   the 4 trees, and stores them to the chunk's index panel [group][object]
 //   fold warps      kWideTile / 32 warps, lane = object: per 4-tree group one panel load,
 //                   four leaf gathers and four adds in tree order -- the reference's left
 //                   fold, binary64 (binary32 for the binary16 family) -- then the
 //                   two-rounding finalize and a coalesced store
 //
 // Shared-memory wavefronts per 128 object-trees at depth 8 (the resource that binds
-// this path on B200): 8 bucket words, ~10.5 leaf gathers (4 x ~2.6 with entropy-ordered
+// this path on B200): 8 bucket words, ~11 leaf gathers (4 x ~2.8 with entropy-ordered
 // levels, see obtree_capi.cu level_order), 1 panel store + 1 panel load, 2 descriptor
-// broadcasts, ~4 of TMA ring fill (1 KB tables over 256 objects).
+// broadcasts (4 before the tree split), 0.5 index swaps.
 #pragma once
 
 #include "obtree_kernels.cuh"
@@ -240,6 +242,85 @@ __global__ void __launch_bounds__(32 * (3 + NIDX + kWideFoldWarps), 1) apply_wid
         }
         const unsigned char* st = descs + (size_t)r.slot * kDescBytes;
         const uint32_t panel = smem_u32(panels + (size_t)r.slot * kPanelBytes) + 4u * obj0;
+        if constexpr (DSRC == 0) {
+          // Tree-split halves (config 4 apply 45.1 -> 43.9 ms against every lane taking all
+          // four trees of a group over 8 objects, the form the parameter-bank source keeps): lanes 0-15 take trees 4g, 4g+1 and lanes 16-31 trees 4g+2,
+          // 4g+3, each half over all 256 objects (lane hl: bucket words 4hl..4hl+3, one
+          // LDS.128 per depth).  One descriptor load now carries two trees' splits (one
+          // address per half-warp), so a group costs half the descriptor broadcasts, half the
+          // bucket loads and address adds; the halves then swap two words per tree (4 SHFL)
+          // so that every lane holds the four trees' indices of 8 objects, as before.
+          const int half = lane >> 4, hl = lane & 15;
+          const uint32_t qh = smem_u32(qtile) + 16u * hl;
+          const int w0i = 4 * hl + 2 * half;                       // first kept bucket word
+          const int objk = (w0i >> 5) * 128 + (w0i & 31);
+          const uint32_t panel_t = smem_u32(panels + (size_t)r.slot * kPanelBytes) + 4u * objk;
+          const uint32_t sel_lo = half ? 0x1054u : 0x5410u, sel_hi = half ? 0x3276u : 0x7632u;
+          for (; rr < kWideGroups; rr += NIDX) {
+            const int g = rr;
+            uint32_t ix[2][4];  // [local tree][word]
+#pragma unroll
+            for (int tl = 0; tl < 2; ++tl) {
+              const int t = 4 * g + 2 * half + tl;
+              uint32_t dw[2 * DI + 2];
+              const uint4* dsrc = reinterpret_cast<const uint4*>(st + (size_t)t * kWideDescBytes(DI));
+#pragma unroll
+              for (int v = 0; v < (DI + 1) / 2; ++v) {
+                const uint4 q4 = dsrc[v];
+                dw[4 * v + 0] = q4.x; dw[4 * v + 1] = q4.y; dw[4 * v + 2] = q4.z; dw[4 * v + 3] = q4.w;
+              }
+              uint32_t w[DI][4];
+#pragma unroll
+              for (int d = 0; d < DI; ++d) {
+                const uint32_t off = CMP == 7 ? dw[2 * d] : (dw[2 * d] >> 8);
+                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(w[d][0]), "=r"(w[d][1]), "=r"(w[d][2]), "=r"(w[d][3]) : "r"(qh + off));
+              }
+              uint32_t a[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+              for (int d = 0; d < DI; ++d) {
+#pragma unroll
+                for (int x = 0; x < 4; ++x) {
+                  uint32_t b;
+                  if constexpr (CMP == 7) {
+                    b = w[d][x] + dw[2 * d + 1];
+                  } else {
+                    const uint32_t k = __byte_perm(dw[2 * d], 0u, 0x0000u) & 0x7f7f7f7fu;
+                    b = maj3((w[d][x] & 0x7f7f7f7fu) + k, w[d][x], dw[2 * d + 1]);
+                  }
+                  a[x] = (a[x] >> 1) | (b & 0x80808080u);
+                }
+              }
+#pragma unroll
+              for (int x = 0; x < 4; ++x) ix[tl][x] = DI < 8 ? a[x] >> (8 - DI) : a[x];
+            }
+            // swap: a lane keeps words 2 half, 2 half + 1 and receives its partner's trees for them
+            uint32_t own[2][2], got[2][2];
+#pragma unroll
+            for (int tl = 0; tl < 2; ++tl)
+#pragma unroll
+              for (int x = 0; x < 2; ++x) {
+                own[tl][x] = half ? ix[tl][x + 2] : ix[tl][x];
+                got[tl][x] = __shfl_xor_sync(0xffffffffu, half ? ix[tl][x] : ix[tl][x + 2], 16);
+              }
+            // 4 x 4 byte transpose per kept word; the selectors put the received pair first
+            // (lanes 16-31: trees 4g, 4g+1 come from the partner) or second
+            uint32_t o[2][4];
+#pragma unroll
+            for (int x = 0; x < 2; ++x) {
+              const uint32_t own_lo = __byte_perm(own[0][x], own[1][x], 0x5140u), own_hi = __byte_perm(own[0][x], own[1][x], 0x7362u);
+              const uint32_t got_lo = __byte_perm(got[0][x], got[1][x], 0x5140u), got_hi = __byte_perm(got[0][x], got[1][x], 0x7362u);
+              o[x][0] = __byte_perm(own_lo, got_lo, sel_lo);
+              o[x][1] = __byte_perm(own_lo, got_lo, sel_hi);
+              o[x][2] = __byte_perm(own_hi, got_hi, sel_lo);
+              o[x][3] = __byte_perm(own_hi, got_hi, sel_hi);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(panel_t + (uint32_t)g * (kWideTile * 4) + 128u * k),
+                           "r"(o[0][k]), "r"(o[1][k]) : "memory");
+          }
+        } else
         for (; rr < kWideGroups; rr += NIDX) {
           const int g = rr;
           uint32_t i0[4], i1[4];  // packed indices of trees 4g..4g+3, words 2l and 2l + 1
