@@ -108,3 +108,21 @@ def test_bench_self_spawns_two_ranks(config, extra):
     assert line["verify"]["passed"] and line["verify"]["ranks"] == 2
     if config == 5:
         assert line["config"]["shard"] == "trees" and line["nccl_reduce_ms"] is not None
+
+
+def test_both_bench_arms_print_the_same_config():
+    """The reference arm (`--impl reference`) names the same workload and partitioning as
+    our arm, key for key, so the driver's ratio compares like with like."""
+    def line(extra):
+        cmd = [sys.executable, str(ROOT / "bench.py"), "--config", "1", "--steps", "3", "--warmup", "3", *extra]
+        res = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT, timeout=900)
+        assert res.returncode == 0, res.stderr[-4000:]
+        return json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][-1])
+
+    ours = line(["--no-e2e", "--no-cpu-baseline"])
+    ref = line(["--impl", "reference", "--no-reference-pkg"])
+    assert ref["impl"] == "reference" and "impl" not in ours
+    assert ours["config"] == ref["config"]
+    for key in ("metric", "unit", "higher_is_better", "scaling", "n_gpus", "steps", "warmup"):
+        assert ours[key] == ref[key], key
+    assert ref["e2e"]["h2d_bytes_per_step"] == 0 and ref["cpu_baseline"]["kind"] == "port"
