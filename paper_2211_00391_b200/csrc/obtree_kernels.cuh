@@ -117,7 +117,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // still queued in the shared-memory pipe, and the copy engine then overwrites the stage
 // under them: K1L at F = 2,000 (a busy pipe: conflicted table lookups of the other warps)
 // quantized one warp's 128 objects of one 8-feature step from the NEXT step's rows in
-// ~20% of predicts (tools/debug/repro_buckets.py; 0 of 100 with the fence).
+// ~20% of predicts (tests/stress/repro_buckets.py; 0 of 100 with the fence).
 __device__ __forceinline__ void mbar_release(uint64_t* bar) {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   mbar_arrive(bar);
