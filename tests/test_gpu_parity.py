@@ -1089,3 +1089,41 @@ def test_quantize_stage_release_is_ordered_before_the_refill(paths):
         assert torch.equal(ws[:qbytes], ws_ref[:qbytes]), (it, int((ws[:qbytes] != ws_ref[:qbytes]).sum()))
         assert torch.equal(got, want), it
         del junk
+
+
+@pytest.mark.parametrize("case", ["k2w", "k2w_fp16", "k2_chained", "k2s", "k5", "k5_fp16", "k5_one_output"])
+def test_repeated_predicts_are_bit_identical(paths, case):
+    """Every ring in these kernels is refilled by the copy engine behind the consumers'
+    release; a release that overtakes its loads shows up as a run that differs.  Repeated
+    predicts with other device work in between must reproduce the first run bit for bit
+    (tests/stress/ runs the same check longer and at the full BASELINE sizes)."""
+    from paper_2211_00391_b200 import multiclass
+
+    W = synthetic.WorkloadSpec
+    half = case.endswith("fp16")
+    n = 200_000
+    if case.startswith("k2w"):
+        spec = W("t", n, 500, 128, 800, 8, 0.02, cfg=4)
+    elif case == "k2_chained":
+        spec = W("t", n, 200, 64, 2000, 6, 0.05, cfg=2)
+    elif case == "k2s":
+        spec, n = W("t", 100_000, 500, 128, 400, 8, 0.02, cfg=4), 100_000
+        paths(wide=0)
+    elif case == "k5_one_output":
+        spec = W("t", n, 2000, 64, 400, 6, 0.05, cfg=6)
+    else:
+        spec, n = W("t", 100_000, 1000, 254, 100, 10, 0.01, n_outputs=10, cfg=5), 100_000
+    if spec.n_outputs > 1:
+        model = multiclass.from_arrays(synthetic.model_arrays(spec))
+        cfg = obt.EvalConfig(strategy=obt.LeafStrategy.NAIVE16) if half else None
+        ev = multiclass.MultiOutputEvaluator(model, device=0, config=cfg)
+    else:
+        model = synthetic.build_model(spec)
+        ev = obt.Evaluator(model, obt.EvalConfig(strategy=obt.LeafStrategy.NAIVE16 if half else obt.LeafStrategy.NAIVE),
+                           device=0)
+    x = synthetic.device_features(spec, n_objects=n, device="cuda")
+    first = ev.predict_device(x).clone()
+    for it in range(12):
+        junk = torch.empty(64 << 20, dtype=torch.uint8, device="cuda").random_()
+        assert torch.equal(ev.predict_device(x), first), (case, it)
+        del junk
